@@ -1,0 +1,128 @@
+"""Pins for the oracle's primitives (CPU only).  Each pin is fixed by mathematics or by
+a SPEC.md worked example (tests/golden/paper_values.json), never by the oracle itself."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+EPS = np.finfo(float).eps
+
+
+def test_forward_solve_spec_example():
+    ex = GOLD["spec_examples"]["forward_solve_unit"]
+    L = np.zeros((2, 2)); L[1, 0] = ex["L21"]
+    np.testing.assert_array_equal(oracle.forward_solve_unit(L, np.array(ex["b"])), ex["x"])
+
+
+def test_forward_solve_ignores_upper_and_diagonal():
+    rng = np.random.default_rng(5)
+    L = np.tril(rng.uniform(-1, 1, (6, 6)), -1)
+    b = rng.standard_normal(6)
+    junk = L + np.triu(rng.uniform(-9, 9, (6, 6)))  # diag/upper must be ignored (unit lower)
+    np.testing.assert_array_equal(oracle.forward_solve_unit(junk, b), oracle.forward_solve_unit(L, b))
+
+
+@pytest.mark.parametrize("order", [1, 8, 50, 200])
+def test_forward_solve_residual_bound(order):
+    # Higham (cited at P:496-503): forward substitution is backward stable, so
+    # |(I+L)x - b| <= gamma_order |I+L| |x| componentwise; checked with the dense product
+    rng = np.random.default_rng(order)
+    L = np.tril(rng.uniform(-1, 1, (order, order)), -1)
+    b = rng.standard_normal(order)
+    x = oracle.forward_solve_unit(L, b)
+    M = np.eye(order) + L
+    r = M @ x - b
+    gam = order * EPS / (1 - order * EPS)
+    assert np.all(np.abs(r) <= 2 * gam * (np.abs(M) @ np.abs(x)) + 1e-300)
+    # S:106 normwise form for the small-L regime the algorithm lives in (||L|| ~ eps kappa)
+    Ls = L * 1e-3
+    xs_ = oracle.forward_solve_unit(Ls, b)
+    rs = (np.eye(order) + Ls) @ xs_ - b
+    assert np.linalg.norm(rs) <= 100 * order * EPS * np.linalg.norm(b) * (1 + np.linalg.norm(Ls))
+    # and against LAPACK's triangular solve
+    import scipy.linalg as sl
+    ref = sl.solve_triangular(np.eye(order) + Ls, b, lower=True, unit_diagonal=True)
+    assert np.allclose(xs_, ref, rtol=1e-13, atol=1e-14 * np.abs(ref).max())
+
+
+def test_hessenberg_lsq_spec_examples():
+    for key in ("hessenberg_lsq_exact", "hessenberg_lsq_ls"):
+        ex = GOLD["spec_examples"][key]
+        y, res = oracle.hessenberg_lsq(np.array(ex["H"]), ex["rho"])
+        np.testing.assert_allclose(y, ex["y"], rtol=0, atol=1e-15)
+        assert abs(res - ex["residual"]) <= 1e-15
+
+
+@pytest.mark.parametrize("p", [1, 5, 10, 40])
+def test_hessenberg_lsq_vs_dense_lstsq(p):
+    # random (p+1) x p upper Hessenberg vs a dense least-squares solve
+    rng = np.random.default_rng(p)
+    H = np.triu(rng.standard_normal((p + 1, p)), -1)
+    rho = 2.5
+    y, res = oracle.hessenberg_lsq(H, rho)
+    e1 = np.zeros(p + 1); e1[0] = rho
+    ys, *_ = np.linalg.lstsq(H, e1, rcond=None)
+    assert np.allclose(y, ys, rtol=1e-10, atol=1e-12)
+    assert abs(res - np.linalg.norm(e1 - H @ ys)) <= 1e-12 * rho
+
+
+def test_dot_and_norm_examples():
+    for v, nrm in GOLD["spec_examples"]["norm2"]["cases"]:
+        v = np.array(v)
+        assert np.sqrt(oracle.dot(v, v)) == nrm
+    ex = GOLD["spec_examples"]["block_inner"]
+    Q = np.eye(3)[:, :2]
+    x = np.array(ex["x"])
+    out = oracle.block_dot(Q, x, np.zeros(3))
+    np.testing.assert_array_equal(out[:2], ex["result"])
+    assert out[2] == x @ x and out[5] == 0.0
+
+
+@pytest.mark.parametrize("block", [0, 7, 64, 1000])
+def test_dot_reduction_orders_agree(block):
+    rng = np.random.default_rng(11)
+    a, b = rng.standard_normal(5001), rng.standard_normal(5001)
+    exact = float(np.dot(a.astype(np.longdouble), b.astype(np.longdouble)))
+    bound = 5001 * EPS * np.dot(np.abs(a), np.abs(b))      # Higham's gamma_n bound
+    assert abs(oracle.dot(a, b, block) - exact) <= bound
+
+
+def test_dot_blocked_is_exactly_the_stated_order():
+    # blocked knob == sequential sum of sequential block sums, written out here in Python
+    rng = np.random.default_rng(3)
+    a, b = rng.standard_normal(103), rng.standard_normal(103)
+    parts = []
+    for i0 in range(0, 103, 10):
+        s = 0.0
+        for i in range(i0, min(i0 + 10, 103)):
+            s += a[i] * b[i]
+        parts.append(s)
+    tot = 0.0
+    for s in parts:
+        tot += s
+    assert oracle.dot(a, b, 10) == tot
+
+
+def test_spmv_walker_example_and_dense():
+    ex = GOLD["spec_examples"]["matvec_walker4"]
+    A, _ = W.walker(ex["n"], ex["alpha"])
+    e4 = np.zeros(4); e4[3] = 1.0
+    np.testing.assert_array_equal(oracle.spmv(A, e4), ex["y"])
+    P = W.config("c3", N=12)
+    x = np.random.default_rng(1).standard_normal(P.A.n_cols)
+    D = P.A.to_dense()
+    assert np.allclose(oracle.spmv(P.A, x), D @ x, rtol=0, atol=10 * EPS * np.abs(D).sum(1).max() * np.abs(x).max())
+
+
+def test_block_dot_layout_matches_definition():
+    rng = np.random.default_rng(2)
+    V = rng.standard_normal((300, 7)); u = rng.standard_normal(300); z = rng.standard_normal(300)
+    out = oracle.block_dot(V, u, z)
+    M = np.column_stack([V, u]).T @ np.column_stack([u, z])    # [V, u]^T [u, z]
+    ref = np.concatenate([M[:7, 0], [M[7, 0]], M[:7, 1], [M[7, 1]]])
+    assert np.allclose(out, ref, rtol=1e-13, atol=1e-13)
