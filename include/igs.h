@@ -1,0 +1,205 @@
+/*
+ * igs.h -- C ABI of libigs: the B200 (sm_100a) hot path of IGS-GMRES
+ * (Thomas, Carson, Rozloznik, Swirydowicz et al., arXiv 2205.07805).
+ *
+ * Citation keys: P:n = PAPER.md line n (the paper's LaTeX source); S:n = SPEC.md line n;
+ * "Alg. 2" = Low-Synchronization Two-Reduce Iterated Gauss-Seidel GMRES;
+ * "Alg. 3" = Low-Synch One-Reduce hybrid MGS-CGS GMRES;
+ * R# = reading of a garbled/silent passage, listed in DESIGN.md "Readings".
+ *
+ * What one Arnoldi iteration does on the device (gs_iters = 2 -> Alg. 3; gs_iters = 1 ->
+ * Alg. 2 Steps 1-13 + 17 with r^(3)=0, i.e. one Gauss-Seidel sweep, reading R8):
+ *   z = A u                                   sparse matvec (Alg. 3 Step 4)
+ *   [V_p, u]^T [u, z]  -> 2(p+1) scalars       ONE fused block dot
+ *   ncclAllReduce of those 2(p+1) doubles      the single "Global Synchronization"
+ *   (I+L)^{-1} correction, lagged norm, Stephen's trick, Hessenberg column, Givens
+ *   v_p = (u - V_p r2)/gamma ; u' = z/gamma - V_{p+1} r1   fused update
+ *
+ * Conventions (all entry points):
+ *   - Status codes only; nothing throws or aborts across the ABI.  On a non-OK status,
+ *     igs_last_error() returns a thread-local message.
+ *   - All floating point is IEEE FP64.  Matrices are CSR: rowptr int64 (local offsets,
+ *     rowptr[0] = 0), column indices 32- or 64-bit GLOBAL indices, strictly increasing per row.
+ *   - Dense n x c blocks are column-major with leading dimension ld (elements).
+ *   - The library copies the matrix at create; the caller keeps ownership of every array
+ *     it passes.  The library owns its device state until igs_destroy.
+ *   - Streams: all device work is enqueued on the cudaStream_t given at create (pass
+ *     torch.cuda.current_stream().cuda_stream).  Calls return after their results are
+ *     available to the caller (igs_solve synchronises the stream before returning).
+ *   - Multi-GPU: one process per GPU; every rank calls create/solve/destroy collectively
+ *     with identical (k, restart, tol, gs_iters).  Rank r owns rows
+ *     [row_begin, row_begin + n_local) of A, of every n-vector and of the Krylov basis V.
+ *   - There is no CPU fallback: without a CUDA device every compute call returns
+ *     IGS_ERR_CUDA.
+ */
+#ifndef IGS_H
+#define IGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct igs_ctx igs_ctx; /* opaque; one per rank */
+
+typedef enum {
+    IGS_OK = 0,
+    IGS_ERR_ARG = 1,       /* invalid argument (checked before any device work)          */
+    IGS_ERR_CUDA = 2,      /* CUDA runtime error, or no CUDA device                     */
+    IGS_ERR_NCCL = 3,      /* NCCL error                                                */
+    IGS_ERR_OOM = 4,       /* device or host allocation failed                          */
+    IGS_ERR_NONFINITE = 5, /* non-finite entry in A or b, or NaN during the solve */
+    IGS_ERR_STATE = 6      /* call out of order (e.g. solve after a failed create)     */
+} igs_status;
+
+typedef enum { IGS_MEM_HOST = 0, IGS_MEM_DEVICE = 1 } igs_mem;
+
+typedef enum {
+    IGS_TERM_CONVERGED = 0, /* true relative residual <= tol                              */
+    IGS_TERM_MAXITER = 1,   /* k Arnoldi iterations done                                 */
+    IGS_TERM_BREAKDOWN = 2  /* (happy) breakdown: H[p,p-1] ~ 0 (reading R12) -- NOT an error */
+} igs_term;
+
+/* Per-kernel timing classes (igs_kernel_stats). */
+typedef enum {
+    IGS_K_SPMV = 0,      /* z = A u (+ halo pack)                           */
+    IGS_K_BLOCK_DOT = 1, /* fused [V_p,u]^T[u,z] incl. deterministic 2nd stage */
+    IGS_K_ALLREDUCE = 2, /* ncclAllReduce of the 2(p+1) dots (G > 1)         */
+    IGS_K_SMALL = 3,     /* replicated small step (trisolve, H, Givens)      */
+    IGS_K_UPDATE = 4,    /* fused GEMV + axpy + lagged normalisation         */
+    IGS_K_HALO = 5,      /* ncclSend/ncclRecv of ghost entries (G > 1)       */
+    IGS_K_CYCLE = 6,     /* cycle end: y, x += V y, r = b - A x, ||r||       */
+    IGS_K_COUNT = 7
+} igs_kernel_kind;
+
+/* Create a solver for this rank's row block of A.
+ *   n_global    : global order n of A (square).
+ *   row_begin   : first global row owned by this rank; n_local rows owned.
+ *   rowptr      : int64[n_local+1], local offsets, rowptr[0] == 0, monotone.
+ *   colind      : int32 or int64 [nnz_local] (colind_bits = 32 | 64), global columns in
+ *                 [0, n_global), strictly increasing within each row.
+ *   values      : double[nnz_local]; must be finite (else IGS_ERR_NONFINITE).
+ *   where       : IGS_MEM_HOST or IGS_MEM_DEVICE for rowptr/colind/values.
+ *   cuda_device : device ordinal this rank uses.
+ *   nccl_unique_id : 128-byte ncclUniqueId from igs_nccl_unique_id() on rank 0, broadcast
+ *                 by the caller (torch.distributed); NULL iff nranks == 1.
+ *   rank, nranks: this rank and the world size; row blocks must tile [0, n_global) in rank
+ *                 order (checked collectively).
+ *   cuda_stream : cudaStream_t (as void*) for all device work; NULL = legacy default stream.
+ * Collective over the ranks when nranks > 1.  */
+igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_begin, int64_t n_local,
+                      const int64_t* rowptr, const void* colind, int colind_bits,
+                      const double* values, int64_t nnz_local, igs_mem where, int cuda_device,
+                      const void* nccl_unique_id, int rank, int nranks, void* cuda_stream);
+
+/* Write a fresh ncclUniqueId (128 bytes) into out (rank 0 only). */
+igs_status igs_nccl_unique_id(void* out128);
+
+/* Device bytes a solve with this max cycle length (restart, or k if unrestarted) needs. */
+size_t igs_workspace_bytes(const igs_ctx* ctx, int max_restart);
+
+/* Optional: let the caller (torch) own the device workspace.  dev_ptr must be 256-byte
+ * aligned and hold igs_workspace_bytes() bytes for every later solve's cycle length;
+ * otherwise the library allocates with cudaMalloc on first use. */
+igs_status igs_bind_workspace(igs_ctx* ctx, void* dev_ptr, size_t bytes);
+
+typedef struct {
+    double* x;             /* [n_local] out, caller-allocated, memory kind = vec_mem of igs_solve */
+    double* H;             /* [(m+1)*m] host, col-major (ld = m+1), cycle-1 Hessenberg,
+                              m = min(k, restart) (restart = 0 -> m = k); may be NULL      */
+    double* res_hist;      /* [k+1] host: res_hist[0] = ||r0||/||b||, res_hist[t] = |g_t|/||b||,
+                              the Givens-recurrence Arnoldi residual after iteration t
+                              (reading R16); may be NULL                        */
+    int want_loo;          /* in: compute ||I - V^T V||_F of the final basis         */
+    double loo_frob;       /* out: NaN if !want_loo                                            */
+    int iters;             /* out: total Arnoldi iterations (Hessenberg columns)              */
+    int cycles;            /* out: restart cycles run                                         */
+    igs_term term;         /* out                                                             */
+    double true_relres;    /* out: ||b - A x|| / ||b|| recomputed at the end                  */
+    int h_cols;            /* out: columns of H filled in cycle 1                             */
+    int basis_cols;        /* out: normalised columns of the final basis (LOO is over these)  */
+    int64_t allreduces;    /* out: NCCL allreduces issued by this solve (0 when nranks == 1)  */
+} igs_result;
+
+/* Solve A x = b by restarted IGS-GMRES.
+ *   vec_mem  : memory kind of b, x0 and res->x (IGS_MEM_HOST: the library copies b/x0 in
+ *              and x out inside the call; IGS_MEM_DEVICE: pointers into this rank's HBM).
+ *   b        : [n_local] this rank's rows of the right-hand side (finite).
+ *   x0       : [n_local] initial guess or NULL (= 0).
+ *   k        : max total Arnoldi iterations, 1 <= k < n_global - 1.
+ *   restart  : cycle length m; 0 or >= k => unrestarted.
+ *   tol      : relative residual target ||b - A x|| <= tol ||b||; 0 => run exactly k
+ *              iterations (unless breakdown).  Inside a cycle the Givens estimate |g_p|
+ *              decides, at cycle start the true residual (SURVEY §8(c) "Driver").
+ *   gs_iters : 1 (one Gauss-Seidel sweep, Alg. 2 minus Steps 14-16) or 2 (Alg. 3, one
+ *              reduction per iteration; reading R7).
+ * Breakdown is reported via res->term, not as an error. */
+igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, const double* x0, int k,
+                     int restart, double tol, int gs_iters, igs_result* res);
+
+/* Cumulative counters since create: NCCL allreduces, halo messages, Arnoldi iterations. */
+igs_status igs_stats(const igs_ctx* ctx, int64_t* allreduces, int64_t* halo_msgs,
+                     int64_t* iterations);
+
+/* Per-kernel timing (CUDA events around every launch on the solver stream) -- off by
+ * default; igs_set_timing(ctx, 1) enables it for later solves, and igs_kernel_stats
+ * returns, for kind, the summed device milliseconds, the launch count and the summed
+ * algorithmic bytes since the last reset (on = 2 resets). */
+igs_status igs_set_timing(igs_ctx* ctx, int on);
+igs_status igs_kernel_stats(const igs_ctx* ctx, int kind, double* ms, int64_t* launches,
+                            double* bytes);
+
+igs_status igs_destroy(igs_ctx* ctx);
+const char* igs_last_error(void);
+
+/* ---------------------------------------------------------------------------------
+ * Kernel-level entry points (device pointers, enqueue on `cuda_stream`, synchronise
+ * before returning).  They run exactly the kernels igs_solve runs and exist so tests
+ * can check each step against the oracle.  No context needed unless stated.
+ * --------------------------------------------------------------------------------- */
+
+/* out[0 : 2(p+1)] = [V_p^T u, u.u, V_p^T z, u.z]  (Alg. 3 Step 4), or with
+ * z == NULL out[0 : p+1] = [V_p^T u, u.u].  V: n x p (ld >= n, ld even, 16-byte aligned),
+ * u, z: n.  Deterministic (fixed two-stage reduction, no FP atomics). */
+igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                            const double* z, double* out, void* cuda_stream);
+
+/* y = A x with the context's (local, nranks == 1) matrix: x, y device [n_local]. */
+igs_status igs_op_spmv(igs_ctx* ctx, const double* x, double* y);
+
+/* Fused update:  w = u - V_p alpha (alpha == NULL -> w = u);
+ *   v = w / gamma  written to v_out;  if u_next != NULL:
+ *   u_next = z / gamma - (V_p beta[0:p] + v * beta[p]).
+ * V: n x p (ld even), alpha: p, beta: p+1 (device). v_out may alias u. */
+igs_status igs_op_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                         const double* z, const double* alpha, const double* beta, double gamma,
+                         double* v_out, double* u_next, void* cuda_stream);
+
+/* x = (I + L)^{-1} b by forward substitution; L strictly lower, col-major
+ * order x order, ld = ldl (device); b, x device [order].  One CTA (the small-step solver). */
+igs_status igs_op_trisolve(int order, const double* L, int ldl, const double* b, double* x,
+                           void* cuda_stream);
+
+/* ---------------------------------------------------------------------------------
+ * Host-only halo planning (no device needed; used by igs_create and by CPU tests).
+ * Phase 1: ghosts = sorted unique global columns of this block outside
+ *   [row_begin, row_begin+n_local); ghost_owner_count[q] = ghosts owned by rank q, given
+ *   the ownership boundaries bounds[0..nranks] (bounds[q] = first row of rank q).
+ *   Returns the number of ghosts in *n_ghost; if ghosts != NULL it is filled (capacity
+ *   must be >= *n_ghost from a first call with ghosts == NULL).
+ * Phase 2: local_colind[nnz] = colind remapped to [0, n_local + n_ghost): local columns
+ *   first, ghost g at n_local + g.  */
+igs_status igs_plan_ghosts(int64_t row_begin, int64_t n_local, const int64_t* rowptr,
+                           const void* colind, int colind_bits, int nranks,
+                           const int64_t* bounds, int64_t* n_ghost, int64_t* ghosts,
+                           int64_t* ghost_owner_count);
+igs_status igs_plan_remap(int64_t row_begin, int64_t n_local, const int64_t* rowptr,
+                          const void* colind, int colind_bits, int64_t n_ghost,
+                          const int64_t* ghosts, int64_t* local_colind);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGS_H */

@@ -55,6 +55,8 @@ def lib():
         _lib.oracle_hessenberg_lsq.restype = D
         _lib.oracle_hessenberg_lsq.argtypes = [I, P, I, D, P]
         _lib.oracle_num_threads.restype = I
+        _lib.oracle_gemv.restype = None
+        _lib.oracle_gemv.argtypes = [I64, I, P, I64, P, P]
     return _lib
 
 
@@ -99,6 +101,28 @@ def block_dot(Vp, u, z, block: int = 0) -> np.ndarray:
         out[p + 1 + j] = dot(Vp[:, j], z, block)
     out[2 * p + 1] = dot(u, z, block)
     return out
+
+
+def gemv(V, c) -> np.ndarray:
+    """t = V c, each row summed over columns in natural order."""
+    V = np.asfortranarray(V, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    t = np.empty(V.shape[0])
+    lib().oracle_gemv(V.shape[0], V.shape[1], _p(V), V.shape[0], _p(c), _p(t))
+    return t
+
+
+def update(Vp, u, z, alpha, beta, gamma):
+    """The fused update of Alg. 3 Steps 10-13, in the oracle's arithmetic:
+    v = (u - V_p alpha) / gamma (alpha None: v = u / gamma, Alg. 2 Step 7);
+    u' = z / gamma - (V_p beta[:p] + v beta[p])  (Step 13 as V_{p+1} r1)."""
+    p = Vp.shape[1]
+    w = u - gemv(Vp, alpha) if alpha is not None else u.copy()
+    v = w / gamma
+    if z is None:
+        return v, None
+    Vp1 = np.column_stack([Vp, v])
+    return v, z / gamma - gemv(Vp1, beta[:p + 1])
 
 
 def forward_solve_unit(L, b) -> np.ndarray:

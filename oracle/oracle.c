@@ -116,6 +116,11 @@ static void gemv_n(int64_t n, int p, const double* V, int64_t ldv, const double*
     }
 }
 
+/* exported for the fused-update parity test: t = V[:, 0:p] c */
+void oracle_gemv(int64_t n, int p, const double* V, int64_t ldv, const double* c, double* t) {
+    gemv_n(n, p, V, ldv, c, t);
+}
+
 /* ------------------------------------------------------- Givens least squares --- */
 /* Progressive Givens QR of H: rotate column j, update g.  R is a copy of H
  * (ld = ldh) that receives the rotated column.  Rotation: d = hypot(a,b), c = a/d,

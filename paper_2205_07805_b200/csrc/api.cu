@@ -1,0 +1,912 @@
+// api.cu -- host side of libigs: the C ABI of include/igs.h, the restarted IGS-GMRES
+// driver, NCCL plumbing (one allreduce per iteration + halo send/recv) and per-kernel
+// timing.  Device work lives in kernels.cu.
+//
+// P:n = PAPER.md line n (arXiv 2205.07805).  Driver semantics: SURVEY §8(c) "Driver";
+// per-iteration structure: Alg. 3 for gs_iters = 2, Alg. 2 without Steps
+// 14-16 for gs_iters = 1.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/igs.h"
+#include "igs_internal.cuh"
+
+namespace igs {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace igs
+
+using namespace igs;
+
+#define CUDA_TRY(x)                                                                        \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) {                                                           \
+            set_error(std::string(#x) + " failed: " + cudaGetErrorString(e_));            \
+            return e_ == cudaErrorMemoryAllocation ? IGS_ERR_OOM : IGS_ERR_CUDA;           \
+        }                                                                                  \
+    } while (0)
+#define NCCL_TRY(x)                                                                        \
+    do {                                                                                   \
+        ncclResult_t r_ = (x);                                                             \
+        if (r_ != ncclSuccess) {                                                           \
+            set_error(std::string(#x) + " failed: " + ncclGetErrorString(r_));            \
+            return IGS_ERR_NCCL;                                                           \
+        }                                                                                  \
+    } while (0)
+#define TRY(x)                        \
+    do {                              \
+        igs_status s_ = (x);          \
+        if (s_ != IGS_OK) return s_;  \
+    } while (0)
+#define ARG_CHECK(cond, msg)              \
+    do {                                  \
+        if (!(cond)) {                    \
+            set_error(std::string(msg));  \
+            return IGS_ERR_ARG;           \
+        }                                 \
+    } while (0)
+
+struct TimedLaunch {
+    int kind;
+    double bytes;
+    int ev0, ev1;
+};
+
+struct igs_ctx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    int rank = 0, nranks = 1;
+    ncclComm_t comm = nullptr;
+    int num_sms = 148;
+    bool ok = false;
+
+    int64_t n_global = 0, row_begin = 0, n_local = 0, ldv = 0;
+    // matrix, local column space [0, n_local + n_ghost)
+    SpmvArgs A{};
+    void* d_rowptr = nullptr;
+    void* d_col = nullptr;
+    double* d_val = nullptr;
+    int64_t nnz = 0;
+    // halo
+    int64_t n_ghost = 0;
+    double* d_ghost = nullptr;
+    double* d_send = nullptr;
+    int64_t* d_send_idx = nullptr;
+    int64_t n_send = 0;
+    std::vector<int> peers;
+    std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;
+    // workspace
+    int m_cap = 0, k_cap = 0;
+    double* d_V = nullptr;
+    double* d_z = nullptr;
+    double* d_b = nullptr;
+    double* d_x = nullptr;
+    double* d_small = nullptr;  // all small double arrays
+    int* d_int = nullptr;
+    double* d_part = nullptr;
+    unsigned* d_counter = nullptr;
+    double* d_gram = nullptr;  // gram partials + G
+    size_t gram_cap = 0;
+    int bdot_grid = 1;
+    Dev dev_state{};
+    double* h_pinned = nullptr;  // small pinned staging
+    int* h_pinned_int = nullptr;
+    void* bound_ws = nullptr;
+    size_t bound_bytes = 0;
+    bool owns_ws = true;
+    // counters
+    int64_t n_allreduce = 0, n_halo = 0, n_iter = 0;
+    // timing
+    bool timing = false;
+    std::vector<cudaEvent_t> events;
+    std::vector<TimedLaunch> recs;
+    double t_ms[IGS_K_COUNT] = {0};
+    double t_bytes[IGS_K_COUNT] = {0};
+    int64_t t_launch[IGS_K_COUNT] = {0};
+};
+
+// ------------------------------------------------------------------------------ misc
+extern "C" const char* igs_last_error(void) { return g_err.c_str(); }
+
+static inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+static igs_status timer_begin(igs_ctx* c, int* idx) {
+    *idx = -1;
+    if (!c->timing) return IGS_OK;
+    const size_t need = 2 * (c->recs.size() + 1);
+    while (c->events.size() < need) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        c->events.push_back(e);
+    }
+    *idx = (int)(2 * c->recs.size());
+    CUDA_TRY(cudaEventRecord(c->events[*idx], c->stream));
+    return IGS_OK;
+}
+
+static igs_status timer_end(igs_ctx* c, int idx, int kind, double bytes) {
+    if (idx < 0) return IGS_OK;
+    CUDA_TRY(cudaEventRecord(c->events[idx + 1], c->stream));
+    c->recs.push_back({kind, bytes, idx, idx + 1});
+    return IGS_OK;
+}
+
+static igs_status timer_flush(igs_ctx* c) {
+    for (const auto& r : c->recs) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, c->events[r.ev0], c->events[r.ev1]));
+        c->t_ms[r.kind] += ms;
+        c->t_bytes[r.kind] += r.bytes;
+        c->t_launch[r.kind] += 1;
+    }
+    c->recs.clear();
+    return IGS_OK;
+}
+
+#define TIMED(kind, bytes, launch_stmt)           \
+    do {                                          \
+        int ti_;                                  \
+        TRY(timer_begin(ctx, &ti_));              \
+        launch_stmt;                              \
+        CUDA_TRY(cudaGetLastError());             \
+        TRY(timer_end(ctx, ti_, (kind), (bytes)));\
+    } while (0)
+
+// --------------------------------------------------------------------- create / destroy
+extern "C" igs_status igs_nccl_unique_id(void* out128) {
+    ARG_CHECK(out128 != nullptr, "igs_nccl_unique_id: NULL output");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return IGS_OK;
+}
+
+static igs_status validate_csr(int64_t n_global, int64_t n_local, const int64_t* rowptr,
+                               const void* colind, int bits, const double* values, int64_t nnz) {
+    ARG_CHECK(rowptr[0] == 0, "igs_create: rowptr[0] != 0");
+    ARG_CHECK(rowptr[n_local] == nnz, "igs_create: rowptr[n_local] != nnz_local");
+    for (int64_t i = 0; i < n_local; i++) {
+        ARG_CHECK(rowptr[i + 1] >= rowptr[i], "igs_create: rowptr not monotone");
+        int64_t prev = -1;
+        for (int64_t q = rowptr[i]; q < rowptr[i + 1]; q++) {
+            const int64_t cc = bits == 64 ? static_cast<const int64_t*>(colind)[q]
+                                          : (int64_t) static_cast<const int32_t*>(colind)[q];
+            ARG_CHECK(cc >= 0 && cc < n_global, "igs_create: column index out of range");
+            ARG_CHECK(cc > prev, "igs_create: column indices not strictly increasing in a row");
+            prev = cc;
+        }
+    }
+    for (int64_t q = 0; q < nnz; q++)
+        if (!std::isfinite(values[q])) {
+            set_error("igs_create: non-finite matrix entry");
+            return IGS_ERR_NONFINITE;
+        }
+    return IGS_OK;
+}
+
+static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* colind, int bits,
+                             std::vector<int64_t>& local_col) {
+    const int G = ctx->nranks;
+    std::vector<int64_t> bounds(G + 1, 0);
+    if (G > 1) {
+        // all-gather (row_begin, n_local) through NCCL
+        int64_t* d_bl = nullptr;
+        CUDA_TRY(cudaMalloc(&d_bl, sizeof(int64_t) * 2 * G));
+        int64_t mine[2] = {ctx->row_begin, ctx->n_local};
+        CUDA_TRY(cudaMemcpyAsync(d_bl + 2 * ctx->rank, mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
+        NCCL_TRY(ncclAllGather(d_bl + 2 * ctx->rank, d_bl, 2, ncclInt64, ctx->comm, ctx->stream));
+        std::vector<int64_t> bl(2 * G);
+        CUDA_TRY(cudaMemcpyAsync(bl.data(), d_bl, sizeof(int64_t) * 2 * G, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        cudaFree(d_bl);
+        for (int q = 0; q < G; q++) {
+            ARG_CHECK(bl[2 * q] == (q == 0 ? 0 : bl[2 * (q - 1)] + bl[2 * (q - 1) + 1]),
+                      "igs_create: row blocks do not tile [0, n) in rank order");
+            bounds[q] = bl[2 * q];
+        }
+        bounds[G] = bl[2 * (G - 1)] + bl[2 * (G - 1) + 1];
+        ARG_CHECK(bounds[G] == ctx->n_global, "igs_create: row blocks do not cover n_global");
+    } else {
+        ARG_CHECK(ctx->row_begin == 0 && ctx->n_local == ctx->n_global,
+                  "igs_create: single rank must own all rows");
+        bounds[1] = ctx->n_global;
+    }
+    int64_t ng = 0;
+    std::vector<int64_t> owner_cnt(G, 0);
+    TRY(igs_plan_ghosts(ctx->row_begin, ctx->n_local, rowptr, colind, bits, G, bounds.data(), &ng,
+                        nullptr, owner_cnt.data()));
+    std::vector<int64_t> ghosts(ng);
+    TRY(igs_plan_ghosts(ctx->row_begin, ctx->n_local, rowptr, colind, bits, G, bounds.data(), &ng,
+                        ghosts.data(), owner_cnt.data()));
+    local_col.resize(ctx->n_local > 0 ? rowptr[ctx->n_local] : 0);
+    TRY(igs_plan_remap(ctx->row_begin, ctx->n_local, rowptr, colind, bits, ng, ghosts.data(),
+                       local_col.data()));
+    ctx->n_ghost = ng;
+    if (G == 1) {
+        ARG_CHECK(ng == 0, "igs_create: ghost columns with one rank");
+        return IGS_OK;
+    }
+    // count matrix cnt[q][r] = ghosts rank q needs from rank r (all-gather of owner counts)
+    int64_t* d_cnt = nullptr;
+    CUDA_TRY(cudaMalloc(&d_cnt, sizeof(int64_t) * G * G));
+    CUDA_TRY(cudaMemcpyAsync(d_cnt + (int64_t)G * ctx->rank, owner_cnt.data(), sizeof(int64_t) * G,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    NCCL_TRY(ncclAllGather(d_cnt + (int64_t)G * ctx->rank, d_cnt, G, ncclInt64, ctx->comm, ctx->stream));
+    std::vector<int64_t> cnt((size_t)G * G);
+    CUDA_TRY(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_cnt);
+    // receive side: my ghosts, grouped by owner (ghosts are sorted, owners ascending)
+    // send side: rows other ranks need from me
+    ctx->peers.clear(); ctx->send_off.clear(); ctx->send_cnt.clear(); ctx->recv_off.clear(); ctx->recv_cnt.clear();
+    int64_t roff = 0, soff = 0;
+    for (int q = 0; q < G; q++) {
+        const int64_t rc = cnt[(size_t)ctx->rank * G + q];  // I need rc from q
+        const int64_t sc = cnt[(size_t)q * G + ctx->rank];  // q needs sc from me
+        if (q == ctx->rank) { ARG_CHECK(rc == 0, "igs_create: self ghost"); continue; }
+        if (rc == 0 && sc == 0) continue;
+        ctx->peers.push_back(q);
+        ctx->recv_off.push_back(roff); ctx->recv_cnt.push_back(rc); roff += rc;
+        ctx->send_off.push_back(soff); ctx->send_cnt.push_back(sc); soff += sc;
+    }
+    ctx->n_send = soff;
+    // exchange the requested global indices
+    int64_t *d_req_out = nullptr, *d_req_in = nullptr;
+    CUDA_TRY(cudaMalloc(&d_req_out, sizeof(int64_t) * std::max<int64_t>(ng, 1)));
+    CUDA_TRY(cudaMalloc(&d_req_in, sizeof(int64_t) * std::max<int64_t>(soff, 1)));
+    CUDA_TRY(cudaMemcpyAsync(d_req_out, ghosts.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice, ctx->stream));
+    NCCL_TRY(ncclGroupStart());
+    for (size_t i = 0; i < ctx->peers.size(); i++) {
+        if (ctx->recv_cnt[i]) NCCL_TRY(ncclSend(d_req_out + ctx->recv_off[i], ctx->recv_cnt[i], ncclInt64, ctx->peers[i], ctx->comm, ctx->stream));
+        if (ctx->send_cnt[i]) NCCL_TRY(ncclRecv(d_req_in + ctx->send_off[i], ctx->send_cnt[i], ncclInt64, ctx->peers[i], ctx->comm, ctx->stream));
+    }
+    NCCL_TRY(ncclGroupEnd());
+    std::vector<int64_t> req(soff);
+    CUDA_TRY(cudaMemcpyAsync(req.data(), d_req_in, sizeof(int64_t) * soff, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d_req_out);
+    cudaFree(d_req_in);
+    for (auto& r : req) {
+        ARG_CHECK(r >= ctx->row_begin && r < ctx->row_begin + ctx->n_local, "igs_create: bad halo request");
+        r -= ctx->row_begin;
+    }
+    CUDA_TRY(cudaMalloc(&ctx->d_send_idx, sizeof(int64_t) * std::max<int64_t>(soff, 1)));
+    CUDA_TRY(cudaMalloc(&ctx->d_send, sizeof(double) * std::max<int64_t>(soff, 1)));
+    CUDA_TRY(cudaMalloc(&ctx->d_ghost, sizeof(double) * std::max<int64_t>(ng, 1)));
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_send_idx, req.data(), sizeof(int64_t) * soff, cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return IGS_OK;
+}
+
+static void free_ctx(igs_ctx* c) {
+    if (!c) return;
+    cudaFree(c->d_rowptr); cudaFree(c->d_col); cudaFree(c->d_val);
+    cudaFree(c->d_ghost); cudaFree(c->d_send); cudaFree(c->d_send_idx);
+    if (c->owns_ws) { cudaFree(c->d_V); }
+    cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
+    cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter);
+    cudaFree(c->d_gram);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
+    for (auto e : c->events) cudaEventDestroy(e);
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+}
+
+extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_begin,
+                                 int64_t n_local, const int64_t* rowptr, const void* colind,
+                                 int colind_bits, const double* values, int64_t nnz_local,
+                                 igs_mem where, int cuda_device, const void* nccl_unique_id,
+                                 int rank, int nranks, void* cuda_stream) {
+    ARG_CHECK(out != nullptr, "igs_create: NULL out");
+    *out = nullptr;
+    ARG_CHECK(n_global > 0, "igs_create: n_global must be > 0");
+    ARG_CHECK(row_begin >= 0 && n_local >= 0 && row_begin + n_local <= n_global, "igs_create: bad row block");
+    ARG_CHECK(colind_bits == 32 || colind_bits == 64, "igs_create: colind_bits must be 32 or 64");
+    ARG_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "igs_create: bad rank/nranks");
+    ARG_CHECK((nranks == 1) == (nccl_unique_id == nullptr), "igs_create: nccl_unique_id must be given iff nranks > 1");
+    ARG_CHECK(nnz_local >= 0, "igs_create: nnz_local < 0");
+    ARG_CHECK(n_local == 0 || (rowptr && (nnz_local == 0 || (colind && values))), "igs_create: NULL CSR array");
+    ARG_CHECK(where == IGS_MEM_HOST || where == IGS_MEM_DEVICE, "igs_create: bad memory kind");
+    ARG_CHECK(colind_bits == 64 || n_global < ((int64_t)1 << 31), "igs_create: 32-bit columns need n_global < 2^31");
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_error("igs_create: no CUDA device (libigs has no CPU fallback)");
+        return IGS_ERR_CUDA;
+    }
+    ARG_CHECK(cuda_device >= 0 && cuda_device < ndev, "igs_create: bad cuda_device");
+    CUDA_TRY(cudaSetDevice(cuda_device));
+
+    // host views of the CSR (copy from the device when given device pointers)
+    std::vector<int64_t> h_rowptr;
+    std::vector<char> h_col;
+    std::vector<double> h_val;
+    const size_t cbytes = (size_t)nnz_local * (colind_bits / 8);
+    if (where == IGS_MEM_DEVICE) {
+        h_rowptr.resize(n_local + 1);
+        h_col.resize(cbytes);
+        h_val.resize(nnz_local);
+        if (n_local > 0) CUDA_TRY(cudaMemcpy(h_rowptr.data(), rowptr, sizeof(int64_t) * (n_local + 1), cudaMemcpyDeviceToHost));
+        else h_rowptr[0] = 0;
+        if (nnz_local) {
+            CUDA_TRY(cudaMemcpy(h_col.data(), colind, cbytes, cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(h_val.data(), values, sizeof(double) * nnz_local, cudaMemcpyDeviceToHost));
+        }
+        rowptr = h_rowptr.data();
+        colind = h_col.data();
+        values = h_val.data();
+    }
+    int64_t zero_ptr = 0;
+    if (n_local == 0) rowptr = &zero_ptr;
+    TRY(validate_csr(n_global, n_local, rowptr, colind, colind_bits, values, nnz_local));
+
+    igs_ctx* ctx = new igs_ctx();
+    ctx->dev = cuda_device;
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    ctx->n_global = n_global;
+    ctx->row_begin = row_begin;
+    ctx->n_local = n_local;
+    ctx->ldv = round_up(std::max<int64_t>(n_local, 1), 32);
+    ctx->nnz = nnz_local;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+
+    auto fail = [&](igs_status s) { free_ctx(ctx); return s; };
+    if (nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_unique_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclCommInitRank failed: ") + ncclGetErrorString(r));
+            return fail(IGS_ERR_NCCL);
+        }
+    }
+    std::vector<int64_t> local_col;
+    {
+        igs_status s = setup_halo(ctx, rowptr, colind, colind_bits, local_col);
+        if (s != IGS_OK) return fail(s);
+    }
+    // device CSR: int32 rowptr unless nnz needs 64 bits or the caller chose 64-bit columns
+    const bool idx64 = colind_bits == 64 || (n_local + ctx->n_ghost) >= ((int64_t)1 << 31);
+    const bool ptr64 = idx64 || nnz_local >= ((int64_t)1 << 31);
+    {
+        std::vector<char> rp((size_t)(n_local + 1) * (ptr64 ? 8 : 4));
+        for (int64_t i = 0; i <= n_local; i++) {
+            if (ptr64) reinterpret_cast<int64_t*>(rp.data())[i] = rowptr[i];
+            else reinterpret_cast<int32_t*>(rp.data())[i] = (int32_t)rowptr[i];
+        }
+        std::vector<char> ci((size_t)std::max<int64_t>(nnz_local, 1) * (idx64 ? 8 : 4));
+        for (int64_t q = 0; q < nnz_local; q++) {
+            if (idx64) reinterpret_cast<int64_t*>(ci.data())[q] = local_col[q];
+            else reinterpret_cast<int32_t*>(ci.data())[q] = (int32_t)local_col[q];
+        }
+        cudaError_t e;
+        if ((e = cudaMalloc(&ctx->d_rowptr, rp.size())) != cudaSuccess ||
+            (e = cudaMalloc(&ctx->d_col, ci.size())) != cudaSuccess ||
+            (e = cudaMalloc(&ctx->d_val, sizeof(double) * std::max<int64_t>(nnz_local, 1))) != cudaSuccess) {
+            set_error(std::string("igs_create: cudaMalloc: ") + cudaGetErrorString(e));
+            return fail(IGS_ERR_OOM);
+        }
+        if ((e = cudaMemcpy(ctx->d_rowptr, rp.data(), rp.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy(ctx->d_col, ci.data(), (size_t)nnz_local * (idx64 ? 8 : 4), cudaMemcpyHostToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy(ctx->d_val, values, sizeof(double) * nnz_local, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            set_error(std::string("igs_create: cudaMemcpy: ") + cudaGetErrorString(e));
+            return fail(IGS_ERR_CUDA);
+        }
+    }
+    ctx->A.nrows = n_local;
+    ctx->A.rowptr = ctx->d_rowptr;
+    ctx->A.col = ctx->d_col;
+    ctx->A.val = ctx->d_val;
+    ctx->A.ptr64 = ptr64;
+    ctx->A.idx64 = idx64;
+    ctx->A.nloc = n_local;
+    ctx->A.ghost = ctx->n_ghost > 0 ? ctx->d_ghost : nullptr;
+    {
+        // short rows (<= 12 nnz on average): CSR-stream kernel (lpr = 0); otherwise vector
+        // CSR with lanes per row = next power of two of the mean row length, in [1, 32]
+        const double avg = n_local > 0 ? (double)nnz_local / (double)n_local : 1.0;
+        int lpr = 1;
+        while (lpr < 32 && lpr < avg) lpr *= 2;
+        ctx->A.lpr = avg <= 12.0 ? 0 : lpr;
+    }
+    ctx->bdot_grid = bdot_grid_size(n_local, ctx->num_sms);
+    cudaError_t e;
+    if ((e = cudaMallocHost(&ctx->h_pinned, sizeof(double) * 64)) != cudaSuccess ||
+        (e = cudaMallocHost(&ctx->h_pinned_int, sizeof(int) * 64)) != cudaSuccess) {
+        set_error(std::string("igs_create: cudaMallocHost: ") + cudaGetErrorString(e));
+        return fail(IGS_ERR_OOM);
+    }
+    ctx->ok = true;
+    *out = ctx;
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_destroy(igs_ctx* ctx) {
+    if (!ctx) return IGS_OK;
+    cudaSetDevice(ctx->dev);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    free_ctx(ctx);
+    return IGS_OK;
+}
+
+// ------------------------------------------------------------------------- workspace
+static size_t small_doubles(int m, int k) {
+    const size_t ldh = m + 1, dld = 2 * (m + 1) + 2;
+    return 3 * ldh * m      // H, HP, R
+           + (size_t)m * m  // L
+           + 2 * (m + 2)    // cs, sn
+           + (m + 2)        // g
+           + (m + 1) * dld  // dots
+           + 3 * (m + 2)    // alpha, beta, y
+           + SC_COUNT + (k + 2);
+}
+
+extern "C" size_t igs_workspace_bytes(const igs_ctx* ctx, int max_restart) {
+    if (!ctx || max_restart < 1) return 0;
+    return (size_t)(max_restart + 1) * ctx->ldv * sizeof(double);
+}
+
+extern "C" igs_status igs_bind_workspace(igs_ctx* ctx, void* dev_ptr, size_t bytes) {
+    ARG_CHECK(ctx && ctx->ok, "igs_bind_workspace: bad context");
+    ARG_CHECK(dev_ptr && ((uintptr_t)dev_ptr % 256) == 0, "igs_bind_workspace: pointer must be 256-byte aligned");
+    if (ctx->owns_ws && ctx->d_V) { cudaFree(ctx->d_V); }
+    ctx->d_V = nullptr;
+    ctx->m_cap = 0;
+    ctx->bound_ws = dev_ptr;
+    ctx->bound_bytes = bytes;
+    ctx->owns_ws = false;
+    return IGS_OK;
+}
+
+static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
+    const int64_t ldv = ctx->ldv;
+    if (m > ctx->m_cap || k > ctx->k_cap) {
+        const int mm = std::max(m, ctx->m_cap), kk = std::max(k, ctx->k_cap);
+        // V
+        const size_t vbytes = (size_t)(mm + 1) * ldv * sizeof(double);
+        if (ctx->owns_ws) {
+            cudaFree(ctx->d_V);
+            ctx->d_V = nullptr;
+            CUDA_TRY(cudaMalloc(&ctx->d_V, vbytes));
+        } else {
+            if (vbytes > ctx->bound_bytes) {
+                set_error("igs_solve: bound workspace too small");
+                return IGS_ERR_OOM;
+            }
+            ctx->d_V = static_cast<double*>(ctx->bound_ws);
+        }
+        // zero once: padding rows of every column must stay 0 (kernels read them as 0)
+        CUDA_TRY(cudaMemsetAsync(ctx->d_V, 0, vbytes, ctx->stream));
+        cudaFree(ctx->d_small);
+        cudaFree(ctx->d_int);
+        cudaFree(ctx->d_part);
+        const size_t nsd = small_doubles(mm, kk);
+        CUDA_TRY(cudaMalloc(&ctx->d_small, nsd * sizeof(double)));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_small, 0, nsd * sizeof(double), ctx->stream));
+        CUDA_TRY(cudaMalloc(&ctx->d_int, sizeof(int) * ST_COUNT));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_int, 0, sizeof(int) * ST_COUNT, ctx->stream));
+        CUDA_TRY(cudaMalloc(&ctx->d_part, sizeof(double) * (size_t)ctx->bdot_grid * (2 * (mm + 1) + 2)));
+        Dev& d = ctx->dev_state;
+        d.m = mm;
+        d.ldh = mm + 1;
+        d.dld = 2 * (mm + 1) + 2;
+        double* q = ctx->d_small;
+        auto take = [&](size_t cnt) { double* r = q; q += cnt; return r; };
+        d.H = take((size_t)d.ldh * mm);
+        d.HP = take((size_t)d.ldh * mm);
+        d.R = take((size_t)d.ldh * mm);
+        d.L = take((size_t)mm * mm);
+        d.cs = take(mm + 2);
+        d.sn = take(mm + 2);
+        d.g = take(mm + 2);
+        d.dots = take((size_t)(mm + 1) * d.dld);
+        d.alpha = take(mm + 2);
+        d.beta = take(mm + 2);
+        d.y = take(mm + 2);
+        d.scal = take(SC_COUNT);
+        d.res_hist = take(kk + 2);
+        d.istate = ctx->d_int;
+        ctx->m_cap = mm;
+        ctx->k_cap = kk;
+    }
+    if (!ctx->d_z) {
+        CUDA_TRY(cudaMalloc(&ctx->d_z, sizeof(double) * ldv));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_z, 0, sizeof(double) * ldv, ctx->stream));
+    }
+    if (!ctx->d_counter) {
+        CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 4));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned) * 4, ctx->stream));
+    }
+    if (host_vec && !ctx->d_b) {
+        CUDA_TRY(cudaMalloc(&ctx->d_b, sizeof(double) * ldv));
+        CUDA_TRY(cudaMalloc(&ctx->d_x, sizeof(double) * ldv));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_b, 0, sizeof(double) * ldv, ctx->stream));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_x, 0, sizeof(double) * ldv, ctx->stream));
+    }
+    return IGS_OK;
+}
+
+// -------------------------------------------------------------------- solve pieces
+static inline double* Vcol(igs_ctx* c, int j) { return c->d_V + (int64_t)j * c->ldv; }
+
+static double spmv_bytes(const igs_ctx* c) {
+    const double sc = c->A.idx64 ? 8 : 4, sp = c->A.ptr64 ? 8 : 4;
+    return (double)c->nnz * (8 + sc) + (double)(c->n_local + 1) * sp + 16.0 * c->n_local +
+           8.0 * c->n_ghost;
+}
+
+static igs_status allreduce(igs_ctx* ctx, double* buf, int64_t count) {
+    if (ctx->nranks == 1) return IGS_OK;
+    TIMED(IGS_K_ALLREDUCE, 0.0,
+          { NCCL_TRY(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm, ctx->stream)); });
+    ctx->n_allreduce++;
+    return IGS_OK;
+}
+
+static igs_status halo(igs_ctx* ctx, const double* x, const int* istate) {
+    if (ctx->nranks == 1 || ctx->peers.empty()) return IGS_OK;
+    TIMED(IGS_K_HALO, 16.0 * ctx->n_send + 8.0 * ctx->n_ghost, {
+        launch_pack(ctx->n_send, ctx->d_send_idx, x, ctx->d_send, istate, ctx->stream);
+        NCCL_TRY(ncclGroupStart());
+        for (size_t i = 0; i < ctx->peers.size(); i++) {
+            if (ctx->send_cnt[i]) NCCL_TRY(ncclSend(ctx->d_send + ctx->send_off[i], ctx->send_cnt[i], ncclDouble, ctx->peers[i], ctx->comm, ctx->stream));
+            if (ctx->recv_cnt[i]) NCCL_TRY(ncclRecv(ctx->d_ghost + ctx->recv_off[i], ctx->recv_cnt[i], ncclDouble, ctx->peers[i], ctx->comm, ctx->stream));
+        }
+        NCCL_TRY(ncclGroupEnd());
+    });
+    ctx->n_halo += (int64_t)ctx->peers.size();
+    return IGS_OK;
+}
+
+// z = A x (with halo) ; resid: y = b - A x
+static igs_status spmv(igs_ctx* ctx, const double* x, double* y, const double* b, bool resid,
+                       const int* istate, int kind) {
+    TRY(halo(ctx, x, istate));
+    TIMED(kind, spmv_bytes(ctx) + (resid ? 8.0 * ctx->n_local : 0.0),
+          launch_spmv(ctx->A, x, y, b, resid, istate, ctx->stream));
+    return IGS_OK;
+}
+
+static igs_status bdot(igs_ctx* ctx, int p, const double* u, const double* z, double* out,
+                       const int* istate, int kind) {
+    const double by = 8.0 * ctx->n_local * (p + 1 + (z ? 1 : 0));
+    TIMED(kind, by,
+          launch_block_dot(ctx->n_local, p, ctx->d_V, ctx->ldv, u, z, out, ctx->d_part,
+                           ctx->d_counter, ctx->bdot_grid, istate, ctx->stream));
+    TRY(allreduce(ctx, out, z ? 2 * (p + 1) : p + 1));
+    return IGS_OK;
+}
+
+// Scalar D2H through pinned staging (synchronises the stream).
+static igs_status fetch(igs_ctx* ctx, const double* dsrc, int nd, double* hd, const int* isrc,
+                        int ni, int* hi) {
+    if (nd) CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned, dsrc, sizeof(double) * nd, cudaMemcpyDeviceToHost, ctx->stream));
+    if (ni) CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned_int, isrc, sizeof(int) * ni, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (nd) std::memcpy(hd, ctx->h_pinned, sizeof(double) * nd);
+    if (ni) std::memcpy(hi, ctx->h_pinned_int, sizeof(int) * ni);
+    return IGS_OK;
+}
+
+// One restart cycle of m iterations (SURVEY §8(c) "Cycle priming" + per-iteration body).
+// On entry z holds r = b - A x and dots[0] = ||r||^2.  Returns after enqueueing (and occasionally waiting at
+// checkpoints, identically on every rank).
+static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
+    Dev& d = ctx->dev_state;
+    cudaStream_t st = ctx->stream;
+    const int64_t n = ctx->n_local;
+    const int* ist = d.istate;
+    CUDA_TRY(cudaMemsetAsync(d.H, 0, sizeof(double) * (size_t)d.ldh * d.m, st));
+    // priming, Steps 1-2 (reading R2): rho, v_0 = r/rho.  ||r||^2 is already in
+    // dots[0] (reduced by igs_solve for the cycle-start residual test).
+    TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_PRIME_NORM, gs, 0, m, t0, st));
+    TIMED(IGS_K_UPDATE, 16.0 * n,
+          launch_update(n, 0, ctx->d_V, ctx->ldv, ctx->d_z, nullptr, nullptr, nullptr,
+                        d.scal + SC_GAMMA, Vcol(ctx, 0), nullptr, ist, 0, st));
+    // z = A v_0 ; h = v_0 . z ; u = z - h v_0
+    TRY(spmv(ctx, Vcol(ctx, 0), ctx->d_z, nullptr, false, ist, IGS_K_SPMV));
+    TRY(bdot(ctx, 0, Vcol(ctx, 0), ctx->d_z, d.dots, ist, IGS_K_BLOCK_DOT));
+    TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_PRIME_H, gs, 0, m, t0, st));
+    TIMED(IGS_K_UPDATE, 24.0 * n,
+          launch_update(n, 0, ctx->d_V, ctx->ldv, Vcol(ctx, 0), ctx->d_z, nullptr, d.beta,
+                        d.scal + SC_GAMMA, Vcol(ctx, 0), Vcol(ctx, 1), ist, 0, st));
+
+    const int poll_every = 16;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int ev_slot = 0, ev_pending = -1;
+    int* h_status = ctx->h_pinned_int + 16;  // 2 slots
+    for (int p = 1; p <= m; p++) {
+        const bool drain = (p == m);
+        double* u = Vcol(ctx, p);
+        if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
+        TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
+        TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_ITER, gs, p, m, t0, st));
+        const double ub = 8.0 * n * ((gs == 2 || !drain) ? p : 0) + 16.0 * n + (drain ? 0.0 : 16.0 * n);
+        TIMED(IGS_K_UPDATE, ub,
+              launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
+                            d.beta, d.scal + SC_GAMMA, u, drain ? nullptr : Vcol(ctx, p + 1), ist, p, st));
+        ctx->n_iter++;
+        // checkpoint: copy the status word; decide on the PREVIOUS checkpoint's value so the
+        // GPU always has one chunk queued and every rank stops at the same iteration
+        if (p % poll_every == 0 && p < m) {
+            if (!ev[0]) {
+                CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+            }
+            CUDA_TRY(cudaMemcpyAsync(h_status + ev_slot, ist + ST_STATUS, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaEventRecord(ev[ev_slot], st));
+            if (ev_pending >= 0) {
+                CUDA_TRY(cudaEventSynchronize(ev[ev_pending]));
+                if (h_status[ev_pending] != RUNNING) { ev_pending = -1; break; }
+            }
+            ev_pending = ev_slot;
+            ev_slot ^= 1;
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, const double* x0,
+                                int k, int restart, double tol, int gs_iters, igs_result* res) {
+    ARG_CHECK(ctx && ctx->ok, "igs_solve: bad context");
+    ARG_CHECK(res && res->x && b, "igs_solve: NULL b / res / res->x");
+    ARG_CHECK(gs_iters == 1 || gs_iters == 2, "igs_solve: gs_iters must be 1 or 2");
+    ARG_CHECK(k >= 1 && (int64_t)k < ctx->n_global - 1, "igs_solve: need 1 <= k < n_global - 1 (P:873)");
+    ARG_CHECK(restart >= 0, "igs_solve: restart < 0");
+    ARG_CHECK(tol >= 0.0 && std::isfinite(tol), "igs_solve: tol must be finite and >= 0");
+    ARG_CHECK(vec_mem == IGS_MEM_HOST || vec_mem == IGS_MEM_DEVICE, "igs_solve: bad memory kind");
+    ARG_CHECK(vec_mem == IGS_MEM_HOST || (((uintptr_t)b % 16) == 0 && ((uintptr_t)res->x % 16) == 0),
+              "igs_solve: device b and x need 16-byte alignment");
+    CUDA_TRY(cudaSetDevice(ctx->dev));
+    const int m1 = (restart > 0 && restart < k) ? restart : k;
+    const bool hostv = vec_mem == IGS_MEM_HOST;
+    TRY(ensure_workspace(ctx, m1, k, hostv));
+    Dev& d = ctx->dev_state;
+    cudaStream_t st = ctx->stream;
+    const int64_t n = ctx->n_local;
+    ctx->recs.clear();
+
+    // vectors in HBM
+    const double* db;
+    double* dx;
+    if (hostv) {
+        TIMED(IGS_K_CYCLE, 0.0, {
+            CUDA_TRY(cudaMemcpyAsync(ctx->d_b, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+            if (x0) CUDA_TRY(cudaMemcpyAsync(ctx->d_x, x0, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+            else CUDA_TRY(cudaMemsetAsync(ctx->d_x, 0, sizeof(double) * n, st));
+        });
+        db = ctx->d_b;
+        dx = ctx->d_x;
+    } else {
+        db = b;
+        dx = res->x;
+        if (x0 && x0 != dx) CUDA_TRY(cudaMemcpyAsync(dx, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        else if (!x0) CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(double) * n, st));
+    }
+    const int64_t ar0 = ctx->n_allreduce;
+
+    // ||b|| (one reduction; also the non-finite check of b)
+    double* dsc = d.scal;
+    TRY(bdot(ctx, 0, db, nullptr, d.dots, nullptr, IGS_K_CYCLE));
+    double nb2 = 0.0;
+    TRY(fetch(ctx, d.dots, 1, &nb2, nullptr, 0, nullptr));
+    if (!std::isfinite(nb2)) {
+        set_error("igs_solve: non-finite right-hand side");
+        return IGS_ERR_NONFINITE;
+    }
+    const double nb = std::sqrt(nb2);
+    std::vector<double> hres(k + 1, std::nan(""));
+    res->iters = 0;
+    res->cycles = 0;
+    res->loo_frob = std::nan("");
+    res->h_cols = 0;
+    res->basis_cols = 0;
+    res->term = IGS_TERM_MAXITER;
+    if (res->H) std::fill(res->H, res->H + (size_t)(m1 + 1) * m1, 0.0);
+    if (nb == 0.0) {
+        CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(double) * n, st));
+        if (hostv) CUDA_TRY(cudaMemcpyAsync(res->x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        res->term = IGS_TERM_CONVERGED;
+        res->true_relres = 0.0;
+        if (res->res_hist) res->res_hist[0] = 0.0;
+        return IGS_OK;
+    }
+    {
+        double hs[SC_COUNT] = {0};
+        hs[SC_NB] = nb;
+        hs[SC_TOL] = tol;
+        CUDA_TRY(cudaMemcpyAsync(dsc, hs, sizeof(hs), cudaMemcpyHostToDevice, st));
+    }
+    int total = 0, cycles = 0, last_basis = 0;
+    bool breakdown = false;
+    double rn = 0.0;
+    for (;;) {
+        // r = b - A x into z (not V[:,0]: the final basis must survive for the LOO
+        // diagnostic); ||r||  (true residual at cycle start)
+        TRY(spmv(ctx, dx, ctx->d_z, db, true, nullptr, IGS_K_CYCLE));
+        TRY(bdot(ctx, 0, ctx->d_z, nullptr, d.dots, nullptr, IGS_K_CYCLE));
+        double rn2 = 0.0;
+        TRY(fetch(ctx, d.dots, 1, &rn2, nullptr, 0, nullptr));
+        if (!std::isfinite(rn2)) {
+            set_error("igs_solve: non-finite residual");
+            return IGS_ERR_NONFINITE;
+        }
+        rn = std::sqrt(rn2);
+        if (total == 0) hres[0] = rn / nb;
+        if (breakdown) { res->term = IGS_TERM_BREAKDOWN; break; }
+        if (tol > 0.0 && rn <= tol * nb) { res->term = IGS_TERM_CONVERGED; break; }
+        if (total >= k) { res->term = IGS_TERM_MAXITER; break; }
+        if (rn == 0.0) { res->term = IGS_TERM_CONVERGED; break; }
+        const int m = std::min(m1, k - total);
+        TRY(run_cycle(ctx, m, gs_iters, total));
+        int istate[ST_COUNT];
+        TRY(fetch(ctx, nullptr, 0, nullptr, d.istate, ST_COUNT, istate));
+        const int status = istate[ST_STATUS], p = istate[ST_PDONE];
+        if (status == STOP_NONFINITE) {
+            set_error("igs_solve: non-finite value during the Arnoldi iteration");
+            return IGS_ERR_NONFINITE;
+        }
+        if (cycles == 0) {
+            res->h_cols = p;
+            if (res->H)
+                CUDA_TRY(cudaMemcpyAsync(res->H, d.H, sizeof(double) * (size_t)(m1 + 1) * m1, cudaMemcpyDeviceToHost, st));
+        }
+        // y = argmin ||rho e1 - H y|| ; x += V_p y
+        TIMED(IGS_K_CYCLE, 0.0, launch_small(d, SS_LSQ, gs_iters, 0, m, total, st));
+        TIMED(IGS_K_CYCLE, 8.0 * n * p + 16.0 * n,
+              launch_xupdate(n, ctx->d_V, ctx->ldv, d.y, dx, d.istate, m, st));
+        total += p;
+        cycles++;
+        last_basis = istate[ST_BASIS];
+        if (status == STOP_BREAKDOWN) breakdown = true;
+    }
+    res->iters = total;
+    res->cycles = cycles;
+    res->basis_cols = last_basis;
+    res->true_relres = rn / nb;
+    if (total > 0) CUDA_TRY(cudaMemcpyAsync(hres.data() + 1, d.res_hist + 1, sizeof(double) * total, cudaMemcpyDeviceToHost, st));
+    // LOO of the final basis, diagnostic
+    if (res->want_loo && last_basis > 0) {
+        const int c = last_basis;
+        const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 4096));
+        const size_t need = (size_t)splits * c * c + (size_t)c * c + 1;
+        if (need > ctx->gram_cap) {
+            cudaFree(ctx->d_gram);
+            ctx->d_gram = nullptr;
+            CUDA_TRY(cudaMalloc(&ctx->d_gram, need * sizeof(double)));
+            ctx->gram_cap = need;
+        }
+        double* G = ctx->d_gram + (size_t)splits * c * c;
+        TIMED(IGS_K_CYCLE, 8.0 * n * c, launch_gram(n, c, ctx->d_V, ctx->ldv, ctx->d_gram, splits, G, st));
+        TRY(allreduce(ctx, G, (int64_t)c * c));
+        TIMED(IGS_K_CYCLE, 0.0, launch_loo_norm(c, G, G + (size_t)c * c, st));
+        double loo = 0.0;
+        TRY(fetch(ctx, G + (size_t)c * c, 1, &loo, nullptr, 0, nullptr));
+        res->loo_frob = loo;
+    }
+    if (hostv) CUDA_TRY(cudaMemcpyAsync(res->x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaGetLastError());
+    if (res->res_hist) std::memcpy(res->res_hist, hres.data(), sizeof(double) * (total + 1));
+    res->allreduces = ctx->n_allreduce - ar0;
+    TRY(timer_flush(ctx));
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_stats(const igs_ctx* ctx, int64_t* allreduces, int64_t* halo_msgs,
+                                int64_t* iterations) {
+    ARG_CHECK(ctx != nullptr, "igs_stats: NULL context");
+    if (allreduces) *allreduces = ctx->n_allreduce;
+    if (halo_msgs) *halo_msgs = ctx->n_halo;
+    if (iterations) *iterations = ctx->n_iter;
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_set_timing(igs_ctx* ctx, int on) {
+    ARG_CHECK(ctx != nullptr, "igs_set_timing: NULL context");
+    ctx->timing = on != 0;
+    if (on == 2) {
+        for (int i = 0; i < IGS_K_COUNT; i++) { ctx->t_ms[i] = 0; ctx->t_bytes[i] = 0; ctx->t_launch[i] = 0; }
+    }
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_kernel_stats(const igs_ctx* ctx, int kind, double* ms, int64_t* launches,
+                                       double* bytes) {
+    ARG_CHECK(ctx != nullptr && kind >= 0 && kind < IGS_K_COUNT, "igs_kernel_stats: bad argument");
+    if (ms) *ms = ctx->t_ms[kind];
+    if (launches) *launches = ctx->t_launch[kind];
+    if (bytes) *bytes = ctx->t_bytes[kind];
+    return IGS_OK;
+}
+
+// ----------------------------------------------------------------- kernel entry points
+static igs_status have_device() {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_error("no CUDA device (libigs has no CPU fallback)");
+        return IGS_ERR_CUDA;
+    }
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                                       const double* z, double* out, void* cuda_stream) {
+    ARG_CHECK(n >= 0 && p >= 0 && u && out && (p == 0 || V), "igs_op_block_dot: bad argument");
+    ARG_CHECK(p == 0 || (ld >= n && ld % 2 == 0 && ((uintptr_t)V % 16) == 0), "igs_op_block_dot: V needs even ld >= n and 16-byte alignment");
+    ARG_CHECK(((uintptr_t)u % 16) == 0 && (!z || ((uintptr_t)z % 16) == 0), "igs_op_block_dot: u, z need 16-byte alignment");
+    TRY(have_device());
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = bdot_grid_size(n, sms);
+    double* part = nullptr;
+    unsigned* counter = nullptr;
+    CUDA_TRY(cudaMalloc(&part, sizeof(double) * (size_t)grid * 2 * (p + 1)));
+    CUDA_TRY(cudaMalloc(&counter, sizeof(unsigned)));
+    CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+    launch_block_dot(n, p, V, ld, u, z, out, part, counter, grid, nullptr, st);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(part);
+    cudaFree(counter);
+    CUDA_TRY(e);
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_op_spmv(igs_ctx* ctx, const double* x, double* y) {
+    ARG_CHECK(ctx && ctx->ok && x && y, "igs_op_spmv: bad argument");
+    ARG_CHECK(ctx->nranks == 1, "igs_op_spmv: single-rank contexts only");
+    CUDA_TRY(cudaSetDevice(ctx->dev));
+    launch_spmv(ctx->A, x, y, nullptr, false, nullptr, ctx->stream);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_op_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                                    const double* z, const double* alpha, const double* beta,
+                                    double gamma, double* v_out, double* u_next, void* cuda_stream) {
+    ARG_CHECK(n >= 0 && p >= 0 && u && v_out && (p == 0 || V), "igs_op_update: bad argument");
+    ARG_CHECK(!u_next || (z && beta), "igs_op_update: u_next needs z and beta");
+    ARG_CHECK(p == 0 || (ld >= n && ld % 2 == 0 && ((uintptr_t)V % 16) == 0), "igs_op_update: V needs even ld >= n and 16-byte alignment");
+    ARG_CHECK(((uintptr_t)u % 16) == 0 && (!z || ((uintptr_t)z % 16) == 0), "igs_op_update: u, z need 16-byte alignment");
+    TRY(have_device());
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    double* dg = nullptr;
+    CUDA_TRY(cudaMalloc(&dg, sizeof(double)));
+    CUDA_TRY(cudaMemcpyAsync(dg, &gamma, sizeof(double), cudaMemcpyHostToDevice, st));
+    launch_update(n, p, V, ld, u, z, alpha, beta, dg, v_out, u_next, nullptr, 0, st);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(dg);
+    CUDA_TRY(e);
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_op_trisolve(int order, const double* L, int ldl, const double* b, double* x,
+                                      void* cuda_stream) {
+    ARG_CHECK(order >= 0 && ldl >= order && (order == 0 || (L && b && x)), "igs_op_trisolve: bad argument");
+    TRY(have_device());
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    launch_trisolve(order, L, ldl, b, x, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return IGS_OK;
+}

@@ -1,0 +1,100 @@
+// igs_internal.cuh -- device-side state and kernel launchers of libigs (sm_100a).
+// Nothing here is shared with oracle/ (the CPU reference); see DESIGN.md.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace igs {
+
+// Device status word (istate[ST_STATUS]); every per-iteration kernel no-ops unless RUNNING.
+enum : int { RUNNING = 0, STOP_CONVERGED = 1, STOP_BREAKDOWN = 2, STOP_END = 3, STOP_NONFINITE = 4 };
+// istate slots
+enum : int {
+    ST_STATUS = 0,     // RUNNING / STOP_*
+    ST_PDONE = 1,      // Hessenberg columns completed in this cycle
+    ST_BASIS = 2,      // normalised basis columns
+    ST_MODE = 3,       // update-kernel mode bits: 1 = write v_p, 2 = write u'
+    ST_MODE_IT = 4,    // iteration index the mode bits belong to
+    ST_COUNT = 8
+};
+// scal slots (device doubles)
+enum : int { SC_GAMMA = 0, SC_RHO = 1, SC_NB = 2, SC_TOL = 3, SC_COUNT = 8 };
+
+constexpr double kEps = 2.220446049250313e-16;
+constexpr double kBreakdownC = 64.0;  // reading R12
+
+// The replicated k x k state of one restart cycle (all device pointers).
+struct Dev {
+    int m;          // cycle capacity (columns of H)
+    int ldh;        // m + 1
+    int dld;        // stride between per-iteration dot vectors (>= 2(m+1))
+    double* H;      // (m+1) x m, col-major, ld = ldh
+    double* HP;     // (m+1) x m, Alg. 3 provisional column r^(4) (reading R1)
+    double* L;      // m x m strictly lower, col-major, ld = m
+    double* R;      // Givens-rotated copy of H, ld = ldh
+    double* cs;     // [m] rotation cosines
+    double* sn;     // [m] rotation sines
+    double* g;      // [m+2] rotated rhs rho e1
+    double* dots;   // [(m+1) * dld] reduced dot vector of iteration p at dots + p*dld
+    double* alpha;  // [m+1] update coefficients (r^(2)) for v_p
+    double* beta;   // [m+1] update coefficients (r^(1)) for u'
+    double* y;      // [m+1] least-squares solution
+    double* scal;   // [SC_COUNT]
+    int* istate;    // [ST_COUNT]
+    double* res_hist;  // [kmax+1]
+};
+
+// ---- launchers (kernels.cu) -----------------------------------------------------------
+struct SpmvArgs {
+    int64_t nrows;
+    const void* rowptr;  // int32 or int64 (ptr64)
+    const void* col;     // int32 or int64 (idx64), local column space [0, nloc + nghost)
+    const double* val;
+    int ptr64, idx64, lpr;
+    int64_t nloc;
+    const double* ghost;  // NULL when no ghosts
+};
+// y = A x  (resid: y = b - A x).  istate may be NULL (no status check).
+void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                 const int* istate, cudaStream_t s);
+
+// Fused block dot: out = [V_p^T u, u.u, V_p^T z, u.z] (z != NULL) or [V_p^T u, u.u].
+// part: [grid * 2(p+1)] scratch, counter: one zeroed unsigned (reset by the kernel).
+int bdot_grid_size(int64_t n, int num_sms);
+void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                      const double* z, double* out, double* part, unsigned* counter, int grid,
+                      const int* istate, cudaStream_t s);
+
+// Fused update (see igs.h igs_op_update).  gamma read from *gamma_dev.
+// istate/it: when istate != NULL the mode bits istate[ST_MODE] (valid iff
+// istate[ST_MODE_IT] == it) select what is written; else mode = v (+ u' if u_next).
+void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                   const double* z, const double* alpha, const double* beta,
+                   const double* gamma_dev, double* v_out, double* u_next, const int* istate,
+                   int it, cudaStream_t s);
+
+// x += V[:, :p] y with p = istate[ST_PDONE]
+void launch_xupdate(int64_t n, const double* V, int64_t ld, const double* y, double* x,
+                    const int* istate, int pmax, cudaStream_t s);
+
+// Small steps (one CTA, replicated on every rank).
+enum SmallStage : int { SS_PRIME_NORM = 0, SS_PRIME_H = 1, SS_ITER = 2, SS_LSQ = 3 };
+void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s);
+
+// x = (I + L)^{-1} b (test entry point; same device routine as the small step).
+void launch_trisolve(int order, const double* L, int ldl, const double* b, double* x,
+                     cudaStream_t s);
+
+// Gram matrix of V[:, :c] (local rows) into G (c x c) ; then ||I - G||_F into *out.
+void launch_gram(int64_t n, int c, const double* V, int64_t ld, double* part, int splits,
+                 double* G, cudaStream_t s);
+void launch_loo_norm(int c, const double* G, double* out, cudaStream_t s);
+
+// halo pack: buf[i] = x[idx[i]]
+void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, const int* istate,
+                 cudaStream_t s);
+
+// small helpers
+void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
+
+}  // namespace igs

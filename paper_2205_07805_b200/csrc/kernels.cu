@@ -1,0 +1,831 @@
+// kernels.cu -- the CUDA kernels of the IGS-GMRES hot path for B200 (sm_100a).
+//
+// P:n = PAPER.md line n (arXiv 2205.07805).  Every kernel is FP64 and HBM- or
+// latency-bound: no tensor cores on the iteration path.
+//
+//   spmv_kernel          z = A u, CSR, LPR lanes per row            (Alg. 3 Step 4)
+//   bdot_kernel          [V_p, u]^T [u, z], one read of V_p, deterministic two-stage
+//                        reduction, last CTA finishes
+//   small_kernel         one CTA: (I+L)^{-1} r2, lagged norm, Stephen's trick, H column,
+//                        Givens, status
+//   update_kernel        v_p = (u - V_p r2)/gamma, u' = z/gamma - V_{p+1} r1, one read of
+//                        V_p (the paper's "merge ... into one GPU kernel")
+//   xupdate_kernel       x += V_p y
+//   gram/loo kernels     ||I - V^T V||_F diagnostic
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "igs_internal.cuh"
+
+namespace igs {
+
+#define FULL_MASK 0xffffffffu
+
+// ------------------------------------------------------------------------------------
+// small utilities
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double2 ld2_guard(const double* __restrict__ p, int64_t r, int64_t n) {
+    if (r + 1 < n) return __ldg(reinterpret_cast<const double2*>(p + r));
+    double2 v;
+    v.x = (r < n) ? __ldg(p + r) : 0.0;
+    v.y = 0.0;
+    return v;
+}
+
+__device__ __forceinline__ bool running(const int* istate) {
+    return istate == nullptr || *(volatile const int*)(istate + ST_STATUS) == RUNNING;
+}
+
+// ------------------------------------------------------------------------------------
+// K1: CSR SpMV with LPR lanes per row (LPR in {1,2,4,8,16,32}).
+//   Local column space: c < nloc -> x[c], else ghost[c - nloc] (halo, multi-GPU).
+// ------------------------------------------------------------------------------------
+template <int LPR, typename IT, typename PT, bool GHOST, bool RESID>
+__global__ void __launch_bounds__(256) spmv_kernel(int64_t nrows, const PT* __restrict__ rowptr,
+                                                   const IT* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   const double* __restrict__ ghost, int64_t nloc,
+                                                   double* __restrict__ y,
+                                                   const double* __restrict__ b,
+                                                   const int* istate) {
+    if (!running(istate)) return;
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t row = gtid / LPR;
+    const int sub = threadIdx.x % LPR;
+    const bool valid = row < nrows;  // no early exit: the whole warp joins the shuffles
+    const int64_t q0 = valid ? (int64_t)__ldg(rowptr + row) : 0;
+    const int64_t q1 = valid ? (int64_t)__ldg(rowptr + row + 1) : 0;
+    double s = 0.0;
+    for (int64_t q = q0 + sub; q < q1; q += LPR) {
+        const int64_t c = (int64_t)__ldg(col + q);
+        double xv;
+        if (GHOST && c >= nloc) xv = __ldg(ghost + (c - nloc));
+        else xv = __ldg(x + c);
+        s = fma(__ldg(val + q), xv, s);
+    }
+#pragma unroll
+    for (int off = LPR / 2; off > 0; off >>= 1) s += __shfl_xor_sync(FULL_MASK, s, off, LPR);
+    if (valid && sub == 0) y[row] = RESID ? b[row] - s : s;
+}
+
+// CSR-stream SpMV for short rows (mean <= SPS_MAX_AVG nnz/row): a CTA owns 256 consecutive
+// rows; its products val[q]*x[col[q]] are formed with fully coalesced val/col loads into
+// shared memory, then thread t sums row t's products left to right -- the same rounding
+// sequence as a sequential CSR row loop (product, then add), with none of the per-row
+// lane waste of vector CSR at ~7 nnz/row.
+constexpr int SPS_ROWS = 256;
+constexpr int SPS_CAP = SPS_ROWS * 14;  // products staged in smem (28 KB)
+
+template <typename IT, typename PT, bool GHOST, bool RESID>
+__global__ void __launch_bounds__(SPS_ROWS)
+    spmv_stream_kernel(int64_t nrows, const PT* __restrict__ rowptr, const IT* __restrict__ col,
+                       const double* __restrict__ val, const double* __restrict__ x,
+                       const double* __restrict__ ghost, int64_t nloc, double* __restrict__ y,
+                       const double* __restrict__ b, const int* istate) {
+    if (!running(istate)) return;
+    __shared__ double prod[SPS_CAP];
+    const int64_t r0 = (int64_t)blockIdx.x * SPS_ROWS;
+    const int64_t r = r0 + threadIdx.x;
+    const int64_t rl = (r0 + SPS_ROWS < nrows) ? r0 + SPS_ROWS : nrows;
+    const int64_t q0 = (int64_t)__ldg(rowptr + r0), q1 = (int64_t)__ldg(rowptr + rl);
+    const int64_t cnt = q1 - q0;
+    if (cnt <= SPS_CAP) {
+#pragma unroll 4
+        for (int64_t i = threadIdx.x; i < cnt; i += SPS_ROWS) {
+            const int64_t c = (int64_t)__ldg(col + q0 + i);
+            double xv;
+            if (GHOST && c >= nloc) xv = __ldg(ghost + (c - nloc));
+            else xv = __ldg(x + c);
+            prod[i] = __dmul_rn(__ldg(val + q0 + i), xv);
+        }
+        __syncthreads();
+        if (r < nrows) {
+            const int a = (int)((int64_t)__ldg(rowptr + r) - q0), e = (int)((int64_t)__ldg(rowptr + r + 1) - q0);
+            double s = 0.0;
+            for (int q = a; q < e; q++) s = __dadd_rn(s, prod[q]);
+            y[r] = RESID ? b[r] - s : s;
+        }
+    } else if (r < nrows) {  // unusually long rows in this block: plain row loop
+        double s = 0.0;
+        for (int64_t q = __ldg(rowptr + r); q < (int64_t)__ldg(rowptr + r + 1); q++) {
+            const int64_t c = (int64_t)__ldg(col + q);
+            const double xv = (GHOST && c >= nloc) ? __ldg(ghost + (c - nloc)) : __ldg(x + c);
+            s = __dadd_rn(s, __dmul_rn(__ldg(val + q), xv));
+        }
+        y[r] = RESID ? b[r] - s : s;
+    }
+}
+
+template <typename IT, typename PT>
+static void spmv_stream(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                        const int* istate, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((a.nrows + SPS_ROWS - 1) / SPS_ROWS);
+    if (blocks == 0) return;
+    const PT* rp = static_cast<const PT*>(a.rowptr);
+    const IT* ci = static_cast<const IT*>(a.col);
+    if (a.ghost) {
+        if (resid) spmv_stream_kernel<IT, PT, true, true><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+        else spmv_stream_kernel<IT, PT, true, false><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+    } else {
+        if (resid) spmv_stream_kernel<IT, PT, false, true><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
+        else spmv_stream_kernel<IT, PT, false, false><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
+    }
+}
+
+template <int LPR, typename IT, typename PT>
+static void spmv_dispatch_g(const SpmvArgs& a, const double* x, double* y, const double* b,
+                            bool resid, const int* istate, cudaStream_t s) {
+    const int threads = 256;
+    const int64_t nthreads = a.nrows * LPR;
+    const unsigned blocks = (unsigned)((nthreads + threads - 1) / threads);
+    if (blocks == 0) return;
+    const PT* rp = static_cast<const PT*>(a.rowptr);
+    const IT* ci = static_cast<const IT*>(a.col);
+    if (a.ghost) {
+        if (resid) spmv_kernel<LPR, IT, PT, true, true><<<blocks, threads, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+        else spmv_kernel<LPR, IT, PT, true, false><<<blocks, threads, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+    } else {
+        if (resid) spmv_kernel<LPR, IT, PT, false, true><<<blocks, threads, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
+        else spmv_kernel<LPR, IT, PT, false, false><<<blocks, threads, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
+    }
+}
+
+template <typename IT, typename PT>
+static void spmv_dispatch_l(const SpmvArgs& a, const double* x, double* y, const double* b,
+                            bool resid, const int* istate, cudaStream_t s) {
+    if (a.lpr == 0) { spmv_stream<IT, PT>(a, x, y, b, resid, istate, s); return; }
+    switch (a.lpr) {
+        case 1: spmv_dispatch_g<1, IT, PT>(a, x, y, b, resid, istate, s); break;
+        case 2: spmv_dispatch_g<2, IT, PT>(a, x, y, b, resid, istate, s); break;
+        case 4: spmv_dispatch_g<4, IT, PT>(a, x, y, b, resid, istate, s); break;
+        case 8: spmv_dispatch_g<8, IT, PT>(a, x, y, b, resid, istate, s); break;
+        case 16: spmv_dispatch_g<16, IT, PT>(a, x, y, b, resid, istate, s); break;
+        default: spmv_dispatch_g<32, IT, PT>(a, x, y, b, resid, istate, s); break;
+    }
+}
+
+void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                 const int* istate, cudaStream_t s) {
+    if (a.idx64) {
+        if (a.ptr64) spmv_dispatch_l<int64_t, int64_t>(a, x, y, b, resid, istate, s);
+        else spmv_dispatch_l<int64_t, int32_t>(a, x, y, b, resid, istate, s);
+    } else {
+        if (a.ptr64) spmv_dispatch_l<int32_t, int64_t>(a, x, y, b, resid, istate, s);
+        else spmv_dispatch_l<int32_t, int32_t>(a, x, y, b, resid, istate, s);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// K2: fused block dot  [V_p, u]^T [u, z]   (one read of V_p, u and z per iteration)
+//
+// CTA = 8 warps; tile = 1024 rows; a lane owns rows {2l, 2l+1, 64+2l, 65+2l} of its warp's
+// 128-row slice (two coalesced 16-B loads per column).  Columns are processed in groups of
+// 8: each lane forms 8 (x2) row-partial dots, a butterfly transpose-reduction (9 shuffles
+// per vector instead of 40) leaves column (lane>>2)'s warp total in lanes 4c..4c+3, and a
+// per-warp shared accumulator carries it across the CTA's tiles.  Stage 2: fixed-order sum
+// over warps -> per-CTA partial in global memory; the last CTA to finish (ticket counter)
+// sums the partials in CTA order.  No floating-point atomics: bitwise deterministic.
+// ------------------------------------------------------------------------------------
+constexpr int BD_WARPS = 8;
+constexpr int BD_THREADS = BD_WARPS * 32;
+constexpr int BD_ROWS_W = 128;
+constexpr int BD_TILE = BD_WARPS * BD_ROWS_W;
+constexpr int BD_CG = 8;
+
+__device__ __forceinline__ double bfly8(double (&a)[8], int lane) {
+    // 8 values per lane -> lane holds column (lane >> 2) summed over the warp
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const bool up = lane & 16;
+        const double send = up ? a[i] : a[i + 4];
+        const double keep = up ? a[i + 4] : a[i];
+        a[i] = keep + __shfl_xor_sync(FULL_MASK, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const bool up = lane & 8;
+        const double send = up ? a[i] : a[i + 2];
+        const double keep = up ? a[i + 2] : a[i];
+        a[i] = keep + __shfl_xor_sync(FULL_MASK, send, 8);
+    }
+    {
+        const bool up = lane & 4;
+        const double send = up ? a[0] : a[1];
+        const double keep = up ? a[1] : a[0];
+        a[0] = keep + __shfl_xor_sync(FULL_MASK, send, 4);
+    }
+    a[0] += __shfl_xor_sync(FULL_MASK, a[0], 2);
+    a[0] += __shfl_xor_sync(FULL_MASK, a[0], 1);
+    return a[0];
+}
+
+template <bool GUARD>
+__device__ __forceinline__ double2 bd_ld(const double* __restrict__ p, int64_t r, int64_t n) {
+    if (GUARD) return ld2_guard(p, r, n);
+    return __ldg(reinterpret_cast<const double2*>(p + r));
+}
+
+// one 1024-row tile for this warp's 128 rows: all column groups, accumulated into acc
+template <int NV, bool GUARD>
+__device__ __forceinline__ void bdot_tile(int64_t n, int p, int ncols, const double* __restrict__ V,
+                                          int64_t ld, const double* __restrict__ u,
+                                          const double* __restrict__ z, int64_t r0, int64_t r1,
+                                          double* acc, int lane) {
+    const double2 u0 = bd_ld<GUARD>(u, r0, n), u1 = bd_ld<GUARD>(u, r1, n);
+    double2 z0 = make_double2(0.0, 0.0), z1 = z0;
+    if (NV == 2) { z0 = bd_ld<GUARD>(z, r0, n); z1 = bd_ld<GUARD>(z, r1, n); }
+    for (int cg = 0; cg < ncols; cg += BD_CG) {
+        double2 va[BD_CG], vb[BD_CG];
+#pragma unroll
+        for (int c = 0; c < BD_CG; c++) {   // all loads first: 16 x 16 B in flight per lane
+            const int j = min(cg + c, ncols - 1);
+            const double* col = (j < p) ? V + (int64_t)j * ld : u;
+            va[c] = bd_ld<GUARD>(col, r0, n);
+            vb[c] = bd_ld<GUARD>(col, r1, n);
+        }
+        double au[BD_CG], az[BD_CG];
+#pragma unroll
+        for (int c = 0; c < BD_CG; c++) {
+            const bool live = cg + c < ncols;
+            const double2 v0 = va[c], v1 = vb[c];
+            au[c] = live ? fma(v1.y, u1.y, fma(v1.x, u1.x, fma(v0.y, u0.y, v0.x * u0.x))) : 0.0;
+            az[c] = 0.0;
+            if (NV == 2) az[c] = live ? fma(v1.y, z1.y, fma(v1.x, z1.x, fma(v0.y, z0.y, v0.x * z0.x))) : 0.0;
+        }
+        const double su = bfly8(au, lane);
+        double sz = 0.0;
+        if (NV == 2) sz = bfly8(az, lane);
+        const int j = cg + (lane >> 2);
+        if ((lane & 3) == 0 && j < ncols) {
+            acc[j] += su;
+            if (NV == 2) acc[ncols + j] += sz;
+        }
+    }
+}
+
+template <int NV>
+__global__ void __launch_bounds__(BD_THREADS, 2)
+    bdot_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
+                const double* __restrict__ u, const double* __restrict__ z,
+                double* __restrict__ part, double* __restrict__ out, unsigned* counter,
+                const int* istate) {
+    if (!running(istate)) return;
+    extern __shared__ double sacc[];  // [BD_WARPS][NV * ncols]
+    __shared__ bool s_last;
+    const int ncols = p + 1;  // columns 0..p-1 of V, then u itself
+    const int stride = NV * ncols;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* acc = sacc + warp * stride;
+    for (int i = lane; i < stride; i += 32) acc[i] = 0.0;
+    __syncwarp();
+
+    const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * BD_TILE + warp * BD_ROWS_W + 2 * lane;
+        const int64_t r1 = r0 + 64;
+        if ((tile + 1) * BD_TILE <= n) bdot_tile<NV, false>(n, p, ncols, V, ld, u, z, r0, r1, acc, lane);
+        else bdot_tile<NV, true>(n, p, ncols, V, ld, u, z, r0, r1, acc, lane);
+    }
+    __syncthreads();
+    // stage 2a: fixed-order sum over warps -> this CTA's partial
+    for (int i = threadIdx.x; i < stride; i += BD_THREADS) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < BD_WARPS; w++) s += sacc[w * stride + i];
+        part[(int64_t)blockIdx.x * stride + i] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // stage 2b: last CTA sums the partials in CTA order
+    for (int i = threadIdx.x; i < stride; i += BD_THREADS) {
+        double s = 0.0;
+        for (int bb = 0; bb < (int)gridDim.x; bb++) s += __ldcg(part + (int64_t)bb * stride + i);
+        out[i] = s;  // layout: [V_p^T u (p), u.u, V_p^T z (p), u.z]
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
+static size_t bdot_smem(int p, int nv) { return (size_t)BD_WARPS * nv * (p + 1) * sizeof(double); }
+
+int bdot_grid_size(int64_t n, int num_sms) {
+    const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
+    int64_t g = (int64_t)num_sms * 2;
+    if (g > ntiles) g = ntiles;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                      const double* z, double* out, double* part, unsigned* counter, int grid,
+                      const int* istate, cudaStream_t s) {
+    const int nv = z ? 2 : 1;
+    const size_t smem = bdot_smem(p, nv);
+    if (nv == 2) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(bdot_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        bdot_kernel<2><<<grid, BD_THREADS, smem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+    } else {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(bdot_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        bdot_kernel<1><<<grid, BD_THREADS, smem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// K5: fused update with lagged normalisation (one read of V_p)
+//   w = u - V_p alpha  (HAS_ALPHA; Alg. 3 Step 10 "Jacobi iteration")  or w = u
+//   v = w / gamma                                     (Step 11 / Alg. 2 Step 7)
+//   u' = z / gamma - (V_p beta[:p] + v beta[p])       (Step 13)
+// Each thread owns two consecutive rows (16-B loads); columns unrolled 8-deep.
+// ------------------------------------------------------------------------------------
+constexpr int UP_THREADS = 256;
+
+template <bool HAS_ALPHA>
+__global__ void __launch_bounds__(UP_THREADS)
+    update_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
+                  const double* u, const double* __restrict__ z,
+                  const double* __restrict__ alpha, const double* __restrict__ beta,
+                  const double* __restrict__ gamma_dev, double* v_out, double* u_next,
+                  const int* istate, int it, int default_mode) {
+    extern __shared__ double coef[];  // alpha[p] | beta[p+1]
+    int mode = default_mode;
+    if (istate) {
+        const volatile int* vs = istate;
+        mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
+    }
+    if (mode == 0) return;
+    const bool want_next = (mode & 2) != 0;
+    double* sa = coef;
+    double* sb = coef + p;
+    if (HAS_ALPHA)
+        for (int j = threadIdx.x; j < p; j += blockDim.x) sa[j] = alpha[j];
+    if (want_next)
+        for (int j = threadIdx.x; j <= p; j += blockDim.x) sb[j] = beta[j];
+    __syncthreads();
+    const double gamma = *gamma_dev;
+    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (r >= n) return;
+    const bool pair = (r + 1 < n);
+    double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
+    if (HAS_ALPHA || want_next) {
+        int j = 0;
+        if (pair) {
+            for (; j + 8 <= p; j += 8) {
+                double2 v[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) v[c] = __ldg(reinterpret_cast<const double2*>(V + (int64_t)(j + c) * ld + r));
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
+                    if (want_next) { t2.x = fma(v[c].x, sb[j + c], t2.x); t2.y = fma(v[c].y, sb[j + c], t2.y); }
+                }
+            }
+        }
+        for (; j < p; j++) {
+            const double2 v = ld2_guard(V + (int64_t)j * ld, r, n);
+            if (HAS_ALPHA) { t1.x = fma(v.x, sa[j], t1.x); t1.y = fma(v.y, sa[j], t1.y); }
+            if (want_next) { t2.x = fma(v.x, sb[j], t2.x); t2.y = fma(v.y, sb[j], t2.y); }
+        }
+    }
+    const double2 uu = ld2_guard(u, r, n);
+    double2 w = uu;
+    if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
+    double2 v;
+    v.x = w.x / gamma;
+    v.y = w.y / gamma;
+    if (want_next) {
+        const double2 zz = ld2_guard(z, r, n);
+        const double bp = sb[p];
+        double2 un;
+        un.x = zz.x / gamma - fma(v.x, bp, t2.x);
+        un.y = zz.y / gamma - fma(v.y, bp, t2.y);
+        u_next[r] = un.x;
+        if (pair) u_next[r + 1] = un.y;
+    }
+    if (mode & 1) {
+        v_out[r] = v.x;
+        if (pair) v_out[r + 1] = v.y;
+    }
+}
+
+void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                   const double* z, const double* alpha, const double* beta,
+                   const double* gamma_dev, double* v_out, double* u_next, const int* istate,
+                   int it, cudaStream_t s) {
+    const int64_t nthreads = (n + 1) / 2;
+    const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
+    if (blocks == 0) return;
+    const size_t smem = (size_t)(2 * p + 1) * sizeof(double);
+    const int dmode = 1 | (u_next ? 2 : 0);
+    if (alpha) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_kernel<true><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode);
+    } else {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_kernel<false><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode);
+    }
+}
+
+// x += V[:, :p] y   (p = istate[ST_PDONE])
+__global__ void __launch_bounds__(UP_THREADS)
+    xupdate_kernel(int64_t n, const double* __restrict__ V, int64_t ld,
+                   const double* __restrict__ y, double* x, const int* istate) {
+    extern __shared__ double sy[];
+    const int p = istate[ST_PDONE];
+    for (int j = threadIdx.x; j < p; j += blockDim.x) sy[j] = y[j];
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n || p == 0) return;
+    double t = 0.0;
+    int j = 0;
+    for (; j + 8 <= p; j += 8) {
+        double v[8];
+#pragma unroll
+        for (int c = 0; c < 8; c++) v[c] = __ldg(V + (int64_t)(j + c) * ld + r);
+#pragma unroll
+        for (int c = 0; c < 8; c++) t = fma(v[c], sy[j + c], t);
+    }
+    for (; j < p; j++) t = fma(__ldg(V + (int64_t)j * ld + r), sy[j], t);
+    x[r] = x[r] + t;
+}
+
+void launch_xupdate(int64_t n, const double* V, int64_t ld, const double* y, double* x,
+                    const int* istate, int pmax, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((n + UP_THREADS - 1) / UP_THREADS);
+    if (blocks == 0) return;
+    xupdate_kernel<<<blocks, UP_THREADS, (size_t)(pmax + 1) * sizeof(double), s>>>(n, V, ld, y, x, istate);
+}
+
+// ------------------------------------------------------------------------------------
+// K4: the small step (one CTA, replicated on every rank from the bit-identical reduced
+// dot vector).  Deterministic block reductions; forward substitution column by column.
+// ------------------------------------------------------------------------------------
+constexpr int SS_THREADS = 256;
+
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(FULL_MASK, v, off);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(FULL_MASK, t, off);
+        if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+// x <- (I + L)^{-1} x in shared memory (forward substitution, natural order)
+__device__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, double* x) {
+    for (int j = 0; j < order; j++) {
+        __syncthreads();
+        const double xj = x[j];
+        for (int i = j + 1 + threadIdx.x; i < order; i += blockDim.x)
+            x[i] = x[i] - L[i + (int64_t)j * ldl] * xj;
+    }
+    __syncthreads();
+}
+
+// Givens rotation of H column j into R, update g; thread 0 does the
+// sequential part from shared copies.  Returns |g[j+1]| to all threads.
+__device__ double givens_column(const Dev& d, int j, double* col, double* scs, double* ssn,
+                                double* red) {
+    const double* Hj = d.H + (int64_t)j * d.ldh;
+    for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) col[i] = Hj[i];
+    for (int i = threadIdx.x; i < j; i += blockDim.x) { scs[i] = d.cs[i]; ssn[i] = d.sn[i]; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double carry = col[0];
+        for (int i = 0; i < j; i++) {
+            const double a = carry, b = col[i + 1];
+            col[i] = scs[i] * a + ssn[i] * b;
+            carry = -ssn[i] * a + scs[i] * b;
+        }
+        const double a = carry, b = col[j + 1];
+        const double dd = hypot(a, b);
+        double c = 1.0, s = 0.0;
+        if (dd != 0.0) { c = a / dd; s = b / dd; }
+        d.cs[j] = c;
+        d.sn[j] = s;
+        col[j] = dd;
+        col[j + 1] = 0.0;
+        const double gj = d.g[j];
+        d.g[j + 1] = -s * gj;
+        d.g[j] = c * gj;
+        red[33] = fabs(-s * gj);
+    }
+    __syncthreads();
+    double* Rj = d.R + (int64_t)j * d.ldh;
+    for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) Rj[i] = col[i];
+    const double res = red[33];
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(SS_THREADS)
+    small_kernel(Dev d, int stage, int gs, int p, int m, int t0) {
+    extern __shared__ double sm[];
+    __shared__ double red[40];
+    const int M = d.m;
+    double* s_a = sm;               // [M+1]  r2 (Alg. 3) / a (Alg. 2)
+    double* s_c = s_a + (M + 1);    // [M+2]  c (and d)
+    double* s_x = s_c + (M + 2);    // [M+2]  r3 / r1
+    double* s_col = s_x + (M + 2);  // [M+2]  Givens column
+    double* s_cs = s_col + (M + 2); // [M+1]
+    double* s_sn = s_cs + (M + 1);  // [M+1]
+    double* s_t = s_sn + (M + 1);   // [M+1]  r2/gamma
+    int* ist = d.istate;
+    const int tid = threadIdx.x;
+
+    if (stage == SS_PRIME_NORM) {  // rho = ||r||, v_0 = r / rho
+        if (tid == 0) {
+            const double s = d.dots[0];
+            const double rho = sqrt(s);
+            d.g[0] = rho;
+            d.scal[SC_RHO] = rho;
+            d.scal[SC_GAMMA] = rho;
+            ist[ST_STATUS] = isfinite(rho) ? RUNNING : STOP_NONFINITE;
+            ist[ST_PDONE] = 0;
+            ist[ST_BASIS] = 0;
+            ist[ST_MODE] = 1;
+            ist[ST_MODE_IT] = 0;
+        }
+        return;
+    }
+    if (stage == SS_PRIME_H) {  // H_11 = v_1^T A v_1, u = A v_1 - H_11 v_1 (reading R2)
+        if (tid == 0) {
+            if (ist[ST_STATUS] != RUNNING) { ist[ST_MODE] = 0; return; }
+            const double h = d.dots[1];
+            if (gs == 1) d.H[0] = h;
+            else d.HP[0] = h;
+            d.beta[0] = h;
+            d.scal[SC_GAMMA] = 1.0;
+            ist[ST_BASIS] = 1;
+            ist[ST_MODE] = isfinite(h) ? 2 : 0;
+            ist[ST_MODE_IT] = 0;
+            if (!isfinite(h)) ist[ST_STATUS] = STOP_NONFINITE;
+        }
+        return;
+    }
+    if (stage == SS_LSQ) {  // y = R^{-1} g  (back substitution)
+        const int pp = ist[ST_PDONE];
+        for (int i = tid; i < pp; i += blockDim.x) s_x[i] = d.g[i];
+        for (int j = pp - 1; j >= 0; j--) {
+            __syncthreads();
+            if (tid == 0) s_x[j] = s_x[j] / d.R[j + (int64_t)j * d.ldh];
+            __syncthreads();
+            const double yj = s_x[j];
+            for (int i = tid; i < j; i += blockDim.x) s_x[i] = s_x[i] - d.R[i + (int64_t)j * d.ldh] * yj;
+        }
+        __syncthreads();
+        for (int i = tid; i < pp; i += blockDim.x) d.y[i] = s_x[i];
+        return;
+    }
+
+    // ---------------- SS_ITER: iteration p >= 1 --------------------------------------
+    if (*(volatile int*)(ist + ST_STATUS) != RUNNING) return;
+    const double* dv = d.dots + (int64_t)p * d.dld;
+    const bool drain = (p == m);
+    const double tol = d.scal[SC_TOL], nb = d.scal[SC_NB];
+    for (int i = tid; i < p; i += blockDim.x) s_a[i] = dv[i];
+    if (!drain) for (int i = tid; i <= p; i += blockDim.x) s_c[i] = dv[p + 1 + i];
+    const double s = dv[p];
+    __syncthreads();
+
+    double gamma, hn2;
+    bool bd;
+    if (gs == 2) {
+        // Step 5: r3 = (I + L_p)^{-1} r2    (r3 only feeds H, Step 14)
+        for (int i = tid; i < p; i += blockDim.x) s_x[i] = s_a[i];
+        trisolve_smem(p, d.L, M, s_x);
+        // Step 6: lagged norm gamma = sqrt(||u||^2 - ||r2||^2)
+        double part = 0.0;
+        for (int i = tid; i < p; i += blockDim.x) part += s_a[i] * s_a[i];
+        const double nr2 = block_sum(part, red);
+        const double t = s - nr2;
+        gamma = t > 0.0 ? sqrt(t) : 0.0;
+        // Step 14: H[:p, p-1] = hp[:p, p-1] + r3 ; H[p, p-1] = gamma  (reading R3)
+        double h2 = 0.0;
+        for (int i = tid; i < p; i += blockDim.x) {
+            const double h = d.HP[i + (int64_t)(p - 1) * d.ldh] + s_x[i];
+            d.H[i + (int64_t)(p - 1) * d.ldh] = h;
+            h2 += h * h;
+        }
+        hn2 = block_sum(h2, red);
+        bd = !(t > kBreakdownC * kEps * s) || !(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma));
+    } else {
+        // Alg. 2 Step 6: gamma = ||w_{k-1}||  (fused into the single reduction)
+        gamma = sqrt(s);
+        double h2 = 0.0;
+        for (int i = tid; i < p; i += blockDim.x) {
+            const double h = d.H[i + (int64_t)(p - 1) * d.ldh];
+            h2 += h * h;
+        }
+        hn2 = block_sum(h2, red);
+        bd = !(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma));
+    }
+    if (tid == 0) d.H[p + (int64_t)(p - 1) * d.ldh] = gamma;  // gamma_{k-1} = H_{k-1,k-2}
+    __syncthreads();
+    const double res = givens_column(d, p - 1, s_col, s_cs, s_sn, red);
+    const bool nonfinite = !isfinite(s) || !isfinite(res) || !isfinite(hn2);
+    const bool conv = tol > 0.0 && res <= tol * nb;
+    if (tid == 0) {
+        d.res_hist[t0 + p] = res / nb;
+        ist[ST_PDONE] = p;
+        ist[ST_MODE_IT] = p;
+        if (nonfinite) { ist[ST_STATUS] = STOP_NONFINITE; ist[ST_MODE] = 0; }
+        else if (bd) { ist[ST_STATUS] = STOP_BREAKDOWN; ist[ST_MODE] = 0; ist[ST_BASIS] = p; }
+        else {
+            d.scal[SC_GAMMA] = gamma;
+            ist[ST_BASIS] = p + 1;
+            if (conv || drain) { ist[ST_STATUS] = conv ? STOP_CONVERGED : STOP_END; ist[ST_MODE] = 1; }
+            else ist[ST_MODE] = 3;
+        }
+    }
+    if (nonfinite || bd || conv || drain) {
+        if (gs == 2) for (int i = tid; i < p; i += blockDim.x) d.alpha[i] = s_a[i];  // v_p still written
+        return;
+    }
+    __syncthreads();
+
+    if (gs == 2) {
+        // Steps 7-9: c /= gamma ; d /= gamma^2 ; L[p, :p] = r2 / gamma  (reading R4)
+        const double dd = s_c[p] / (gamma * gamma);
+        double part = 0.0;
+        for (int i = tid; i < p; i += blockDim.x) {
+            const double ci = s_c[i] / gamma;
+            const double li = s_a[i] / gamma;
+            s_c[i] = ci;
+            s_t[i] = li;
+            d.L[p + (int64_t)i * M] = li;
+            part += li * ci;
+            d.alpha[i] = s_a[i];
+        }
+        // Step 12 (Stephen's trick): r1 = [c ; d - L[p,:p] . c]
+        const double acc = block_sum(part, red);
+        for (int i = tid; i < p; i += blockDim.x) { d.beta[i] = s_c[i]; s_x[i] = s_c[i]; }
+        if (tid == 0) { const double r1p = dd - acc; d.beta[p] = r1p; s_x[p] = r1p; }
+        __syncthreads();
+        // Step 15, derived (reading R1): hp[:p+1, p] = r1 - H[:p+1, :p] (r2 / gamma)
+        for (int i = tid; i <= p; i += blockDim.x) {
+            double sacc = 0.0;
+            for (int j = 0; j < p; j++) sacc += d.H[i + (int64_t)j * d.ldh] * s_t[j];
+            d.HP[i + (int64_t)p * d.ldh] = s_x[i] - sacc;
+        }
+    } else {
+        // Alg. 2 Steps 8-10: c /= gamma ; c[p] /= gamma ; L[p, :p] = a / gamma
+        for (int i = tid; i <= p; i += blockDim.x) {
+            double ci = s_c[i] / gamma;
+            if (i == p) ci = ci / gamma;  // reading R5
+            s_x[i] = ci;
+        }
+        for (int i = tid; i < p; i += blockDim.x) d.L[p + (int64_t)i * M] = s_a[i] / gamma;
+        __syncthreads();
+        // Step 12: r1 = (I + L_{p+1})^{-1} c ; Step 17 (r3 = 0): H[:p+1, p] = r1
+        trisolve_smem(p + 1, d.L, M, s_x);
+        for (int i = tid; i <= p; i += blockDim.x) {
+            d.beta[i] = s_x[i];
+            d.H[i + (int64_t)p * d.ldh] = s_x[i];
+        }
+    }
+}
+
+static size_t small_smem(int M) { return (size_t)(7 * (M + 2)) * sizeof(double); }
+
+void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s) {
+    const size_t smem = small_smem(d.m);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    small_kernel<<<1, SS_THREADS, smem, s>>>(d, stage, gs, p, m, t0);
+}
+
+__global__ void __launch_bounds__(SS_THREADS)
+    trisolve_kernel(int order, const double* L, int ldl, const double* b, double* x) {
+    extern __shared__ double sx[];
+    for (int i = threadIdx.x; i < order; i += blockDim.x) sx[i] = b[i];
+    trisolve_smem(order, L, ldl, sx);
+    for (int i = threadIdx.x; i < order; i += blockDim.x) x[i] = sx[i];
+}
+
+void launch_trisolve(int order, const double* L, int ldl, const double* b, double* x,
+                     cudaStream_t s) {
+    const size_t smem = (size_t)(order + 1) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(trisolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    trisolve_kernel<<<1, SS_THREADS, smem, s>>>(order, L, ldl, b, x);
+}
+
+// ------------------------------------------------------------------------------------
+// LOO diagnostic: G = V^T V (tiled, deterministic), ||I - G||_F
+// ------------------------------------------------------------------------------------
+constexpr int GR_T = 32, GR_R = 64;
+
+__global__ void __launch_bounds__(256)
+    gram_kernel(int64_t n, int c, const double* __restrict__ V, int64_t ld,
+                double* __restrict__ part, int ntile) {
+    __shared__ double A[GR_T][GR_R + 1];
+    __shared__ double B[GR_T][GR_R + 1];
+    // tile pair (ti <= tj) from blockIdx.x
+    int idx = blockIdx.x, ti = 0;
+    while (idx >= ntile - ti) { idx -= ntile - ti; ti++; }
+    const int tj = ti + idx;
+    const int split = blockIdx.y, splits = gridDim.y;
+    const int64_t chunk = (n + splits - 1) / splits;
+    const int64_t rbeg = (int64_t)split * chunk;
+    const int64_t rend = rbeg + chunk < n ? rbeg + chunk : n;
+    const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int64_t r0 = rbeg; r0 < rend; r0 += GR_R) {
+        for (int e = threadIdx.x; e < GR_T * GR_R; e += 256) {
+            const int cc = e / GR_R, rr = e % GR_R;
+            const int64_t row = r0 + rr;
+            const int ca = ti * GR_T + cc, cb = tj * GR_T + cc;
+            A[cc][rr] = (row < rend && ca < c) ? V[(int64_t)ca * ld + row] : 0.0;
+            B[cc][rr] = (row < rend && cb < c) ? V[(int64_t)cb * ld + row] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int rr = 0; rr < GR_R; rr++) {
+            const double a0 = A[2 * ty][rr], a1 = A[2 * ty + 1][rr];
+            const double b0 = B[2 * tx][rr], b1 = B[2 * tx + 1][rr];
+            acc[0][0] = fma(a0, b0, acc[0][0]);
+            acc[0][1] = fma(a0, b1, acc[0][1]);
+            acc[1][0] = fma(a1, b0, acc[1][0]);
+            acc[1][1] = fma(a1, b1, acc[1][1]);
+        }
+        __syncthreads();
+    }
+    for (int a = 0; a < 2; a++)
+        for (int b = 0; b < 2; b++) {
+            const int i = ti * GR_T + 2 * ty + a, j = tj * GR_T + 2 * tx + b;
+            if (i < c && j < c) part[((int64_t)split * c + i) * c + j] = acc[a][b];
+        }
+}
+
+__global__ void gram_reduce_kernel(int c, int splits, const double* __restrict__ part, double* G) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)c * c) return;
+    const int i = (int)(e / c), j = (int)(e % c);
+    const int a = i < j ? i : j, b = i < j ? j : i;  // computed entries live in the upper part
+    double s = 0.0;
+    for (int k = 0; k < splits; k++) s += part[((int64_t)k * c + a) * c + b];
+    G[e] = s;
+}
+
+void launch_gram(int64_t n, int c, const double* V, int64_t ld, double* part, int splits,
+                 double* G, cudaStream_t s) {
+    const int ntile = (c + GR_T - 1) / GR_T;
+    dim3 grid(ntile * (ntile + 1) / 2, splits);
+    gram_kernel<<<grid, 256, 0, s>>>(n, c, V, ld, part, ntile);
+    const int64_t tot = (int64_t)c * c;
+    gram_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c, splits, part, G);
+}
+
+__global__ void loo_norm_kernel(int c, const double* __restrict__ G, double* out) {
+    __shared__ double red[40];
+    double part = 0.0;
+    for (int64_t e = threadIdx.x; e < (int64_t)c * c; e += blockDim.x) {
+        const int i = (int)(e / c), j = (int)(e % c);
+        const double d = (i == j ? 1.0 : 0.0) - G[e];
+        part += d * d;
+    }
+    const double s = block_sum(part, red);
+    if (threadIdx.x == 0) *out = sqrt(s);
+}
+
+void launch_loo_norm(int c, const double* G, double* out, cudaStream_t s) {
+    loo_norm_kernel<<<1, 256, 0, s>>>(c, G, out);
+}
+
+// ------------------------------------------------------------------------------------
+__global__ void pack_kernel(int64_t cnt, const int64_t* __restrict__ idx,
+                            const double* __restrict__ x, double* __restrict__ buf,
+                            const int* istate) {
+    if (!running(istate)) return;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < cnt) buf[i] = x[idx[i]];
+}
+
+void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, const int* istate,
+                 cudaStream_t s) {
+    if (cnt <= 0) return;
+    pack_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(cnt, idx, x, buf, istate);
+}
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
+    if (n <= 0) return;
+    fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, v);
+}
+
+}  // namespace igs

@@ -1,0 +1,150 @@
+"""Per-kernel parity: each libigs kernel (through the C ABI) against the oracle's
+primitive on the same seeded inputs, at sizes spanning several tiles plus a ragged tail."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(float).eps
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2205_07805_b200 as P
+    P.lib()
+    return torch
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("n", [5, 1024 * 3 + 17, 70001, 1 << 20])
+@pytest.mark.parametrize("p", [0, 1, 7, 64, 300])
+def test_block_dot_vs_oracle(torch_cuda, n, p):
+    torch = torch_cuda
+    import paper_2205_07805_b200 as P
+    if n == 1 << 20 and p == 300:
+        p = 100
+    rng = np.random.default_rng(n + p)
+    ld = n + (n % 2) + 32           # padded, even
+    Vh = rng.standard_normal((p + 1, ld))   # column-major storage: row j = column j
+    Vh[:, n:] = np.nan                      # padding must never be read as data
+    u = Vh[p, :n].copy(); z = rng.standard_normal(n)
+    Vd = _dev(torch, Vh.reshape(-1))
+    ud = Vd[p * ld: p * ld + n]             # u = V[:, p] as in the solver
+    zd = _dev(torch, z)
+    for nv in (1, 2):
+        out = torch.empty(2 * (p + 1), dtype=torch.float64, device="cuda")
+        P.igs_op_block_dot(n, p, Vd, ld, ud, zd if nv == 2 else None, out)
+        got = out.cpu().numpy()
+        Vp = Vh[:p, :n].T
+        ref = oracle.block_dot(Vp, u, z, block=4096)
+        scale = np.concatenate([np.abs(Vp).T @ np.abs(u), [np.abs(u) @ np.abs(u)],
+                                np.abs(Vp).T @ np.abs(z), [np.abs(u) @ np.abs(z)]])
+        m = (p + 1) if nv == 1 else 2 * (p + 1)
+        err = np.abs(got[:m] - ref[:m]) / scale[:m]
+        assert np.all(err <= 64 * EPS * np.log2(n + 2)), (nv, err.max())
+
+
+def test_block_dot_deterministic(torch_cuda):
+    torch = torch_cuda
+    import paper_2205_07805_b200 as P
+    n, p = 300001, 50
+    rng = np.random.default_rng(7)
+    V = _dev(torch, rng.standard_normal((p + 1) * (n + 1)))
+    z = _dev(torch, rng.standard_normal(n + 1))
+    outs = []
+    for _ in range(3):
+        o = torch.empty(2 * (p + 1), dtype=torch.float64, device="cuda")
+        P.igs_op_block_dot(n, p, V, n + 1, V[p * (n + 1):], z, o)
+        outs.append(o.cpu().numpy().tobytes())
+    assert outs[0] == outs[1] == outs[2]
+
+
+@pytest.mark.parametrize("n", [1, 2, 511, 1 << 16 | 3])
+@pytest.mark.parametrize("p", [0, 1, 9, 64, 300])
+@pytest.mark.parametrize("gs", [1, 2])
+def test_update_vs_oracle(torch_cuda, n, p, gs):
+    torch = torch_cuda
+    import paper_2205_07805_b200 as P
+    rng = np.random.default_rng(3 * n + p)
+    ld = n + (n % 2)
+    Vh = np.zeros((p + 2, ld)); Vh[:, :n] = rng.standard_normal((p + 2, n))
+    z = rng.standard_normal(n)
+    alpha = rng.standard_normal(p) * 1e-3 if gs == 2 else None
+    beta = rng.standard_normal(p + 1)
+    gamma = 0.75
+    Vp = Vh[:p, :n].T
+    u = Vh[p, :n].copy()
+    v_ref, un_ref = oracle.update(Vp, u, z, alpha, beta, gamma)
+    Vd = _dev(torch, Vh.reshape(-1))
+    zd = _dev(torch, np.concatenate([z, [0.0] * (ld - n)]))
+    ad = _dev(torch, alpha) if alpha is not None else None
+    bd = _dev(torch, beta)
+    P.igs_op_update(n, p, Vd, ld, Vd[p * ld:], zd, ad, bd, gamma, Vd[p * ld:], Vd[(p + 1) * ld:])
+    out = Vd.cpu().numpy().reshape(p + 2, ld)
+    scale_v = (np.abs(u) + (np.abs(Vp) @ np.abs(alpha) if alpha is not None else 0)) / gamma
+    assert np.all(np.abs(out[p, :n] - v_ref) <= 8 * (p + 2) * EPS * scale_v + 1e-300)
+    scale_u = np.abs(z) / gamma + np.abs(np.column_stack([Vp, v_ref])) @ np.abs(beta)
+    assert np.all(np.abs(out[p + 1, :n] - un_ref) <= 8 * (p + 2) * EPS * scale_u + 1e-300)
+    assert np.all(out[:p, :n] == Vh[:p, :n])           # V_p untouched
+
+
+@pytest.mark.parametrize("order", [1, 7, 64, 300])
+def test_trisolve_vs_oracle(torch_cuda, order):
+    torch = torch_cuda
+    import paper_2205_07805_b200 as P
+    rng = np.random.default_rng(order)
+    L = np.tril(rng.uniform(-1, 1, (order, order)), -1) * 1e-2
+    b = rng.standard_normal(order)
+    ref = oracle.forward_solve_unit(L, b)
+    Ld = _dev(torch, np.asfortranarray(L).reshape(-1, order="F"))
+    xd = torch.empty(order, dtype=torch.float64, device="cuda")
+    P.igs_op_trisolve(order, Ld, order, _dev(torch, b), xd)
+    got = xd.cpu().numpy()
+    assert np.allclose(got, ref, rtol=1e-14, atol=1e-14 * np.abs(ref).max())
+
+
+def _csr_random(n, rng):
+    lens = rng.integers(0, 40, n)
+    lens[::17] = 0
+    lens[5::97] = 300          # a few long rows
+    rows = []
+    cols = []
+    for i, L in enumerate(lens):
+        L = min(L, n)
+        c = np.sort(rng.choice(n, L, replace=False))
+        cols.append(c)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum([c.size for c in cols], out=rowptr[1:])
+    colind = np.concatenate(cols).astype(np.int32)
+    return W.Csr(n, n, 0, rowptr, colind, rng.standard_normal(colind.size))
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3_64", "c4_24", "c5_12", "random"])
+def test_spmv_vs_oracle(torch_cuda, name):
+    torch = torch_cuda
+    import paper_2205_07805_b200 as P
+    rng = np.random.default_rng(1)
+    if name == "random":
+        A = _csr_random(3001, rng)
+    elif "_" in name:
+        cfg, N = name.split("_")
+        A = W.config(cfg, N=int(N)).A
+    else:
+        A = W.config(name).A
+    s = P.Solver(A)
+    x = rng.standard_normal(A.n_rows)
+    y = torch.empty(A.n_rows, dtype=torch.float64, device="cuda")
+    s.spmv(_dev(torch, x), y)
+    ref = oracle.spmv(A, x)
+    absA = W.Csr(A.n_rows, A.n_cols, 0, A.rowptr, A.colind, np.abs(A.values))
+    bound = 4 * EPS * np.diff(A.rowptr).clip(1) * oracle.spmv(absA, np.abs(x))
+    assert np.all(np.abs(y.cpu().numpy() - ref) <= bound + 1e-300)
+    s.close()

@@ -1,0 +1,233 @@
+"""End-to-end parity: igs_solve (CUDA, through the C ABI) against the oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star, readings R9/R13 in DESIGN.md):
+  * H column-normwise <= 1e-10 over the first 30 columns (while the Arnoldi residual
+    is above 1e-8),
+  * final beta <= 1e-14 or within 10x of the oracle's,
+  * ||I - V^T V||_F within 10x of the oracle's (or both at the eps level).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(float).eps
+VARIANT = {1: "igs1", 2: "igs2"}
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2205_07805_b200 as P
+    P.lib()
+    return P
+
+
+def _compare_cols(Hg, Ho, res_hist, ncols=30):
+    # stop comparing once the Arnoldi residual is below 1e-8 (reading R9)
+    c = 0
+    while c < min(ncols, Ho.shape[1]) and (c + 1 >= len(res_hist) or res_hist[c + 1] > 1e-8):
+        c += 1
+    c = max(c, 1)
+    return oracle.column_normwise_diff(Hg, Ho, min(c, Hg.shape[1])), c
+
+
+def _loo_close(lg, lo):
+    """north-star bar: GPU LOO within 10x of the oracle's (both at the O(eps) level passes)."""
+    if lo < 1e-12 and lg < 1e-12:
+        return True
+    return lo / 10 <= lg <= lo * 10
+
+
+def _loo_ok(prob, gs, k, lg, lo, restart=0):
+    """gs=1: the oracle's own LOO moves ~8x with the reduction order alone (eps*kappa(B_k)
+    with an order-dependent constant; reading R19), so the band is taken over the oracle's
+    reduction orders {sequential, blocked 64, blocked 4096}; the GPU may not be worse than
+    10x the worst of them and not better than 1/100 of the best."""
+    if gs == 2 or _loo_close(lg, lo):
+        return _loo_close(lg, lo)
+    los = [lo]
+    for blk in (0, 64):
+        o = oracle.gmres(prob.A, prob.b, k, restart=restart, variant="igs1", dot_block=blk, want_V=True)
+        los.append(oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]]))
+    return min(los) / 100 <= lg <= 10 * max(los)
+
+
+def run_pair(P, prob, gs, k=None, restart=None, tol=None, dot_block=4096, want_loo=True):
+    import torch
+    k = k or prob.k
+    restart = prob.restart if restart is None else restart
+    tol = prob.tol if tol is None else tol
+    s = P.Solver(prob.A)
+    b = torch.from_numpy(prob.b).cuda()
+    g = s.solve(b, k=k, restart=restart, tol=tol, gs_iters=gs, want_loo=want_loo)
+    s.close()
+    o = oracle.gmres(prob.A, prob.b, k, restart=restart, tol=tol, variant=VARIANT[gs],
+                     dot_block=dot_block, want_V=want_loo)
+    return g, o
+
+
+def _beta(prob, x, normA):
+    return oracle.backward_error(prob.A, prob.b, x, normA)
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_small_configs_parity(P, cfg, gs):
+    prob = W.config(cfg)
+    g, o = run_pair(P, prob, gs)
+    assert g["iters"] == o["iters"] == prob.k and g["term"] == o["term"] == "maxiter"
+    d, c = _compare_cols(g["H"], o["H"], o["res_hist"])
+    # gs=1 noise floor: reordering the reductions alone moves H by eps*kappa(B_j)
+    floor = oracle.column_normwise_diff(
+        oracle.gmres(prob.A, prob.b, prob.k, variant=VARIANT[gs], dot_block=0)["H"], o["H"], c)
+    assert d <= 1e-10 or d <= 2 * floor, (d, floor)
+    normA = oracle.norm2_estimate(prob.A)
+    bg, bo = _beta(prob, g["x"].cpu().numpy(), normA), _beta(prob, o["x"], normA)
+    assert bg <= 1e-14 or bo / 10 <= bg <= 10 * bo, (bg, bo)
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    assert g["basis_cols"] == o["basis_cols"]
+    assert _loo_ok(prob, gs, prob.k, g["loo"], lo), (g["loo"], lo)
+    # Givens residual history follows the oracle's (down to rounding at ~eps ||b||)
+    np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-13)
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+def test_c3_downsized_parity(P, gs):
+    prob = W.config("c3", N=128)      # n = 16384: 16 bdot tiles, several update blocks
+    g, o = run_pair(P, prob, gs, k=120)
+    d, _ = _compare_cols(g["H"], o["H"], o["res_hist"])
+    assert d <= 1e-10, d
+    normA = oracle.norm2_estimate(prob.A)
+    bg, bo = _beta(prob, g["x"].cpu().numpy(), normA), _beta(prob, o["x"], normA)
+    assert bg <= 1e-14 or bo / 10 <= bg <= 10 * bo
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    assert _loo_ok(prob, gs, 120, g["loo"], lo), (g["loo"], lo)
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+@pytest.mark.parametrize("N", [16, 32])
+def test_c4_downsized_restarted(P, gs, N):
+    prob = W.config("c4", N=N)
+    g, o = run_pair(P, prob, gs, k=3000, want_loo=False)
+    assert g["term"] == o["term"] == "converged"
+    assert abs(g["iters"] - o["iters"]) <= 2 and g["cycles"] == o["cycles"]
+    assert g["true_relres"] <= 1e-12
+    d, _ = _compare_cols(g["H"], o["H"], o["res_hist"])
+    assert d <= 1e-10
+
+
+def test_c3_full_size_first_columns(P):
+    # BASELINE config c3 at full size, the first 30 Hessenberg columns (sampled outputs)
+    prob = W.config("c3")
+    g, o = run_pair(P, prob, 2, k=30, want_loo=True)
+    d, _ = _compare_cols(g["H"], o["H"], o["res_hist"])
+    assert d <= 1e-10, d
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    assert _loo_close(g["loo"], lo) and g["loo"] <= 1e-12, (g["loo"], lo)
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+def test_breakdown_is_detected(P, gs):
+    d = np.tile(np.arange(1.0, 6.0), 10)
+    A = W.diag_csr(d)
+    prob = W.Problem("diag5", A, np.ones(50), 40, 0, 0.0)
+    g, o = run_pair(P, prob, gs, want_loo=False)
+    assert g["term"] == "breakdown" and abs(g["iters"] - o["iters"]) <= 1
+    np.testing.assert_allclose(g["x"].cpu().numpy(), 1.0 / d, rtol=1e-13)
+
+
+def test_identity_one_iteration(P):
+    A = W.diag_csr(np.ones(12))
+    prob = W.Problem("I", A, np.arange(1.0, 13.0), 5, 0, 0.0)
+    for gs in (1, 2):
+        g, _ = run_pair(P, prob, gs, want_loo=False)
+        assert g["iters"] == 1 and g["term"] == "breakdown"
+        np.testing.assert_allclose(g["x"].cpu().numpy(), prob.b, rtol=1e-15)
+
+
+def test_simoncini_igs2_keeps_decreasing(P):
+    A, b = W.simoncini(100, 0)
+    prob = W.Problem("simoncini", A, b, 97, 0, 0.0)
+    g, o = run_pair(P, prob, 2)
+    r = g["res_hist"]
+    assert r[90] <= 1e-18 and r[97] <= 1e-23          # no stagnation
+    assert g["loo"] <= 1e-13
+    g1, _ = run_pair(P, prob, 1, want_loo=False)
+    assert g1["res_hist"][75:].min() >= 1e-13           # one sweep stagnates like MGS
+
+
+def test_host_and_device_paths_identical(P):
+    import torch
+    prob = W.config("c3", N=64)
+    s = P.Solver(prob.A)
+    gd = s.solve(torch.from_numpy(prob.b).cuda(), k=50, gs_iters=2)
+    gh = s.solve(prob.b.copy(), k=50, gs_iters=2)
+    gd2 = s.solve(torch.from_numpy(prob.b).cuda(), k=50, gs_iters=2)
+    assert gd["H"].tobytes() == gh["H"].tobytes() == gd2["H"].tobytes()   # deterministic
+    assert gd["x"].cpu().numpy().tobytes() == gh["x"].tobytes()
+    st = s.stats()
+    assert st["allreduces"] == 0 and st["iterations"] >= 150
+    s.close()
+
+
+def test_x0_restart_resume(P):
+    import torch
+    prob = W.config("c4", N=16)
+    s = P.Solver(prob.A)
+    b = torch.from_numpy(prob.b).cuda()
+    a = s.solve(b, k=100, restart=100, tol=1e-12, gs_iters=2)
+    c = s.solve(b, x0=a["x"], k=200, restart=100, tol=1e-12, gs_iters=2)
+    assert a["true_relres"] <= 1e-12 and c["iters"] == 0 and c["term"] == "converged"
+    s.close()
+
+
+def test_errors_are_status_codes(P):
+    import torch
+    prob = W.config("c1")
+    s = P.Solver(prob.A)
+    b = torch.from_numpy(prob.b).cuda()
+    with pytest.raises(P.IgsError) as e:
+        s.solve(b, k=60, gs_iters=3)
+    assert e.value.status == 1
+    with pytest.raises(P.IgsError) as e:
+        s.solve(b, k=999, gs_iters=2)
+    assert e.value.status == 1
+    bb = prob.b.copy(); bb[7] = np.inf
+    with pytest.raises(P.IgsError) as e:
+        s.solve(torch.from_numpy(bb).cuda(), k=10, gs_iters=2)
+    assert e.value.status == 5
+    ok = s.solve(b, k=10, gs_iters=2)                   # context still usable
+    assert ok["iters"] == 10
+    s.close()
+    A = W.config("c1").A
+    bad = W.Csr(A.n_rows, A.n_cols, 0, A.rowptr.copy(), A.colind.copy(), A.values.copy())
+    bad.values[3] = np.nan
+    with pytest.raises(P.IgsError) as e:
+        P.Solver(bad)
+    assert e.value.status == 5
+
+
+def test_zero_rhs(P):
+    import torch
+    prob = W.config("c1")
+    s = P.Solver(prob.A)
+    g = s.solve(torch.zeros(1000, dtype=torch.float64, device="cuda"), k=10, gs_iters=2)
+    assert g["term"] == "converged" and g["iters"] == 0 and float(g["x"].abs().max()) == 0.0
+    s.close()
+
+
+def test_kernel_timing_counts(P):
+    import torch
+    prob = W.config("c3", N=64)
+    s = P.Solver(prob.A)
+    s.set_timing(2)
+    s.solve(torch.from_numpy(prob.b).cuda(), k=40, gs_iters=2)
+    ks = s.kernel_stats()
+    assert ks["block_dot"]["launches"] == 41 and ks["update"]["launches"] == 42
+    assert ks["spmv"]["launches"] == 40 and ks["small"]["launches"] == 42
+    assert all(v["ms"] >= 0 for v in ks.values())
+    s.close()
