@@ -1,0 +1,73 @@
+"""CPU-only checks of the C ABI: libigs.so loads, exports every function include/igs.h
+declares, host-only planners work, and compute entry points fail loudly (no CPU
+fallback) when no CUDA device is present."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_2205_07805_b200 import build
+    build.build()
+    import paper_2205_07805_b200 as P
+    P.lib()
+    return P
+
+
+def test_exports_every_declared_symbol(P):
+    hdr = open(os.path.join(ROOT, "include", "igs.h")).read()
+    declared = set(re.findall(r"\b(igs_[a-z_0-9]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    L = P.lib()
+    missing = [s for s in declared if not hasattr(L, s)]
+    assert not missing, missing
+    assert declared == set(P.EXPORTS)
+
+
+def test_no_cpu_fallback(P):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    A = W.config("c1").A
+    with pytest.raises(P.IgsError) as e:
+        P.igs_create(A.n_cols, 0, A.n_rows, A.rowptr, A.colind, A.values, stream=0)
+    assert e.value.status == 2          # IGS_ERR_CUDA, never a silent CPU path
+    with pytest.raises(P.IgsError):
+        P.igs_op_trisolve(3, None, 3, None, None, stream=0)
+
+
+def test_plan_ghosts_and_remap_3d(P):
+    N, G = 10, 3
+    n = N ** 3
+    bounds = np.array([0, 300, 700, n])
+    for r in range(G):
+        A = W.stencil_csr(N, 3, W.C4_BETA, bounds[r], bounds[r + 1])
+        ghosts, cnt = P.igs_plan_ghosts(bounds[r], A.n_rows, A.rowptr, A.colind, G, bounds)
+        cols = A.colind.astype(np.int64)
+        ext = np.unique(cols[(cols < bounds[r]) | (cols >= bounds[r + 1])])
+        np.testing.assert_array_equal(ghosts, ext)
+        assert cnt[r] == 0 and cnt.sum() == ghosts.size
+        for q in range(G):
+            assert cnt[q] == np.sum((ghosts >= bounds[q]) & (ghosts < bounds[q + 1]))
+        loc = P.igs_plan_remap(bounds[r], A.n_rows, A.rowptr, A.colind, ghosts)
+        back = np.where(loc < A.n_rows, loc + bounds[r], ghosts[np.clip(loc - A.n_rows, 0, None)] if ghosts.size else 0)
+        np.testing.assert_array_equal(back, cols)
+
+
+def test_plan_rejects_bad_input(P):
+    A = W.config("c1").A
+    bad = A.colind.copy(); bad[5] = 5000                  # beyond every rank's rows
+    with pytest.raises(P.IgsError) as e:
+        P.igs_plan_ghosts(0, 500, A.rowptr[:501], bad, 2, np.array([0, 500, 1000]))
+    assert e.value.status == 1
+    ghosts, _ = P.igs_plan_ghosts(0, 500, A.rowptr[:501], A.colind, 2, np.array([0, 500, 1000]))
+    assert list(ghosts) == [500]
+    with pytest.raises(P.IgsError):                       # column missing from the ghost list
+        P.igs_plan_remap(0, 500, A.rowptr[:501], A.colind, np.zeros(0, dtype=np.int64))
