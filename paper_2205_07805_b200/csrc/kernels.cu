@@ -311,11 +311,175 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
     if (threadIdx.x == 0) *counter = 0u;
 }
 
+// ------------------------------------------------------------------------------------
+// K2 (sm_100a pipeline): the same block dot with the Blackwell bulk-copy engine.
+//   Persistent CTA per SM = 8 consumer warps + 1 producer warp.  Tile = 512 rows.  For each
+//   tile the producer streams V_p in groups of 8 columns (8 x 4 KB cp.async.bulk copies per
+//   stage, completion counted on an mbarrier with expect_tx) into a 6-stage shared-memory
+//   ring (192 KB in flight per SM).  Consumer warp w owns column 8g+w of group g: lane l
+//   multiplies rows l+32k (k<16) against u, z held in registers for the whole tile, one warp
+//   reduction per column, and adds into a per-CTA shared accumulator that only it touches
+//   for that column -> fixed order, deterministic.  Column p ("u itself") comes from the
+//   registers.  Stage 2 (per-CTA partials, last CTA sums in CTA order) as in bdot_kernel.
+// ------------------------------------------------------------------------------------
+constexpr int BT_CONS_WARPS = 8;
+constexpr int BT_THREADS = (BT_CONS_WARPS + 1) * 32;
+constexpr int BT_ROWS = 512;
+constexpr int BT_RPL = BT_ROWS / 32;  // rows per lane
+constexpr int BT_STAGES = 6;
+constexpr int BT_STAGE_DOUBLES = BT_CONS_WARPS * BT_ROWS;  // 8 columns x 512 rows = 32 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int NV>
+__global__ void __launch_bounds__(BT_THREADS, 1)
+    bdot_tma_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
+                    const double* __restrict__ u, const double* __restrict__ z,
+                    double* __restrict__ part, double* __restrict__ out, unsigned* counter,
+                    const int* istate) {
+    if (!running(istate)) return;
+    extern __shared__ __align__(128) double smem_bt[];
+    double* ring = smem_bt;                                        // [STAGES][8][512]
+    double* acc = ring + BT_STAGES * BT_STAGE_DOUBLES;             // [NV*(p+1)]
+    const int ncols = p + 1;
+    const int stride = NV * ncols;
+    uint64_t* full = reinterpret_cast<uint64_t*>(acc + ((stride + 1) & ~1));
+    uint64_t* empty = full + BT_STAGES;
+    __shared__ bool s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < BT_STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, BT_CONS_WARPS); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
+    const int ngroups = (ncols + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
+    if (warp == BT_CONS_WARPS) {
+        // ---------------- producer: one elected lane issues the bulk copies ----------------
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int64_t row0 = tile * BT_ROWS;
+                const int64_t rows = (n - row0 < BT_ROWS) ? n - row0 : BT_ROWS;
+                const uint32_t bytes = (uint32_t)(((rows + 1) & ~1LL) * sizeof(double));
+                for (int g = 0; g < ngroups; g++, it++) {
+                    const int s = it % BT_STAGES;
+                    mbar_wait(empty + s, ((it / BT_STAGES) & 1) ^ 1);
+                    const int c0 = g * BT_CONS_WARPS;
+                    const int c1 = min(c0 + BT_CONS_WARPS, p);  // V columns only (col p = u)
+                    const int nc = c1 > c0 ? c1 - c0 : 0;
+                    mbar_arrive_expect_tx(full + s, (uint32_t)nc * bytes);
+                    for (int c = 0; c < nc; c++)
+                        bulk_g2s(ring + (size_t)s * BT_STAGE_DOUBLES + c * BT_ROWS,
+                                 V + (int64_t)(c0 + c) * ld + row0, bytes, full + s);
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        uint32_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t row0 = tile * BT_ROWS;
+            const bool full_tile = row0 + BT_ROWS <= n;
+            double ur[BT_RPL], zr[BT_RPL];
+#pragma unroll
+            for (int k = 0; k < BT_RPL; k++) {
+                const int64_t r = row0 + lane + 32 * k;
+                const bool ok = full_tile || r < n;
+                ur[k] = ok ? __ldg(u + r) : 0.0;
+                zr[k] = (NV == 2 && ok) ? __ldg(z + r) : 0.0;
+            }
+            for (int g = 0; g < ngroups; g++, it++) {
+                const int s = it % BT_STAGES;
+                const int c = g * BT_CONS_WARPS + warp;
+                mbar_wait(full + s, (it / BT_STAGES) & 1);
+                if (c < ncols) {
+                    double su = 0.0, sz = 0.0;
+                    if (c < p) {
+                        const double* col = ring + (size_t)s * BT_STAGE_DOUBLES + warp * BT_ROWS;
+#pragma unroll
+                        for (int k = 0; k < BT_RPL; k++) {
+                            double v = col[lane + 32 * k];
+                            if (!full_tile && row0 + lane + 32 * k >= n) v = 0.0;
+                            su = fma(v, ur[k], su);
+                            if (NV == 2) sz = fma(v, zr[k], sz);
+                        }
+                    } else {  // column p is u itself
+#pragma unroll
+                        for (int k = 0; k < BT_RPL; k++) {
+                            su = fma(ur[k], ur[k], su);
+                            if (NV == 2) sz = fma(ur[k], zr[k], sz);
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        su += __shfl_xor_sync(FULL_MASK, su, off);
+                        if (NV == 2) sz += __shfl_xor_sync(FULL_MASK, sz, off);
+                    }
+                    if (lane == 0) {
+                        acc[c] += su;
+                        if (NV == 2) acc[ncols + c] += sz;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) part[(int64_t)blockIdx.x * stride + i] = acc[i];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) {
+        double sacc = 0.0;
+        for (int bb = 0; bb < (int)gridDim.x; bb++) sacc += __ldcg(part + (int64_t)bb * stride + i);
+        out[i] = sacc;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
+static size_t bdot_tma_smem(int p, int nv) {
+    const size_t stride = (size_t)nv * (p + 1);
+    return (size_t)BT_STAGES * BT_STAGE_DOUBLES * sizeof(double) + ((stride + 1) & ~(size_t)1) * sizeof(double) +
+           2 * BT_STAGES * sizeof(uint64_t);
+}
+
 static size_t bdot_smem(int p, int nv) { return (size_t)BD_WARPS * nv * (p + 1) * sizeof(double); }
 
 int bdot_grid_size(int64_t n, int num_sms) {
     const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
-    int64_t g = (int64_t)num_sms * 2;
+    int64_t g = (int64_t)num_sms * 2;  // also >= the TMA kernel's grid (num_sms)
     if (g > ntiles) g = ntiles;
     if (g < 1) g = 1;
     return (int)g;
@@ -325,6 +489,26 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
                       const double* z, double* out, double* part, unsigned* counter, int grid,
                       const int* istate, cudaStream_t s) {
     const int nv = z ? 2 : 1;
+    // sm_100a bulk-copy pipeline when V columns are 16-B aligned with an even ld and the
+    // accumulators fit next to the 192 KB ring; the register kernel otherwise
+    const size_t tsmem = bdot_tma_smem(p, nv);
+    if (p > 0 && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 && tsmem <= 227 * 1024 && n >= BT_ROWS) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
+        const int tg = (int)(ntiles < sms ? ntiles : sms);
+        if (tg <= grid) {
+            if (nv == 2) {
+                cudaFuncSetAttribute(bdot_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+                bdot_tma_kernel<2><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+            } else {
+                cudaFuncSetAttribute(bdot_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
+                bdot_tma_kernel<1><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+            }
+            return;
+        }
+    }
     const size_t smem = bdot_smem(p, nv);
     if (nv == 2) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(bdot_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
