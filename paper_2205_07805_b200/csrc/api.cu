@@ -414,12 +414,12 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
     ctx->A.nloc = n_local;
     ctx->A.ghost = ctx->n_ghost > 0 ? ctx->d_ghost : nullptr;
     {
-        // short rows (<= 12 nnz on average): CSR-stream kernel (lpr = 0); otherwise vector
+        // short rows (<= 8 nnz on average): CSR-stream kernel (lpr = 0); otherwise vector
         // CSR with lanes per row = next power of two of the mean row length, in [1, 32]
         const double avg = n_local > 0 ? (double)nnz_local / (double)n_local : 1.0;
         int lpr = 1;
         while (lpr < 32 && lpr < avg) lpr *= 2;
-        ctx->A.lpr = avg <= 12.0 ? 0 : lpr;
+        ctx->A.lpr = avg <= 8.0 ? 0 : lpr;
     }
     ctx->bdot_grid = bdot_grid_size(n_local, ctx->num_sms);
     cudaError_t e;

@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t nrows, const PT* __re
 // sequence as a sequential CSR row loop (product, then add), with none of the per-row
 // lane waste of vector CSR at ~7 nnz/row.
 constexpr int SPS_ROWS = 256;
-constexpr int SPS_CAP = SPS_ROWS * 14;  // products staged in smem (28 KB)
+constexpr int SPS_K = 8;                     // staged nonzeros per thread (fast path)
+constexpr int SPS_CAP = SPS_ROWS * SPS_K;    // 2048 products = 16 KB of shared memory
 
 template <typename IT, typename PT, bool GHOST, bool RESID>
 __global__ void __launch_bounds__(SPS_ROWS)
@@ -90,31 +91,44 @@ __global__ void __launch_bounds__(SPS_ROWS)
     const int64_t r = r0 + threadIdx.x;
     const int64_t rl = (r0 + SPS_ROWS < nrows) ? r0 + SPS_ROWS : nrows;
     const int64_t q0 = (int64_t)__ldg(rowptr + r0), q1 = (int64_t)__ldg(rowptr + rl);
-    const int64_t cnt = q1 - q0;
+    const int cnt = (int)(q1 - q0 < (int64_t)SPS_CAP + 1 ? q1 - q0 : (int64_t)SPS_CAP + 1);
+    int a = 0, e = 0;
+    if (r < nrows) { a = (int)((int64_t)__ldg(rowptr + r) - q0); e = (int)((int64_t)__ldg(rowptr + r + 1) - q0); }
     if (cnt <= SPS_CAP) {
-#pragma unroll 4
-        for (int64_t i = threadIdx.x; i < cnt; i += SPS_ROWS) {
-            const int64_t c = (int64_t)__ldg(col + q0 + i);
-            double xv;
-            if (GHOST && c >= nloc) xv = __ldg(ghost + (c - nloc));
-            else xv = __ldg(x + c);
-            prod[i] = __dmul_rn(__ldg(val + q0 + i), xv);
+        // all column and value loads first, then all gathers: 3 x 8 independent loads per thread
+        int64_t cc[SPS_K];
+        double vv[SPS_K], xv[SPS_K];
+#pragma unroll
+        for (int k = 0; k < SPS_K; k++) {
+            const int i = threadIdx.x + k * SPS_ROWS;
+            cc[k] = i < cnt ? (int64_t)__ldg(col + q0 + i) : 0;
+            vv[k] = i < cnt ? __ldg(val + q0 + i) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < SPS_K; k++) {
+            const int i = threadIdx.x + k * SPS_ROWS;
+            if (GHOST && cc[k] >= nloc) xv[k] = i < cnt ? __ldg(ghost + (cc[k] - nloc)) : 0.0;
+            else xv[k] = i < cnt ? __ldg(x + cc[k]) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < SPS_K; k++) {
+            const int i = threadIdx.x + k * SPS_ROWS;
+            if (i < cnt) prod[i] = __dmul_rn(vv[k], xv[k]);
         }
         __syncthreads();
         if (r < nrows) {
-            const int a = (int)((int64_t)__ldg(rowptr + r) - q0), e = (int)((int64_t)__ldg(rowptr + r + 1) - q0);
-            double s = 0.0;
-            for (int q = a; q < e; q++) s = __dadd_rn(s, prod[q]);
-            y[r] = RESID ? b[r] - s : s;
+            double sum = 0.0;
+            for (int q = a; q < e; q++) sum = __dadd_rn(sum, prod[q]);
+            y[r] = RESID ? b[r] - sum : sum;
         }
-    } else if (r < nrows) {  // unusually long rows in this block: plain row loop
-        double s = 0.0;
-        for (int64_t q = __ldg(rowptr + r); q < (int64_t)__ldg(rowptr + r + 1); q++) {
+    } else if (r < nrows) {  // more than SPS_K nonzeros per row on average here: row loop
+        double sum = 0.0;
+        for (int64_t q = q0 + a; q < q0 + e; q++) {
             const int64_t c = (int64_t)__ldg(col + q);
-            const double xv = (GHOST && c >= nloc) ? __ldg(ghost + (c - nloc)) : __ldg(x + c);
-            s = __dadd_rn(s, __dmul_rn(__ldg(val + q), xv));
+            const double xq = (GHOST && c >= nloc) ? __ldg(ghost + (c - nloc)) : __ldg(x + c);
+            sum = __dadd_rn(sum, __dmul_rn(__ldg(val + q), xq));
         }
-        y[r] = RESID ? b[r] - s : s;
+        y[r] = RESID ? b[r] - sum : sum;
     }
 }
 
