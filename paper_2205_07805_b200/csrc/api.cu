@@ -64,6 +64,8 @@ struct TimedLaunch {
 struct igs_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // small-step tail (H, Givens, status), overlapped with the update
+    cudaEvent_t ev_crit = nullptr, ev_tail = nullptr;
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
     int num_sms = 148;
@@ -112,6 +114,7 @@ struct igs_ctx {
     double t_ms[IGS_K_COUNT] = {0};
     double t_bytes[IGS_K_COUNT] = {0};
     int64_t t_launch[IGS_K_COUNT] = {0};
+    int64_t tail_launches = 0;  // side-stream small-step tails (untimed)
 };
 
 // ------------------------------------------------------------------------------ misc
@@ -119,7 +122,7 @@ extern "C" const char* igs_last_error(void) { return g_err.c_str(); }
 
 static inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
-static igs_status timer_begin(igs_ctx* c, int* idx) {
+static igs_status timer_begin(igs_ctx* c, int* idx, cudaStream_t st) {
     *idx = -1;
     if (!c->timing) return IGS_OK;
     const size_t need = 2 * (c->recs.size() + 1);
@@ -129,19 +132,21 @@ static igs_status timer_begin(igs_ctx* c, int* idx) {
         c->events.push_back(e);
     }
     *idx = (int)(2 * c->recs.size());
-    CUDA_TRY(cudaEventRecord(c->events[*idx], c->stream));
+    CUDA_TRY(cudaEventRecord(c->events[*idx], st));
+    c->recs.push_back({-1, 0.0, *idx, *idx + 1});  // reserve the pair
     return IGS_OK;
 }
 
-static igs_status timer_end(igs_ctx* c, int idx, int kind, double bytes) {
+static igs_status timer_end(igs_ctx* c, int idx, int kind, double bytes, cudaStream_t st) {
     if (idx < 0) return IGS_OK;
-    CUDA_TRY(cudaEventRecord(c->events[idx + 1], c->stream));
-    c->recs.push_back({kind, bytes, idx, idx + 1});
+    CUDA_TRY(cudaEventRecord(c->events[idx + 1], st));
+    c->recs[idx / 2] = {kind, bytes, idx, idx + 1};
     return IGS_OK;
 }
 
 static igs_status timer_flush(igs_ctx* c) {
     for (const auto& r : c->recs) {
+        if (r.kind < 0) continue;
         float ms = 0.f;
         CUDA_TRY(cudaEventElapsedTime(&ms, c->events[r.ev0], c->events[r.ev1]));
         c->t_ms[r.kind] += ms;
@@ -152,14 +157,15 @@ static igs_status timer_flush(igs_ctx* c) {
     return IGS_OK;
 }
 
-#define TIMED(kind, bytes, launch_stmt)           \
-    do {                                          \
-        int ti_;                                  \
-        TRY(timer_begin(ctx, &ti_));              \
-        launch_stmt;                              \
-        CUDA_TRY(cudaGetLastError());             \
-        TRY(timer_end(ctx, ti_, (kind), (bytes)));\
+#define TIMED_ON(strm, kind, bytes, launch_stmt)         \
+    do {                                                  \
+        int ti_;                                          \
+        TRY(timer_begin(ctx, &ti_, (strm)));              \
+        launch_stmt;                                      \
+        CUDA_TRY(cudaGetLastError());                     \
+        TRY(timer_end(ctx, ti_, (kind), (bytes), (strm)));\
     } while (0)
+#define TIMED(kind, bytes, launch_stmt) TIMED_ON(ctx->stream, kind, bytes, launch_stmt)
 
 // --------------------------------------------------------------------- create / destroy
 extern "C" igs_status igs_nccl_unique_id(void* out128) {
@@ -298,6 +304,9 @@ static void free_ctx(igs_ctx* c) {
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
     for (auto e : c->events) cudaEventDestroy(e);
+    if (c->ev_crit) cudaEventDestroy(c->ev_crit);
+    if (c->ev_tail) cudaEventDestroy(c->ev_tail);
+    if (c->side) cudaStreamDestroy(c->side);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -423,6 +432,12 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
     }
     ctx->bdot_grid = bdot_grid_size(n_local, ctx->num_sms);
     cudaError_t e;
+    if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_crit, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->ev_tail, cudaEventDisableTiming)) != cudaSuccess) {
+        set_error(std::string("igs_create: stream/event: ") + cudaGetErrorString(e));
+        return fail(IGS_ERR_CUDA);
+    }
     if ((e = cudaMallocHost(&ctx->h_pinned, sizeof(double) * 64)) != cudaSuccess ||
         (e = cudaMallocHost(&ctx->h_pinned_int, sizeof(int) * 64)) != cudaSuccess) {
         set_error(std::string("igs_create: cudaMallocHost: ") + cudaGetErrorString(e));
@@ -449,7 +464,7 @@ static size_t small_doubles(int m, int k) {
            + 2 * (m + 2)    // cs, sn
            + (m + 2)        // g
            + (m + 1) * dld  // dots
-           + 3 * (m + 2)    // alpha, beta, y
+           + 4 * (m + 2)    // alpha, beta, y, gam
            + SC_COUNT + (k + 2);
 }
 
@@ -515,6 +530,7 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.alpha = take(mm + 2);
         d.beta = take(mm + 2);
         d.y = take(mm + 2);
+        d.gam = take(mm + 2);
         d.scal = take(SC_COUNT);
         d.res_hist = take(kk + 2);
         d.istate = ctx->d_int;
@@ -630,9 +646,18 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
     for (int p = 1; p <= m; p++) {
         const bool drain = (p == m);
         double* u = Vcol(ctx, p);
+        if (p > 1) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));  // tail(p-1): status, H
         if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
         TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
-        TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_ITER, gs, p, m, t0, st));
+        TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_CRIT, gs, p, m, t0, st));
+        // tail of the small step on the side stream, overlapped with the fused update
+        CUDA_TRY(cudaEventRecord(ctx->ev_crit, st));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_crit, 0));
+        // (untimed: its events would span the concurrent update; counted as a launch)
+        launch_small(d, SS_TAIL, gs, p, m, t0, ctx->side);
+        CUDA_TRY(cudaGetLastError());
+        if (ctx->timing) ctx->tail_launches++;
+        CUDA_TRY(cudaEventRecord(ctx->ev_tail, ctx->side));
         const double ub = 8.0 * n * ((gs == 2 || !drain) ? p : 0) + 16.0 * n + (drain ? 0.0 : 16.0 * n);
         TIMED(IGS_K_UPDATE, ub,
               launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
@@ -655,6 +680,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
             ev_slot ^= 1;
         }
     }
+    CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
     CUDA_TRY(cudaStreamSynchronize(st));
     if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
     return IGS_OK;
@@ -822,6 +848,7 @@ extern "C" igs_status igs_set_timing(igs_ctx* ctx, int on) {
     ctx->timing = on != 0;
     if (on == 2) {
         for (int i = 0; i < IGS_K_COUNT; i++) { ctx->t_ms[i] = 0; ctx->t_bytes[i] = 0; ctx->t_launch[i] = 0; }
+        ctx->tail_launches = 0;
     }
     return IGS_OK;
 }
@@ -830,7 +857,7 @@ extern "C" igs_status igs_kernel_stats(const igs_ctx* ctx, int kind, double* ms,
                                        double* bytes) {
     ARG_CHECK(ctx != nullptr && kind >= 0 && kind < IGS_K_COUNT, "igs_kernel_stats: bad argument");
     if (ms) *ms = ctx->t_ms[kind];
-    if (launches) *launches = ctx->t_launch[kind];
+    if (launches) *launches = ctx->t_launch[kind] + (kind == IGS_K_SMALL ? ctx->tail_launches : 0);
     if (bytes) *bytes = ctx->t_bytes[kind];
     return IGS_OK;
 }

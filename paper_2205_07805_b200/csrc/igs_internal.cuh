@@ -15,6 +15,7 @@ enum : int {
     ST_BASIS = 2,      // normalised basis columns
     ST_MODE = 3,       // update-kernel mode bits: 1 = write v_p, 2 = write u'
     ST_MODE_IT = 4,    // iteration index the mode bits belong to
+    ST_CRITBD = 5,     // iteration at which the critical step saw a breakdown (else -1)
     ST_COUNT = 8
 };
 // scal slots (device doubles)
@@ -39,6 +40,7 @@ struct Dev {
     double* alpha;  // [m+1] update coefficients (r^(2)) for v_p
     double* beta;   // [m+1] update coefficients (r^(1)) for u'
     double* y;      // [m+1] least-squares solution
+    double* gam;    // [m+2] gamma of iteration p (written by crit, read by tail)
     double* scal;   // [SC_COUNT]
     int* istate;    // [ST_COUNT]
     double* res_hist;  // [kmax+1]
@@ -78,7 +80,7 @@ void launch_xupdate(int64_t n, const double* V, int64_t ld, const double* y, dou
                     const int* istate, int pmax, cudaStream_t s);
 
 // Small steps (one CTA, replicated on every rank).
-enum SmallStage : int { SS_PRIME_NORM = 0, SS_PRIME_H = 1, SS_ITER = 2, SS_LSQ = 3 };
+enum SmallStage : int { SS_PRIME_NORM = 0, SS_PRIME_H = 1, SS_CRIT = 2, SS_TAIL = 3, SS_LSQ = 4 };
 void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s);
 
 // x = (I + L)^{-1} b (test entry point; same device routine as the small step).

@@ -660,9 +660,16 @@ void launch_xupdate(int64_t n, const double* V, int64_t ld, const double* y, dou
 
 // ------------------------------------------------------------------------------------
 // K4: the small step (one CTA, replicated on every rank from the bit-identical reduced
-// dot vector).  Deterministic block reductions; forward substitution column by column.
+// dot vector).  Split in two kernels:
+//   crit  (main stream)  -- exactly what the fused update needs: gamma, the update
+//                           coefficients alpha = r2 and beta = r1, L[p,:p], mode bits;
+//   tail  (side stream)  -- what only the Hessenberg/least-squares state needs: r3, the H
+//                           column, Givens, residual, convergence/breakdown status, hp.
+// For Alg. 3 the (I+L)^{-1} solve (Step 5) only feeds H (Step 14), so it runs in the tail,
+// overlapped with the update kernel; for Alg. 2 (one sweep) r1 = (I+L)^{-1} c is on the
+// critical path.  Deterministic block reductions; blocked forward substitution.
 // ------------------------------------------------------------------------------------
-constexpr int SS_THREADS = 256;
+constexpr int SS_THREADS = 512;
 
 __device__ double block_sum(double v, double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -681,15 +688,42 @@ __device__ double block_sum(double v, double* red) {
     return red[32];
 }
 
-// x <- (I + L)^{-1} x in shared memory (forward substitution, natural order)
+// x <- (I + L)^{-1} x in shared memory: forward substitution blocked by 32.
+// Row i still subtracts L[i,j] x_j for j = 0, 1, 2, ... in natural order; warp 0 solves each
+// 32x32 diagonal block with shuffles, then every thread updates its trailing rows with 32
+// independent loads in flight.
 __device__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, double* x) {
-    for (int j = 0; j < order; j++) {
-        __syncthreads();
-        const double xj = x[j];
-        for (int i = j + 1 + threadIdx.x; i < order; i += blockDim.x)
-            x[i] = x[i] - L[i + (int64_t)j * ldl] * xj;
-    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __syncthreads();
+    for (int kb = 0; kb < order; kb += 32) {
+        const int nb = min(32, order - kb);
+        if (warp == 0) {
+            const bool mine = lane < nb;
+            double xi = mine ? x[kb + lane] : 0.0;
+            double lrow[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++)
+                lrow[j] = (mine && j < lane) ? L[(kb + lane) + (int64_t)(kb + j) * ldl] : 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; j++) {
+                const double xj = __shfl_sync(FULL_MASK, xi, j);
+                if (j < lane) xi = xi - lrow[j] * xj;
+            }
+            if (mine) x[kb + lane] = xi;
+        }
+        __syncthreads();
+        for (int i = kb + nb + threadIdx.x; i < order; i += blockDim.x) {
+            double lv[32];
+#pragma unroll
+            for (int j = 0; j < 32; j++) lv[j] = j < nb ? L[i + (int64_t)(kb + j) * ldl] : 0.0;
+            double sacc = x[i];
+#pragma unroll
+            for (int j = 0; j < 32; j++)
+                if (j < nb) sacc = sacc - lv[j] * x[kb + j];
+            x[i] = sacc;
+        }
+        __syncthreads();
+    }
 }
 
 // Givens rotation of H column j into R, update g; thread 0 does the
@@ -755,6 +789,7 @@ __global__ void __launch_bounds__(SS_THREADS)
             ist[ST_BASIS] = 0;
             ist[ST_MODE] = 1;
             ist[ST_MODE_IT] = 0;
+            ist[ST_CRITBD] = -1;
         }
         return;
     }
@@ -788,29 +823,89 @@ __global__ void __launch_bounds__(SS_THREADS)
         return;
     }
 
-    // ---------------- SS_ITER: iteration p >= 1 --------------------------------------
     if (*(volatile int*)(ist + ST_STATUS) != RUNNING) return;
     const double* dv = d.dots + (int64_t)p * d.dld;
     const bool drain = (p == m);
-    const double tol = d.scal[SC_TOL], nb = d.scal[SC_NB];
-    for (int i = tid; i < p; i += blockDim.x) s_a[i] = dv[i];
-    if (!drain) for (int i = tid; i <= p; i += blockDim.x) s_c[i] = dv[p + 1 + i];
     const double s = dv[p];
-    __syncthreads();
 
-    double gamma, hn2;
-    bool bd;
+    if (stage == SS_CRIT) {
+        // ---------------- critical path of iteration p (feeds the fused update) ----------
+        for (int i = tid; i < p; i += blockDim.x) s_a[i] = dv[i];
+        if (!drain) for (int i = tid; i <= p; i += blockDim.x) s_c[i] = dv[p + 1 + i];
+        double gamma;
+        bool bd;
+        if (gs == 2) {
+            // Step 6: lagged norm gamma = sqrt(||u||^2 - ||r2||^2)
+            double part = 0.0;
+            for (int i = tid; i < p; i += blockDim.x) part += s_a[i] * s_a[i];
+            const double t = s - block_sum(part, red);
+            gamma = t > 0.0 ? sqrt(t) : 0.0;
+            bd = !(t > kBreakdownC * kEps * s);  // S:274 / reading R12 cancellation guard
+            for (int i = tid; i < p; i += blockDim.x) d.alpha[i] = s_a[i];  // Step 10 uses r2
+        } else {
+            // Alg. 2 Step 6: gamma = ||w_{k-1}|| (fused into the single reduction)
+            gamma = sqrt(s);
+            double h2 = 0.0;
+            for (int i = tid; i < p; i += blockDim.x) {
+                const double h = d.H[i + (int64_t)(p - 1) * d.ldh];
+                h2 += h * h;
+            }
+            const double hn2 = block_sum(h2, red);
+            bd = !(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma));  // reading R12
+        }
+        if (!isfinite(gamma)) bd = true;
+        if (tid == 0) {
+            d.gam[p] = gamma;
+            d.scal[SC_GAMMA] = gamma;
+            ist[ST_CRITBD] = bd ? p : -1;
+            ist[ST_MODE] = bd ? 0 : (drain ? 1 : 3);
+            ist[ST_MODE_IT] = p;
+            if (gs == 1) d.H[p + (int64_t)(p - 1) * d.ldh] = gamma;  // gamma_{k-1} = H_{k-1,k-2}
+        }
+        if (bd || drain) return;
+        __syncthreads();
+        if (gs == 2) {
+            // Steps 7-9: c /= gamma ; d /= gamma^2 ; L[p, :p] = r2 / gamma  (reading R4)
+            const double dd = s_c[p] / (gamma * gamma);
+            double part = 0.0;
+            for (int i = tid; i < p; i += blockDim.x) {
+                const double ci = s_c[i] / gamma;
+                const double li = s_a[i] / gamma;
+                d.L[p + (int64_t)i * M] = li;
+                d.beta[i] = ci;
+                part += li * ci;
+            }
+            // Step 12 (Stephen's trick): r1 = [c ; d - L[p,:p] . c]
+            const double acc = block_sum(part, red);
+            if (tid == 0) d.beta[p] = dd - acc;
+        } else {
+            // Alg. 2 Steps 8-10: c /= gamma ; c[p] /= gamma ; L[p, :p] = a / gamma
+            for (int i = tid; i <= p; i += blockDim.x) {
+                double ci = s_c[i] / gamma;
+                if (i == p) ci = ci / gamma;  // reading R5
+                s_x[i] = ci;
+            }
+            for (int i = tid; i < p; i += blockDim.x) d.L[p + (int64_t)i * M] = s_a[i] / gamma;
+            __threadfence_block();
+            // Step 12: r1 = (I + L_{p+1})^{-1} c ; Step 17 (r3 = 0): H[:p+1, p] = r1
+            trisolve_smem(p + 1, d.L, M, s_x);
+            for (int i = tid; i <= p; i += blockDim.x) {
+                d.beta[i] = s_x[i];
+                d.H[i + (int64_t)p * d.ldh] = s_x[i];
+            }
+        }
+        return;
+    }
+
+    // ---------------- SS_TAIL: Hessenberg column p-1, Givens, status, hp ------------------
+    const double tol = d.scal[SC_TOL], nb = d.scal[SC_NB];
+    const double gamma = d.gam[p];
+    bool bd = ist[ST_CRITBD] == p;
+    double hn2 = 0.0;
     if (gs == 2) {
-        // Step 5: r3 = (I + L_p)^{-1} r2    (r3 only feeds H, Step 14)
-        for (int i = tid; i < p; i += blockDim.x) s_x[i] = s_a[i];
+        // Step 5: r3 = (I + L_p)^{-1} r2 ; Step 14: H[:p, p-1] = hp + r3, H[p, p-1] = gamma (R3)
+        for (int i = tid; i < p; i += blockDim.x) s_x[i] = dv[i];
         trisolve_smem(p, d.L, M, s_x);
-        // Step 6: lagged norm gamma = sqrt(||u||^2 - ||r2||^2)
-        double part = 0.0;
-        for (int i = tid; i < p; i += blockDim.x) part += s_a[i] * s_a[i];
-        const double nr2 = block_sum(part, red);
-        const double t = s - nr2;
-        gamma = t > 0.0 ? sqrt(t) : 0.0;
-        // Step 14: H[:p, p-1] = hp[:p, p-1] + r3 ; H[p, p-1] = gamma  (reading R3)
         double h2 = 0.0;
         for (int i = tid; i < p; i += blockDim.x) {
             const double h = d.HP[i + (int64_t)(p - 1) * d.ldh] + s_x[i];
@@ -818,81 +913,40 @@ __global__ void __launch_bounds__(SS_THREADS)
             h2 += h * h;
         }
         hn2 = block_sum(h2, red);
-        bd = !(t > kBreakdownC * kEps * s) || !(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma));
-    } else {
-        // Alg. 2 Step 6: gamma = ||w_{k-1}||  (fused into the single reduction)
-        gamma = sqrt(s);
-        double h2 = 0.0;
-        for (int i = tid; i < p; i += blockDim.x) {
-            const double h = d.H[i + (int64_t)(p - 1) * d.ldh];
-            h2 += h * h;
-        }
-        hn2 = block_sum(h2, red);
-        bd = !(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma));
+        if (!(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma))) bd = true;  // reading R12
+        if (tid == 0) d.H[p + (int64_t)(p - 1) * d.ldh] = gamma;
+        __syncthreads();
     }
-    if (tid == 0) d.H[p + (int64_t)(p - 1) * d.ldh] = gamma;  // gamma_{k-1} = H_{k-1,k-2}
-    __syncthreads();
     const double res = givens_column(d, p - 1, s_col, s_cs, s_sn, red);
-    const bool nonfinite = !isfinite(s) || !isfinite(res) || !isfinite(hn2);
+    const bool nonfinite = !isfinite(s) || !isfinite(res) || !isfinite(hn2) || !isfinite(gamma);
     const bool conv = tol > 0.0 && res <= tol * nb;
     if (tid == 0) {
         d.res_hist[t0 + p] = res / nb;
         ist[ST_PDONE] = p;
-        ist[ST_MODE_IT] = p;
-        if (nonfinite) { ist[ST_STATUS] = STOP_NONFINITE; ist[ST_MODE] = 0; }
-        else if (bd) { ist[ST_STATUS] = STOP_BREAKDOWN; ist[ST_MODE] = 0; ist[ST_BASIS] = p; }
+        if (nonfinite) ist[ST_STATUS] = STOP_NONFINITE;
+        else if (bd) { ist[ST_STATUS] = STOP_BREAKDOWN; ist[ST_BASIS] = p; }
         else {
-            d.scal[SC_GAMMA] = gamma;
             ist[ST_BASIS] = p + 1;
-            if (conv || drain) { ist[ST_STATUS] = conv ? STOP_CONVERGED : STOP_END; ist[ST_MODE] = 1; }
-            else ist[ST_MODE] = 3;
+            if (conv || drain) ist[ST_STATUS] = conv ? STOP_CONVERGED : STOP_END;
         }
     }
-    if (nonfinite || bd || conv || drain) {
-        if (gs == 2) for (int i = tid; i < p; i += blockDim.x) d.alpha[i] = s_a[i];  // v_p still written
-        return;
-    }
+    if (gs == 1 || nonfinite || bd || conv || drain) return;
+    // Step 15, derived (reading R1): hp[:p+1, p] = r1 - H[:p+1, :p] (r2 / gamma); H is upper
+    // Hessenberg, so row i only meets columns j >= i-1 (the skipped terms are exact zeros)
+    for (int j = tid; j < p; j += blockDim.x) s_t[j] = d.L[p + (int64_t)j * M];
     __syncthreads();
-
-    if (gs == 2) {
-        // Steps 7-9: c /= gamma ; d /= gamma^2 ; L[p, :p] = r2 / gamma  (reading R4)
-        const double dd = s_c[p] / (gamma * gamma);
-        double part = 0.0;
-        for (int i = tid; i < p; i += blockDim.x) {
-            const double ci = s_c[i] / gamma;
-            const double li = s_a[i] / gamma;
-            s_c[i] = ci;
-            s_t[i] = li;
-            d.L[p + (int64_t)i * M] = li;
-            part += li * ci;
-            d.alpha[i] = s_a[i];
+    for (int i = tid; i <= p; i += blockDim.x) {
+        double sacc = 0.0;
+        int j = i > 0 ? i - 1 : 0;
+        for (; j + 8 <= p; j += 8) {
+            double hv[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) hv[c] = d.H[i + (int64_t)(j + c) * d.ldh];
+#pragma unroll
+            for (int c = 0; c < 8; c++) sacc += hv[c] * s_t[j + c];
         }
-        // Step 12 (Stephen's trick): r1 = [c ; d - L[p,:p] . c]
-        const double acc = block_sum(part, red);
-        for (int i = tid; i < p; i += blockDim.x) { d.beta[i] = s_c[i]; s_x[i] = s_c[i]; }
-        if (tid == 0) { const double r1p = dd - acc; d.beta[p] = r1p; s_x[p] = r1p; }
-        __syncthreads();
-        // Step 15, derived (reading R1): hp[:p+1, p] = r1 - H[:p+1, :p] (r2 / gamma)
-        for (int i = tid; i <= p; i += blockDim.x) {
-            double sacc = 0.0;
-            for (int j = 0; j < p; j++) sacc += d.H[i + (int64_t)j * d.ldh] * s_t[j];
-            d.HP[i + (int64_t)p * d.ldh] = s_x[i] - sacc;
-        }
-    } else {
-        // Alg. 2 Steps 8-10: c /= gamma ; c[p] /= gamma ; L[p, :p] = a / gamma
-        for (int i = tid; i <= p; i += blockDim.x) {
-            double ci = s_c[i] / gamma;
-            if (i == p) ci = ci / gamma;  // reading R5
-            s_x[i] = ci;
-        }
-        for (int i = tid; i < p; i += blockDim.x) d.L[p + (int64_t)i * M] = s_a[i] / gamma;
-        __syncthreads();
-        // Step 12: r1 = (I + L_{p+1})^{-1} c ; Step 17 (r3 = 0): H[:p+1, p] = r1
-        trisolve_smem(p + 1, d.L, M, s_x);
-        for (int i = tid; i <= p; i += blockDim.x) {
-            d.beta[i] = s_x[i];
-            d.H[i + (int64_t)p * d.ldh] = s_x[i];
-        }
+        for (; j < p; j++) sacc += d.H[i + (int64_t)j * d.ldh] * s_t[j];
+        d.HP[i + (int64_t)p * d.ldh] = d.beta[i] - sacc;
     }
 }
 

@@ -228,6 +228,6 @@ def test_kernel_timing_counts(P):
     s.solve(torch.from_numpy(prob.b).cuda(), k=40, gs_iters=2)
     ks = s.kernel_stats()
     assert ks["block_dot"]["launches"] == 41 and ks["update"]["launches"] == 42
-    assert ks["spmv"]["launches"] == 40 and ks["small"]["launches"] == 42
+    assert ks["spmv"]["launches"] == 40 and ks["small"]["launches"] == 2 + 2 * 40
     assert all(v["ms"] >= 0 for v in ks.values())
     s.close()
