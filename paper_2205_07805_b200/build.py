@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libigs.so")
-SOURCES = ["kernels.cu", "api.cu", "plan.cpp"]
+SOURCES = ["kernels.cu", "fused.cu", "api.cu", "plan.cpp"]
 HEADERS = ["igs_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

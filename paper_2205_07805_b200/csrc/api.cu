@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -115,6 +116,14 @@ struct igs_ctx {
     double t_bytes[IGS_K_COUNT] = {0};
     int64_t t_launch[IGS_K_COUNT] = {0};
     int64_t tail_launches = 0;  // side-stream small-step tails (untimed)
+    // fused wavefront path (single GPU): reach = max |col - row|, flags per 128-row tile
+    int64_t reach = 0;
+    bool fused_enabled = false;  // IGS_FUSED=1 enables the wavefront kernel (experimental)
+    double fused_budget = 72e6;  // bytes of V the L2 must hold between phase A and phase B
+    int fused_grid = 0;
+    long long* d_flags = nullptr;  // per-CTA progress words of the fused kernel
+    int epoch = 0;
+    int64_t n_fused = 0;
 };
 
 // ------------------------------------------------------------------------------ misc
@@ -301,6 +310,7 @@ static void free_ctx(igs_ctx* c) {
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
     cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter);
     cudaFree(c->d_gram);
+    cudaFree(c->d_flags);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
     for (auto e : c->events) cudaEventDestroy(e);
@@ -431,6 +441,21 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         ctx->A.lpr = avg <= 8.0 ? 0 : lpr;
     }
     ctx->bdot_grid = bdot_grid_size(n_local, ctx->num_sms);
+    {
+        int64_t reach = 0;
+        for (int64_t i = 0; i < n_local; i++)
+            for (int64_t q = rowptr[i]; q < rowptr[i + 1]; q++) {
+                const int64_t cc = colind_bits == 64 ? static_cast<const int64_t*>(colind)[q]
+                                                     : (int64_t) static_cast<const int32_t*>(colind)[q];
+                const int64_t d = cc - (row_begin + i);
+                reach = std::max(reach, d < 0 ? -d : d);
+            }
+        ctx->reach = reach;
+        ctx->fused_grid = fused_grid(ctx->num_sms);
+        if (ctx->fused_grid > ctx->bdot_grid) ctx->bdot_grid = ctx->fused_grid;
+        if (const char* e = std::getenv("IGS_FUSED")) ctx->fused_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_FUSED_L2_MB")) ctx->fused_budget = std::atof(e) * 1e6;
+    }
     cudaError_t e;
     if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->ev_crit, cudaEventDisableTiming)) != cudaSuccess ||
@@ -541,6 +566,10 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         CUDA_TRY(cudaMalloc(&ctx->d_z, sizeof(double) * ldv));
         CUDA_TRY(cudaMemsetAsync(ctx->d_z, 0, sizeof(double) * ldv, ctx->stream));
     }
+    if (!ctx->d_flags && ctx->nranks == 1) {
+        CUDA_TRY(cudaMalloc(&ctx->d_flags, sizeof(long long) * (ctx->fused_grid + 1)));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(long long) * (ctx->fused_grid + 1), ctx->stream));
+    }
     if (!ctx->d_counter) {
         CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 4));
         CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned) * 4, ctx->stream));
@@ -643,12 +672,15 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int ev_slot = 0, ev_pending = -1;
     int* h_status = ctx->h_pinned_int + 16;  // 2 slots
+    bool dots_ready = false;  // dots of iteration p already produced by the fused kernel
     for (int p = 1; p <= m; p++) {
         const bool drain = (p == m);
         double* u = Vcol(ctx, p);
         if (p > 1) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));  // tail(p-1): status, H
-        if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
-        TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
+        if (!dots_ready) {
+            if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
+            TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
+        }
         TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_CRIT, gs, p, m, t0, st));
         // tail of the small step on the side stream, overlapped with the fused update
         CUDA_TRY(cudaEventRecord(ctx->ev_crit, st));
@@ -658,10 +690,31 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
         CUDA_TRY(cudaGetLastError());
         if (ctx->timing) ctx->tail_launches++;
         CUDA_TRY(cudaEventRecord(ctx->ev_tail, ctx->side));
-        const double ub = 8.0 * n * ((gs == 2 || !drain) ? p : 0) + 16.0 * n + (drain ? 0.0 : 16.0 * n);
-        TIMED(IGS_K_UPDATE, ub,
-              launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
-                            d.beta, d.scal + SC_GAMMA, u, drain ? nullptr : Vcol(ctx, p + 1), ist, p, st));
+        const int T = fused_tile_rows();
+        const double window = (double)(ctx->reach + (int64_t)ctx->fused_grid * T + 2 * T) * (p + 3) * 8.0;
+        if (!drain && ctx->nranks == 1 && ctx->fused_enabled && ctx->d_flags && p + 2 <= fused_max_cols() &&
+            window <= ctx->fused_budget && n >= 4 * T) {
+            // update(p) + SpMV(p+1) + block dot(p+1), V_p read from HBM once
+            const int lag = (int)((ctx->reach + T - 1) / T) + 1;
+            const bool dr1 = (p + 1 == m);
+            const double by = 8.0 * n * p + 32.0 * n + (dr1 ? 0.0 : spmv_bytes(ctx) - 8.0 * n);
+            ctx->epoch++;
+            TIMED(IGS_K_UPDATE, by, {
+                cudaError_t e_ = launch_fused(n, p, m, ctx->d_V, ctx->ldv, ctx->d_z, gs == 2 ? d.alpha : nullptr,
+                                              d.beta, d.scal + SC_GAMMA, ctx->A, lag, ctx->d_flags, ctx->epoch,
+                                              ctx->d_part, d.dots + (int64_t)(p + 1) * d.dld, ctx->d_counter,
+                                              ist, ctx->fused_grid, st);
+                CUDA_TRY(e_);
+            });
+            ctx->n_fused++;
+            dots_ready = true;
+        } else {
+            const double ub = 8.0 * n * ((gs == 2 || !drain) ? p : 0) + 16.0 * n + (drain ? 0.0 : 16.0 * n);
+            TIMED(IGS_K_UPDATE, ub,
+                  launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
+                                d.beta, d.scal + SC_GAMMA, u, drain ? nullptr : Vcol(ctx, p + 1), ist, p, st));
+            dots_ready = false;
+        }
         ctx->n_iter++;
         // checkpoint: copy the status word; decide on the PREVIOUS checkpoint's value so the
         // GPU always has one chunk queued and every rank stops at the same iteration

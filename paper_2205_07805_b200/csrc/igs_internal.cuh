@@ -99,4 +99,14 @@ void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, 
 // small helpers
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
 
+// fused.cu: update(p) + SpMV(p+1) + block dot(p+1) in one persistent wavefront kernel
+int fused_max_cols();
+int fused_tile_rows();
+int fused_grid(int num_sms);
+cudaError_t launch_fused(int64_t n, int p, int m, const double* V, int64_t ld, double* z,
+                         const double* alpha, const double* beta, const double* gamma_dev,
+                         const SpmvArgs& A, int lag, long long* progress, int epoch, double* part,
+                         double* out, unsigned* counter, const int* istate, int grid,
+                         cudaStream_t s);
+
 }  // namespace igs

@@ -231,3 +231,41 @@ def test_kernel_timing_counts(P):
     assert ks["spmv"]["launches"] == 40 and ks["small"]["launches"] == 2 + 2 * 40
     assert all(v["ms"] >= 0 for v in ks.values())
     s.close()
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+def test_fused_wavefront_matches_unfused(P, gs, monkeypatch):
+    """The persistent update+SpMV+block-dot kernel (fused.cu) vs the three-kernel path:
+    same iterations, H to rounding, and both against the oracle."""
+    import torch
+    prob = W.config("c4", N=40)             # reach = 1600 rows: lag 14 tiles, 500 tiles
+    outs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("IGS_FUSED", fused)
+        s = P.Solver(prob.A)
+        s.set_timing(2)
+        outs[fused] = s.solve(torch.from_numpy(prob.b).cuda(), k=60, gs_iters=gs, want_loo=True)
+        outs[fused]["launches"] = s.kernel_stats()
+        s.close()
+    f, u = outs["1"], outs["0"]
+    assert f["launches"]["block_dot"]["launches"] < u["launches"]["block_dot"]["launches"]  # fused ran
+    assert f["iters"] == u["iters"] == 60
+    assert oracle.column_normwise_diff(f["H"], u["H"], 60) <= 1e-12
+    o = oracle.gmres(prob.A, prob.b, 60, variant=VARIANT[gs], dot_block=4096, want_V=True)
+    d, _ = _compare_cols(f["H"], o["H"], o["res_hist"])
+    assert d <= 1e-10
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    assert _loo_ok(prob, gs, 60, f["loo"], lo), (f["loo"], lo)
+    np.testing.assert_allclose(f["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-13)
+
+
+def test_fused_deterministic(P):
+    import torch
+    prob = W.config("c3", N=96)
+    s = P.Solver(prob.A)
+    b = torch.from_numpy(prob.b).cuda()
+    a = s.solve(b, k=80, gs_iters=2)
+    c = s.solve(b, k=80, gs_iters=2)
+    assert a["H"].tobytes() == c["H"].tobytes()
+    assert a["x"].cpu().numpy().tobytes() == c["x"].cpu().numpy().tobytes()
+    s.close()
