@@ -14,7 +14,7 @@ needed between steps.  N > 1: the same 256^3 problem row-block sharded over N ra
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 --impl reference times the CPU oracle (oracle/, plain FP64 C + OpenMP) on the host cores,
-rank 0 only; each step is a bounded sample (the first 20 Arnoldi iterations of the same
+rank 0 only; each step is a bounded sample (the first 50 Arnoldi iterations of the same
 cycle), projected to the cycle-average iteration with the byte model of DESIGN.md.
 """
 from __future__ import annotations
@@ -36,7 +36,15 @@ METRIC = "Arnoldi iterations/s and achieved HBM GB/s (fraction of roofline) at 1
 UNIT = "Arnoldi iterations/s"
 N_GRID = 256
 M = 100                     # GMRES(100)
-CPU_SAMPLE_ITERS = 20       # oracle sample: iterations 1..20 of the cycle
+CPU_SAMPLE_ITERS = 50       # oracle sample: iterations 1..50 of the cycle (~10 s on 16 cores)
+
+
+def bench_config(gs: int, world: int) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": f"c4: 3D 7-point convection-diffusion 256^3, GMRES(100) cycle, gs_iters={gs} "
+                        f"({'Alg. 3' if gs == 2 else 'Alg. 2, one sweep'})",
+            "n": N_GRID ** 3, "nnz": 7 * N_GRID ** 3 - 6 * N_GRID ** 2, "restart": M,
+            "parallelism": f"row-block x{world}", "l2": "inputs larger than L2 (V = 13.6 GB), no flush"}
 
 
 def byte_model(n: int, nnz: int, p: int, s_col: int = 4, s_ptr: int = 4) -> float:
@@ -144,7 +152,8 @@ def run_reference(args, rank, world):
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        o = oracle.gmres(A, b, CPU_SAMPLE_ITERS, restart=M, tol=0.0, variant="igs2", dot_block=4096)
+        o = oracle.gmres(A, b, CPU_SAMPLE_ITERS, restart=M, tol=0.0, variant="igs2" if args.gs == 2 else "igs1",
+                         dot_block=4096)
         dt = time.perf_counter() - t0
         assert o["iters"] == CPU_SAMPLE_ITERS
         if i >= args.warmup:
@@ -152,15 +161,14 @@ def run_reference(args, rank, world):
     t = float(np.mean(times))
     gbs = sample_bytes / t / 1e9
     val = gbs * 1e9 / cycle_avg_bytes(n, nnz)            # projected to the cycle average
-    sample = (f"oracle igs2 (Alg. 3), first {CPU_SAMPLE_ITERS} Arnoldi iterations of the c4 "
+    sample = (f"oracle gs_iters={args.gs}, first {CPU_SAMPLE_ITERS} Arnoldi iterations of the c4 "
               f"GMRES(100) cycle per step ({t:.1f} s); it/s projected to the 100-iteration cycle "
               f"average by the byte model (sample ran {CPU_SAMPLE_ITERS / t:.3f} it/s, {gbs:.1f} GB/s)")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, workloads/)",
-            "config": {"workload": "c4: 3D 7-point convection-diffusion 256^3, GMRES(100), Alg. 3 (gs_iters=2)",
-                       "n": n, "nnz": nnz, "restart": M, "l2": "inputs larger than L2 (no flush)"},
+            "config": bench_config(args.gs, world),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
                              "gbs": gbs},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -318,10 +326,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, workloads/)",
-            "config": {"workload": "c4: 3D 7-point convection-diffusion 256^3, GMRES(100) cycle, "
-                                   f"Alg. 3 (gs_iters={args.gs})",
-                       "n": n_global, "nnz": nnz_g, "restart": M, "parallelism": f"row-block x{world}",
-                       "l2": "inputs larger than L2 (V = 13.6 GB), no flush"},
+            "config": bench_config(args.gs, world),
             "achieved_gbs_per_iteration_model": gbs_iter,
             "roofline_frac_iteration": gbs_iter / (peak * world),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,

@@ -269,3 +269,26 @@ def test_fused_deterministic(P):
     assert a["H"].tobytes() == c["H"].tobytes()
     assert a["x"].cpu().numpy().tobytes() == c["x"].cpu().numpy().tobytes()
     s.close()
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+def test_c4_full_size_first_columns(P, gs):
+    """BASELINE config c4 at full size (n = 16.8M) in bench.py's launch configuration
+    (GMRES(100), default kernels): the first 20 Hessenberg columns against the oracle."""
+    prob = W.config("c4")
+    g, o = run_pair(P, prob, gs, k=20, restart=100, tol=0.0, want_loo=True)
+    d, _ = _compare_cols(g["H"], o["H"], o["res_hist"], ncols=20)
+    assert d <= 1e-10, d
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    assert _loo_close(g["loo"], lo) or gs == 1 and g["loo"] <= 10 * lo, (g["loo"], lo)
+    np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-8)
+
+
+def test_c5_full_size_int64_first_columns(P):
+    """BASELINE config c5 (512^3, n = 134M, nnz = 938M, int64 column indices) on one GPU:
+    the int64 CSR path at full size, first 6 Hessenberg columns against the oracle."""
+    prob = W.config("c5")
+    assert prob.A.colind.dtype == np.int64
+    g, o = run_pair(P, prob, 2, k=6, restart=0, tol=0.0, want_loo=False)
+    d, _ = _compare_cols(g["H"], o["H"], o["res_hist"], ncols=6)
+    assert d <= 1e-10, d
