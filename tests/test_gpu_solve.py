@@ -259,8 +259,9 @@ def test_fused_wavefront_matches_unfused(P, gs, monkeypatch):
     np.testing.assert_allclose(f["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-13)
 
 
-def test_fused_deterministic(P):
+def test_fused_deterministic(P, monkeypatch):
     import torch
+    monkeypatch.setenv("IGS_FUSED", "1")
     prob = W.config("c3", N=96)
     s = P.Solver(prob.A)
     b = torch.from_numpy(prob.b).cuda()
