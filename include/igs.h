@@ -62,6 +62,15 @@ typedef enum {
     IGS_TERM_BREAKDOWN = 2  /* (happy) breakdown: H[p,p-1] ~ 0 (reading R12) -- NOT an error */
 } igs_term;
 
+/* Algorithms of igs_solve_alg.  IGS_ALG_IGS1 and IGS_ALG_IGS2 are what igs_solve's gs_iters
+ * 1 and 2 select; the other two are SURVEY §8(f) NEXT-1 / NEXT-3. */
+typedef enum {
+    IGS_ALG_IGS1 = 1,     /* Alg. 2 Steps 1-13 + 17, one Gauss-Seidel sweep: 1 reduction/iteration */
+    IGS_ALG_IGS2 = 2,     /* Alg. 3, one-reduce hybrid MGS-CGS: 1 reduction/iteration */
+    IGS_ALG_IGS2_TWO = 3, /* Alg. 2 literal, two sweeps: 2 reductions/iteration */
+    IGS_ALG_MGS = 4       /* MGS-GMRES: j+2 reductions at column j */
+} igs_alg;
+
 /* Per-kernel timing classes (igs_kernel_stats). */
 typedef enum {
     IGS_K_SPMV = 0,      /* z = A u (+ halo pack)                           */
@@ -121,6 +130,9 @@ typedef struct {
     int h_cols;            /* out: columns of H filled in cycle 1                             */
     int basis_cols;        /* out: normalised columns of the final basis (LOO is over these)  */
     int64_t allreduces;    /* out: NCCL allreduces issued by this solve (0 when nranks == 1)  */
+    int64_t reductions;    /* out: global reductions (device block dots, each followed by one
+                              allreduce when nranks > 1) issued by this solve -- the paper's
+                              synchronization count                            */
 } igs_result;
 
 /* Solve A x = b by restarted IGS-GMRES.
@@ -138,6 +150,11 @@ typedef struct {
  * Breakdown is reported via res->term, not as an error. */
 igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, const double* x0, int k,
                      int restart, double tol, int gs_iters, igs_result* res);
+
+/* Same as igs_solve with an explicit algorithm (igs_alg); igs_solve(gs_iters = g) ==
+ * igs_solve_alg(algorithm = g). */
+igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double* b, const double* x0, int k,
+                         int restart, double tol, int algorithm, igs_result* res);
 
 /* Cumulative counters since create: NCCL allreduces, halo messages, Arnoldi iterations. */
 igs_status igs_stats(const igs_ctx* ctx, int64_t* allreduces, int64_t* halo_msgs,

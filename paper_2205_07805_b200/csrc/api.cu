@@ -107,7 +107,7 @@ struct igs_ctx {
     size_t bound_bytes = 0;
     bool owns_ws = true;
     // counters
-    int64_t n_allreduce = 0, n_halo = 0, n_iter = 0;
+    int64_t n_allreduce = 0, n_halo = 0, n_iter = 0, n_reduce = 0;
     // timing
     bool timing = false;
     std::vector<cudaEvent_t> events;
@@ -490,6 +490,7 @@ static size_t small_doubles(int m, int k) {
            + (m + 2)        // g
            + (m + 1) * dld  // dots
            + 4 * (m + 2)    // alpha, beta, y, gam
+           + (m + 3)        // dots2
            + SC_COUNT + (k + 2);
 }
 
@@ -556,6 +557,7 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.beta = take(mm + 2);
         d.y = take(mm + 2);
         d.gam = take(mm + 2);
+        d.dots2 = take(mm + 3);
         d.scal = take(SC_COUNT);
         d.res_hist = take(kk + 2);
         d.istate = ctx->d_int;
@@ -631,6 +633,7 @@ static igs_status bdot(igs_ctx* ctx, int p, const double* u, const double* z, do
           launch_block_dot(ctx->n_local, p, ctx->d_V, ctx->ldv, u, z, out, ctx->d_part,
                            ctx->d_counter, ctx->bdot_grid, istate, ctx->stream));
     TRY(allreduce(ctx, out, z ? 2 * (p + 1) : p + 1));
+    ctx->n_reduce++;
     return IGS_OK;
 }
 
@@ -648,7 +651,14 @@ static igs_status fetch(igs_ctx* ctx, const double* dsrc, int nd, double* hd, co
 // One restart cycle of m iterations (SURVEY §8(c) "Cycle priming" + per-iteration body).
 // On entry z holds r = b - A x and dots[0] = ||r||^2.  Returns after enqueueing (and occasionally waiting at
 // checkpoints, identically on every rank).
-static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
+static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0);
+
+// alg: IGS_ALG_IGS1 (1), IGS_ALG_IGS2 (2, Alg. 3), IGS_ALG_IGS2_TWO (3, Alg. 2 literal),
+// IGS_ALG_MGS (4).  Algorithms 1 and 3 share the gs = 1 small-step stages.
+static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
+    if (alg == IGS_ALG_MGS) return run_cycle_mgs(ctx, m, t0);
+    const int gs = alg == IGS_ALG_IGS2 ? 2 : 1;
+    const bool two_reduce = alg == IGS_ALG_IGS2_TWO;
     Dev& d = ctx->dev_state;
     cudaStream_t st = ctx->stream;
     const int64_t n = ctx->n_local;
@@ -676,11 +686,13 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
     for (int p = 1; p <= m; p++) {
         const bool drain = (p == m);
         double* u = Vcol(ctx, p);
-        if (p > 1) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));  // tail(p-1): status, H
         if (!dots_ready) {
             if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
             TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
         }
+        // tail(p-1) (status, H column p-2, hp) must finish before this iteration's small step;
+        // it overlaps update(p-1), SpMV(p) and the block dot(p)
+        if (p > 1) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
         TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_CRIT, gs, p, m, t0, st));
         // tail of the small step on the side stream, overlapped with the fused update
         CUDA_TRY(cudaEventRecord(ctx->ev_crit, st));
@@ -692,7 +704,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
         CUDA_TRY(cudaEventRecord(ctx->ev_tail, ctx->side));
         const int T = fused_tile_rows();
         const double window = (double)(ctx->reach + (int64_t)ctx->fused_grid * T + 2 * T) * (p + 3) * 8.0;
-        if (!drain && ctx->nranks == 1 && ctx->fused_enabled && ctx->d_flags && p + 2 <= fused_max_cols() &&
+        if (!drain && !two_reduce && ctx->nranks == 1 && ctx->fused_enabled && ctx->d_flags && p + 2 <= fused_max_cols() &&
             window <= ctx->fused_budget && n >= 4 * T) {
             // update(p) + SpMV(p+1) + block dot(p+1), V_p read from HBM once
             const int lag = (int)((ctx->reach + T - 1) / T) + 1;
@@ -714,6 +726,16 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
                   launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
                                 d.beta, d.scal + SC_GAMMA, u, drain ? nullptr : Vcol(ctx, p + 1), ist, p, st));
             dots_ready = false;
+            if (two_reduce && !drain) {
+                // Alg. 2 Steps 14-16: r2 = V_{p+1}^T u (second reduction), r3 = (I+L)^{-1} r2,
+                // w = u - V_{p+1} r3 (in place), H[:p+1, p] = r1 + r3
+                double* un = Vcol(ctx, p + 1);
+                TRY(bdot(ctx, p + 1, un, nullptr, d.dots2, ist, IGS_K_BLOCK_DOT));
+                TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_CRIT2, gs, p, m, t0, st));
+                TIMED(IGS_K_UPDATE, 8.0 * n * (p + 1) + 16.0 * n,
+                      launch_update(n, p + 1, ctx->d_V, ctx->ldv, un, nullptr, d.alpha, nullptr,
+                                    d.scal + SC_ONE, un, nullptr, ist, p, st));
+            }
         }
         ctx->n_iter++;
         // checkpoint: copy the status word; decide on the PREVIOUS checkpoint's value so the
@@ -739,11 +761,67 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int gs, int t0) {
     return IGS_OK;
 }
 
+// MGS-GMRES cycle (the sync-count baseline): column j needs j+1
+// separate inner products and one norm, each a device reduction (+ allreduce when G > 1).
+static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0) {
+    Dev& d = ctx->dev_state;
+    cudaStream_t st = ctx->stream;
+    const int64_t n = ctx->n_local;
+    const int* ist = d.istate;
+    CUDA_TRY(cudaMemsetAsync(d.H, 0, sizeof(double) * (size_t)d.ldh * d.m, st));
+    TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_PRIME_NORM, 1, 0, m, t0, st));
+    TIMED(IGS_K_UPDATE, 16.0 * n,
+          launch_update(n, 0, ctx->d_V, ctx->ldv, ctx->d_z, nullptr, nullptr, nullptr,
+                        d.scal + SC_GAMMA, Vcol(ctx, 0), nullptr, ist, 0, st));
+    const int poll_every = 16;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int ev_slot = 0, ev_pending = -1;
+    int* h_status = ctx->h_pinned_int + 16;
+    for (int j = 0; j < m; j++) {
+        TRY(spmv(ctx, Vcol(ctx, j), ctx->d_z, nullptr, false, ist, IGS_K_SPMV));
+        for (int i = 0; i <= j; i++) {
+            TRY(bdot(ctx, 0, Vcol(ctx, i), ctx->d_z, d.dots, ist, IGS_K_BLOCK_DOT));  // h = v_i . w
+            TIMED(IGS_K_UPDATE, 24.0 * n,
+                  launch_mgs_axpy(n, Vcol(ctx, i), ctx->d_z, d.dots + 1, d.H + i + (int64_t)j * d.ldh, ist, st));
+        }
+        TRY(bdot(ctx, 0, ctx->d_z, nullptr, d.dots, ist, IGS_K_BLOCK_DOT));          // ||w||^2
+        TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_MGS_NORM, 1, j + 1, m, t0, st));
+        TIMED(IGS_K_UPDATE, 16.0 * n,
+              launch_update(n, 0, ctx->d_V, ctx->ldv, ctx->d_z, nullptr, nullptr, nullptr,
+                            d.scal + SC_GAMMA, Vcol(ctx, j + 1), nullptr, ist, j + 1, st));
+        ctx->n_iter++;
+        if ((j + 1) % poll_every == 0 && j + 1 < m) {
+            if (!ev[0]) {
+                CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+                CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+            }
+            CUDA_TRY(cudaMemcpyAsync(h_status + ev_slot, ist + ST_STATUS, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaEventRecord(ev[ev_slot], st));
+            if (ev_pending >= 0) {
+                CUDA_TRY(cudaEventSynchronize(ev[ev_pending]));
+                if (h_status[ev_pending] != RUNNING) break;
+            }
+            ev_pending = ev_slot;
+            ev_slot ^= 1;
+        }
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
+    return IGS_OK;
+}
+
 extern "C" igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, const double* x0,
                                 int k, int restart, double tol, int gs_iters, igs_result* res) {
+    ARG_CHECK(gs_iters == 1 || gs_iters == 2, "igs_solve: gs_iters must be 1 or 2");
+    return igs_solve_alg(ctx, vec_mem, b, x0, k, restart, tol, gs_iters, res);
+}
+
+extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double* b, const double* x0,
+                                    int k, int restart, double tol, int algorithm, igs_result* res) {
+    const int gs_iters = algorithm;
     ARG_CHECK(ctx && ctx->ok, "igs_solve: bad context");
     ARG_CHECK(res && res->x && b, "igs_solve: NULL b / res / res->x");
-    ARG_CHECK(gs_iters == 1 || gs_iters == 2, "igs_solve: gs_iters must be 1 or 2");
+    ARG_CHECK(algorithm >= IGS_ALG_IGS1 && algorithm <= IGS_ALG_MGS, "igs_solve_alg: unknown algorithm");
     ARG_CHECK(k >= 1 && (int64_t)k < ctx->n_global - 1, "igs_solve: need 1 <= k < n_global - 1 (P:873)");
     ARG_CHECK(restart >= 0, "igs_solve: restart < 0");
     ARG_CHECK(tol >= 0.0 && std::isfinite(tol), "igs_solve: tol must be finite and >= 0");
@@ -776,7 +854,7 @@ extern "C" igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, 
         if (x0 && x0 != dx) CUDA_TRY(cudaMemcpyAsync(dx, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         else if (!x0) CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(double) * n, st));
     }
-    const int64_t ar0 = ctx->n_allreduce;
+    const int64_t ar0 = ctx->n_allreduce, red0 = ctx->n_reduce;
 
     // ||b|| (one reduction; also the non-finite check of b)
     double* dsc = d.scal;
@@ -809,6 +887,7 @@ extern "C" igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, 
         double hs[SC_COUNT] = {0};
         hs[SC_NB] = nb;
         hs[SC_TOL] = tol;
+        hs[SC_ONE] = 1.0;
         CUDA_TRY(cudaMemcpyAsync(dsc, hs, sizeof(hs), cudaMemcpyHostToDevice, st));
     }
     int total = 0, cycles = 0, last_basis = 0;
@@ -883,6 +962,7 @@ extern "C" igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, 
     CUDA_TRY(cudaGetLastError());
     if (res->res_hist) std::memcpy(res->res_hist, hres.data(), sizeof(double) * (total + 1));
     res->allreduces = ctx->n_allreduce - ar0;
+    res->reductions = ctx->n_reduce - red0;
     TRY(timer_flush(ctx));
     return IGS_OK;
 }

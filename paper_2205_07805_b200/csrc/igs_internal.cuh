@@ -19,7 +19,7 @@ enum : int {
     ST_COUNT = 8
 };
 // scal slots (device doubles)
-enum : int { SC_GAMMA = 0, SC_RHO = 1, SC_NB = 2, SC_TOL = 3, SC_COUNT = 8 };
+enum : int { SC_GAMMA = 0, SC_RHO = 1, SC_NB = 2, SC_TOL = 3, SC_ONE = 4, SC_COUNT = 8 };
 
 constexpr double kEps = 2.220446049250313e-16;
 constexpr double kBreakdownC = 64.0;  // reading R12
@@ -41,6 +41,7 @@ struct Dev {
     double* beta;   // [m+1] update coefficients (r^(1)) for u'
     double* y;      // [m+1] least-squares solution
     double* gam;    // [m+2] gamma of iteration p (written by crit, read by tail)
+    double* dots2;  // [m+3] second reduction of Alg. 2 (two-reduce): V_{p+1}^T u
     double* scal;   // [SC_COUNT]
     int* istate;    // [ST_COUNT]
     double* res_hist;  // [kmax+1]
@@ -80,7 +81,13 @@ void launch_xupdate(int64_t n, const double* V, int64_t ld, const double* y, dou
                     const int* istate, int pmax, cudaStream_t s);
 
 // Small steps (one CTA, replicated on every rank).
-enum SmallStage : int { SS_PRIME_NORM = 0, SS_PRIME_H = 1, SS_CRIT = 2, SS_TAIL = 3, SS_LSQ = 4 };
+enum SmallStage : int { SS_PRIME_NORM = 0, SS_PRIME_H = 1, SS_CRIT = 2, SS_TAIL = 3, SS_LSQ = 4,
+                        SS_CRIT2 = 5,      // Alg. 2 Steps 15, 17: r3 = (I+L)^{-1} r2, H += r3
+                        SS_MGS_NORM = 6 }; // MGS: h_{j+1,j} = ||w||, Givens, status
+
+// MGS step: h = dots[1] (v_i . z); H[i,j] = h; z -= h v_i  (one projection of modified GS)
+void launch_mgs_axpy(int64_t n, const double* v, double* z, const double* hsrc, double* Hdst,
+                     const int* istate, cudaStream_t s);
 void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s);
 
 // x = (I + L)^{-1} b (test entry point; same device routine as the small step).

@@ -554,6 +554,7 @@ __global__ void __launch_bounds__(UP_THREADS)
     if (istate) {
         const volatile int* vs = istate;
         mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
+        mode &= default_mode;  // never write u' without a u' buffer
     }
     if (mode == 0) return;
     const bool want_next = (mode & 2) != 0;
@@ -823,7 +824,65 @@ __global__ void __launch_bounds__(SS_THREADS)
         return;
     }
 
+    if (stage == SS_CRIT2 && *(volatile int*)(ist + ST_STATUS) != RUNNING) {
+        if (tid == 0) ist[ST_MODE] = 0;  // the second update must not run either
+        return;
+    }
     if (*(volatile int*)(ist + ST_STATUS) != RUNNING) return;
+
+    if (stage == SS_CRIT2) {
+        // Alg. 2 two-reduce, second Gauss-Seidel sweep: r2 = V_{p+1}^T u is in
+        // dots2; r3 = (I + L_{p+1})^{-1} r2 (Step 15); H[:p+1, p] = r1 + r3 (Step 17);
+        // alpha = r3 for w = u - V_{p+1} r3 (Step 16)
+        if (ist[ST_MODE_IT] != p || ist[ST_MODE] != 3) {
+            if (tid == 0) ist[ST_MODE] = 0;
+            return;
+        }
+        for (int i = tid; i <= p; i += blockDim.x) s_x[i] = d.dots2[i];
+        trisolve_smem(p + 1, d.L, M, s_x);
+        for (int i = tid; i <= p; i += blockDim.x) {
+            d.H[i + (int64_t)p * d.ldh] = d.H[i + (int64_t)p * d.ldh] + s_x[i];
+            d.alpha[i] = s_x[i];
+        }
+        __syncthreads();
+        if (tid == 0) ist[ST_MODE] = 1;  // the second update writes w in place
+        return;
+    }
+    if (stage == SS_MGS_NORM) {
+        // MGS-GMRES: gamma = ||w|| after the j+1 projections of column
+        // j = p-1; H[p, p-1] = gamma, Givens, status; v_p = w / gamma by the update kernel
+        const int j = p - 1;
+        const double s2 = d.dots[0];
+        const double gamma = sqrt(s2);
+        double h2 = 0.0;
+        for (int i = tid; i <= j; i += blockDim.x) {
+            const double h = d.H[i + (int64_t)j * d.ldh];
+            h2 += h * h;
+        }
+        const double hn2 = block_sum(h2, red);
+        const bool bd = !(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma));
+        if (tid == 0) d.H[p + (int64_t)j * d.ldh] = gamma;
+        __syncthreads();
+        const double res = givens_column(d, j, s_col, s_cs, s_sn, red);
+        const double tol = d.scal[SC_TOL], nb = d.scal[SC_NB];
+        const bool nonfinite = !isfinite(s2) || !isfinite(res) || !isfinite(hn2);
+        const bool conv = tol > 0.0 && res <= tol * nb;
+        if (tid == 0) {
+            d.res_hist[t0 + p] = res / nb;
+            ist[ST_PDONE] = p;
+            ist[ST_MODE_IT] = p;
+            d.scal[SC_GAMMA] = gamma;
+            if (nonfinite) { ist[ST_STATUS] = STOP_NONFINITE; ist[ST_MODE] = 0; }
+            else if (bd) { ist[ST_STATUS] = STOP_BREAKDOWN; ist[ST_MODE] = 0; ist[ST_BASIS] = p; }
+            else {
+                ist[ST_MODE] = 1;
+                ist[ST_BASIS] = p + 1;
+                if (conv || p == m) ist[ST_STATUS] = conv ? STOP_CONVERGED : STOP_END;
+            }
+        }
+        return;
+    }
+
     const double* dv = d.dots + (int64_t)p * d.dld;
     const bool drain = (p == m);
     const double s = dv[p];
@@ -1056,6 +1115,20 @@ void launch_loo_norm(int c, const double* G, double* out, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------------------------
+__global__ void mgs_axpy_kernel(int64_t n, const double* __restrict__ v, double* __restrict__ z,
+                                const double* __restrict__ hsrc, double* Hdst, const int* istate) {
+    if (!running(istate)) return;
+    const double h = *hsrc;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *Hdst = h;
+    if (i < n) z[i] = z[i] - h * v[i];
+}
+
+void launch_mgs_axpy(int64_t n, const double* v, double* z, const double* hsrc, double* Hdst,
+                     const int* istate, cudaStream_t s) {
+    mgs_axpy_kernel<<<(unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1), 256, 0, s>>>(n, v, z, hsrc, Hdst, istate);
+}
+
 __global__ void pack_kernel(int64_t cnt, const int64_t* __restrict__ idx,
                             const double* __restrict__ x, double* __restrict__ buf,
                             const int* istate) {

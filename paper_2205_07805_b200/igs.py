@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "OK", 1: "ERR_ARG", 2: "ERR_CUDA", 3: "ERR_NCCL", 4: "ERR_OOM
 
 # every symbol include/igs.h declares
 EXPORTS = ["igs_create", "igs_nccl_unique_id", "igs_workspace_bytes", "igs_bind_workspace",
-           "igs_solve", "igs_stats", "igs_set_timing", "igs_kernel_stats", "igs_destroy",
+           "igs_solve", "igs_solve_alg", "igs_stats", "igs_set_timing", "igs_kernel_stats", "igs_destroy",
            "igs_last_error", "igs_op_block_dot", "igs_op_spmv", "igs_op_update",
            "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap"]
 
@@ -40,7 +40,8 @@ class igs_result(ctypes.Structure):
     _fields_ = [("x", ctypes.c_void_p), ("H", ctypes.c_void_p), ("res_hist", ctypes.c_void_p),
                 ("want_loo", ctypes.c_int), ("loo_frob", ctypes.c_double), ("iters", ctypes.c_int),
                 ("cycles", ctypes.c_int), ("term", ctypes.c_int), ("true_relres", ctypes.c_double),
-                ("h_cols", ctypes.c_int), ("basis_cols", ctypes.c_int), ("allreduces", ctypes.c_int64)]
+                ("h_cols", ctypes.c_int), ("basis_cols", ctypes.c_int), ("allreduces", ctypes.c_int64),
+                ("reductions", ctypes.c_int64)]
 
 
 _lib = None
@@ -60,6 +61,7 @@ def lib() -> ctypes.CDLL:
             "igs_workspace_bytes": [P, I],
             "igs_bind_workspace": [P, P, S],
             "igs_solve": [P, I, P, P, I, I, D, I, ctypes.POINTER(igs_result)],
+            "igs_solve_alg": [P, I, P, P, I, I, D, I, ctypes.POINTER(igs_result)],
             "igs_stats": [P, P, P, P],
             "igs_set_timing": [P, I],
             "igs_kernel_stats": [P, I, P, P, P],
@@ -132,6 +134,15 @@ def igs_solve(ctx: int, vec_mem: int, b, x0, k: int, restart: int, tol: float, g
               res: igs_result):
     _check(lib().igs_solve(ctx, vec_mem, _ptr(b), _ptr(x0), int(k), int(restart), float(tol),
                            int(gs_iters), ctypes.byref(res)), "igs_solve")
+
+
+ALGORITHMS = {"igs1": 1, "igs2": 2, "alg3": 2, "igs2_two": 3, "mgs": 4}
+
+
+def igs_solve_alg(ctx: int, vec_mem: int, b, x0, k: int, restart: int, tol: float, algorithm: int,
+                  res: igs_result):
+    _check(lib().igs_solve_alg(ctx, vec_mem, _ptr(b), _ptr(x0), int(k), int(restart), float(tol),
+                               int(algorithm), ctypes.byref(res)), "igs_solve_alg")
 
 
 def igs_stats(ctx: int) -> dict:
@@ -248,9 +259,11 @@ class Solver:
             pass
 
     def solve(self, b, *, k: int, restart: int = 0, tol: float = 0.0, gs_iters: int = 2,
-              x0=None, x_out=None, want_loo: bool = False, want_H: bool = True) -> dict:
+              x0=None, x_out=None, want_loo: bool = False, want_H: bool = True,
+              algorithm: Optional[str] = None) -> dict:
         """b/x0/x_out: torch CUDA tensors (IGS_MEM_DEVICE) or host arrays/tensors
-        (IGS_MEM_HOST: the H2D/D2H copies happen inside the call)."""
+        (IGS_MEM_HOST: the H2D/D2H copies happen inside the call).  algorithm in
+        {'igs1','igs2','igs2_two','mgs'} overrides gs_iters (igs_solve_alg)."""
         import torch
         dev = isinstance(b, torch.Tensor) and b.is_cuda
         if x_out is None:
@@ -264,11 +277,15 @@ class Solver:
         res.H = _ptr(H)
         res.res_hist = rh.ctypes.data
         res.want_loo = int(want_loo)
-        igs_solve(self.ctx, IGS_MEM_DEVICE if dev else IGS_MEM_HOST, b, x0, k, restart, tol,
-                  gs_iters, res)
+        if algorithm is None:
+            igs_solve(self.ctx, IGS_MEM_DEVICE if dev else IGS_MEM_HOST, b, x0, k, restart, tol,
+                      gs_iters, res)
+        else:
+            igs_solve_alg(self.ctx, IGS_MEM_DEVICE if dev else IGS_MEM_HOST, b, x0, k, restart, tol,
+                          ALGORITHMS[algorithm], res)
         out = dict(x=x_out, iters=res.iters, cycles=res.cycles, term=TERM[res.term],
                    true_relres=res.true_relres, loo=res.loo_frob, h_cols=res.h_cols,
-                   basis_cols=res.basis_cols, allreduces=res.allreduces,
+                   basis_cols=res.basis_cols, allreduces=res.allreduces, reductions=res.reductions,
                    res_hist=rh[:res.iters + 1], m=m1)
         if want_H:
             out["H"] = H.reshape(m1, m1 + 1).T

@@ -293,3 +293,70 @@ def test_c5_full_size_int64_first_columns(P):
     g, o = run_pair(P, prob, 2, k=6, restart=0, tol=0.0, want_loo=False)
     d, _ = _compare_cols(g["H"], o["H"], o["res_hist"], ncols=6)
     assert d <= 1e-10, d
+
+
+ALG_ORACLE = {"igs1": "igs1", "igs2": "igs2", "igs2_two": "igs2_two", "mgs": "mgs"}
+
+
+def _reductions_one_cycle(alg, m):
+    """Global reductions of one unrestarted solve of m iterations (no early stop):
+    ||b|| + residual at cycle start + final residual, plus per algorithm: priming h and one
+    reduction per iteration (IGS1, Alg. 3), one more per non-drain iteration (Alg. 2
+    two-reduce), j+2 at column j (MGS)."""
+    if alg == "mgs":
+        return 3 + sum(j + 2 for j in range(m))
+    base = 3 + 1 + m
+    return base + (m - 1 if alg == "igs2_two" else 0)
+
+
+@pytest.mark.parametrize("alg", ["igs2_two", "mgs"])
+@pytest.mark.parametrize("cfg", ["c1", "c3_64"])
+def test_next_algorithms_parity(P, alg, cfg):
+    """SURVEY §8(f) NEXT-1 (Alg. 2 two-reduce) and NEXT-3 (MGS-GMRES) on the GPU vs the
+    oracle's implementation of the same algorithm."""
+    import torch
+    if cfg == "c1":
+        prob, k = W.config("c1"), 60
+    else:
+        prob, k = W.config("c3", N=64), 50
+    s = P.Solver(prob.A)
+    g = s.solve(torch.from_numpy(prob.b).cuda(), k=k, algorithm=alg, want_loo=True)
+    s.close()
+    o = oracle.gmres(prob.A, prob.b, k, variant=ALG_ORACLE[alg], dot_block=4096, want_V=True)
+    assert g["iters"] == o["iters"] == k
+    d, c = _compare_cols(g["H"], o["H"], o["res_hist"])
+    floor = oracle.column_normwise_diff(
+        oracle.gmres(prob.A, prob.b, k, variant=ALG_ORACLE[alg], dot_block=0)["H"], o["H"], c)
+    assert d <= 1e-10 or d <= 2 * floor, (d, floor)
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    if alg == "igs2_two":
+        assert _loo_close(g["loo"], lo), (g["loo"], lo)      # O(eps), P:792-797
+    else:
+        assert lo / 100 <= g["loo"] <= 10 * lo or g["loo"] <= 1e-12, (g["loo"], lo)
+    assert g["reductions"] == _reductions_one_cycle(alg, k)
+    np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-13)
+
+
+def test_reduction_counts_one_sync(P):
+    """The paper's sync count: one reduction per Arnoldi iteration for IGS(1) and
+    Alg. 3, two for Alg. 2, j+2 for MGS."""
+    import torch
+    prob = W.config("c3", N=32)
+    s = P.Solver(prob.A)
+    b = torch.from_numpy(prob.b).cuda()
+    for alg in ("igs1", "igs2", "igs2_two", "mgs"):
+        g = s.solve(b, k=30, algorithm=alg)
+        assert g["iters"] == 30 and g["reductions"] == _reductions_one_cycle(alg, 30), (alg, g["reductions"])
+    s.close()
+
+
+@pytest.mark.parametrize("alg", ["igs2_two", "mgs"])
+def test_next_algorithms_restarted(P, alg):
+    import torch
+    prob = W.config("c4", N=16)
+    s = P.Solver(prob.A)
+    g = s.solve(torch.from_numpy(prob.b).cuda(), k=3000, restart=100, tol=1e-12, algorithm=alg)
+    s.close()
+    o = oracle.gmres(prob.A, prob.b, 3000, restart=100, tol=1e-12, variant=ALG_ORACLE[alg], dot_block=4096)
+    assert g["term"] == o["term"] == "converged" and abs(g["iters"] - o["iters"]) <= 2
+    assert g["true_relres"] <= 1e-12
