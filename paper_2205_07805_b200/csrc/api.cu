@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <utility>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -66,6 +68,8 @@ struct igs_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // small-step tail (H, Givens, status), overlapped with the update
+    cudaStream_t gstream = nullptr;  // private stream for CUDA-graph capture/replay
+    cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
     cudaEvent_t ev_crit = nullptr, ev_tail = nullptr;
     int rank = 0, nranks = 1;
     ncclComm_t comm = nullptr;
@@ -124,6 +128,15 @@ struct igs_ctx {
     long long* d_flags = nullptr;  // per-CTA progress words of the fused kernel
     int epoch = 0;
     int64_t n_fused = 0;
+    // CUDA graphs of whole restart cycles (small problems, single GPU, timing off)
+    bool graphs_enabled = true;
+    bool capturing = false;
+    struct CycleGraph {
+        cudaGraphExec_t exec;
+        int64_t reductions, allreduces, halos;  // counters one replay accounts for
+    };
+    std::map<std::pair<int, int>, CycleGraph> graphs;  // (m, alg) -> executable cycle
+    int64_t n_graph_launches = 0;
 };
 
 // ------------------------------------------------------------------------------ misc
@@ -133,7 +146,7 @@ static inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * 
 
 static igs_status timer_begin(igs_ctx* c, int* idx, cudaStream_t st) {
     *idx = -1;
-    if (!c->timing) return IGS_OK;
+    if (!c->timing || c->capturing) return IGS_OK;
     const size_t need = 2 * (c->recs.size() + 1);
     while (c->events.size() < need) {
         cudaEvent_t e;
@@ -317,6 +330,10 @@ static void free_ctx(igs_ctx* c) {
     if (c->ev_crit) cudaEventDestroy(c->ev_crit);
     if (c->ev_tail) cudaEventDestroy(c->ev_tail);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->gstream) cudaStreamDestroy(c->gstream);
+    if (c->ev_g0) cudaEventDestroy(c->ev_g0);
+    if (c->ev_g1) cudaEventDestroy(c->ev_g1);
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -454,6 +471,7 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         ctx->fused_grid = fused_grid(ctx->num_sms);
         if (ctx->fused_grid > ctx->bdot_grid) ctx->bdot_grid = ctx->fused_grid;
         if (const char* e = std::getenv("IGS_FUSED")) ctx->fused_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_GRAPHS")) ctx->graphs_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_FUSED_L2_MB")) ctx->fused_budget = std::atof(e) * 1e6;
     }
     cudaError_t e;
@@ -491,6 +509,7 @@ static size_t small_doubles(int m, int k) {
            + (m + 1) * dld  // dots
            + 4 * (m + 2)    // alpha, beta, y, gam
            + (m + 3)        // dots2
+           + (size_t)(m + 1) * (m + 2) + (m + 2)  // r1h, cbd
            + SC_COUNT + (k + 2);
 }
 
@@ -528,6 +547,8 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
             }
             ctx->d_V = static_cast<double*>(ctx->bound_ws);
         }
+        for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
+        ctx->graphs.clear();
         // zero once: padding rows of every column must stay 0 (kernels read them as 0)
         CUDA_TRY(cudaMemsetAsync(ctx->d_V, 0, vbytes, ctx->stream));
         cudaFree(ctx->d_small);
@@ -558,6 +579,8 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.y = take(mm + 2);
         d.gam = take(mm + 2);
         d.dots2 = take(mm + 3);
+        d.r1h = take((size_t)(mm + 1) * (mm + 2));
+        d.cbd = take(mm + 2);
         d.scal = take(SC_COUNT);
         d.res_hist = take(kk + 2);
         d.istate = ctx->d_int;
@@ -690,9 +713,9 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
             TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
         }
-        // tail(p-1) (status, H column p-2, hp) must finish before this iteration's small step;
-        // it overlaps update(p-1), SpMV(p) and the block dot(p)
-        if (p > 1) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
+        // (no wait on tail(p-1): the critical step reads nothing the tail writes; a stop the
+        //  tail decides is seen one iteration later at worst, and the tails stay ordered on
+        //  the side stream; the cycle end joins the side stream)
         TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_CRIT, gs, p, m, t0, st));
         // tail of the small step on the side stream, overlapped with the fused update
         CUDA_TRY(cudaEventRecord(ctx->ev_crit, st));
@@ -740,7 +763,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         ctx->n_iter++;
         // checkpoint: copy the status word; decide on the PREVIOUS checkpoint's value so the
         // GPU always has one chunk queued and every rank stops at the same iteration
-        if (p % poll_every == 0 && p < m) {
+        if (!ctx->capturing && p % poll_every == 0 && p < m) {
             if (!ev[0]) {
                 CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
                 CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
@@ -756,7 +779,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         }
     }
     CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    if (!ctx->capturing) CUDA_TRY(cudaStreamSynchronize(st));
     if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
     return IGS_OK;
 }
@@ -790,7 +813,7 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0) {
               launch_update(n, 0, ctx->d_V, ctx->ldv, ctx->d_z, nullptr, nullptr, nullptr,
                             d.scal + SC_GAMMA, Vcol(ctx, j + 1), nullptr, ist, j + 1, st));
         ctx->n_iter++;
-        if ((j + 1) % poll_every == 0 && j + 1 < m) {
+        if (!ctx->capturing && (j + 1) % poll_every == 0 && j + 1 < m) {
             if (!ev[0]) {
                 CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
                 CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
@@ -805,8 +828,65 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0) {
             ev_slot ^= 1;
         }
     }
-    CUDA_TRY(cudaStreamSynchronize(st));
+    if (!ctx->capturing) CUDA_TRY(cudaStreamSynchronize(st));
     if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
+    return IGS_OK;
+}
+
+// Run one cycle: for small single-GPU problems replay a captured CUDA graph of the whole
+// cycle (p is baked into every node; the first iteration index t0 lives in device memory),
+// otherwise enqueue it directly with status polling.
+static igs_status launch_cycle(igs_ctx* ctx, int m, int alg, int t0) {
+    cudaStream_t st = ctx->stream;
+    ctx->h_pinned[40] = (double)t0;
+    CUDA_TRY(cudaMemcpyAsync(ctx->dev_state.scal + SC_T0, ctx->h_pinned + 40, sizeof(double),
+                             cudaMemcpyHostToDevice, st));
+    const bool use_graph = ctx->graphs_enabled && !ctx->timing && ctx->nranks == 1 &&
+                           ctx->n_local <= ((int64_t)1 << 21) && !ctx->fused_enabled &&
+                           alg != IGS_ALG_MGS && m <= 512;  // MGS: O(m^2) nodes
+    if (!use_graph) return run_cycle(ctx, m, alg, t0);
+    // capture and replay on a private stream (the caller's may be the legacy default stream,
+    // which cannot be captured); joined to the caller's stream with events
+    if (!ctx->gstream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_g0, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_g1, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(ctx->ev_g0, st));
+    CUDA_TRY(cudaStreamWaitEvent(ctx->gstream, ctx->ev_g0, 0));
+    const auto key = std::make_pair(m, alg);
+    auto itg = ctx->graphs.find(key);
+    if (itg == ctx->graphs.end()) {
+        cudaGraph_t g = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        ctx->stream = ctx->gstream;
+        const int64_t it0 = ctx->n_iter, r0 = ctx->n_reduce, a0 = ctx->n_allreduce, h0 = ctx->n_halo;
+        igs_status s1 = run_cycle(ctx, m, alg, t0);
+        ctx->stream = st;
+        ctx->capturing = false;
+        const int64_t dr = ctx->n_reduce - r0, da = ctx->n_allreduce - a0, dh = ctx->n_halo - h0;
+        ctx->n_iter = it0;
+        ctx->n_reduce = r0;
+        ctx->n_allreduce = a0;
+        ctx->n_halo = h0;
+        cudaError_t e = cudaStreamEndCapture(ctx->gstream, &g);
+        if (s1 != IGS_OK) { if (g) cudaGraphDestroy(g); return s1; }
+        CUDA_TRY(e);
+        cudaGraphExec_t ex = nullptr;
+        e = cudaGraphInstantiate(&ex, g, 0);
+        cudaGraphDestroy(g);
+        CUDA_TRY(e);
+        itg = ctx->graphs.emplace(key, igs_ctx::CycleGraph{ex, dr, da, dh}).first;
+    }
+    CUDA_TRY(cudaGraphLaunch(itg->second.exec, ctx->gstream));
+    ctx->n_reduce += itg->second.reductions;
+    ctx->n_allreduce += itg->second.allreduces;
+    ctx->n_halo += itg->second.halos;
+    CUDA_TRY(cudaEventRecord(ctx->ev_g1, ctx->gstream));
+    CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_g1, 0));
+    ctx->n_graph_launches++;
+    ctx->n_iter += m;
     return IGS_OK;
 }
 
@@ -911,7 +991,7 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         if (total >= k) { res->term = IGS_TERM_MAXITER; break; }
         if (rn == 0.0) { res->term = IGS_TERM_CONVERGED; break; }
         const int m = std::min(m1, k - total);
-        TRY(run_cycle(ctx, m, gs_iters, total));
+        TRY(launch_cycle(ctx, m, gs_iters, total));
         int istate[ST_COUNT];
         TRY(fetch(ctx, nullptr, 0, nullptr, d.istate, ST_COUNT, istate));
         const int status = istate[ST_STATUS], p = istate[ST_PDONE];
@@ -961,6 +1041,8 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
     if (res->res_hist) std::memcpy(res->res_hist, hres.data(), sizeof(double) * (total + 1));
+    if (res->H && res->h_cols < m1)  // columns past the last completed one are unspecified on
+        std::fill(res->H + (size_t)(m1 + 1) * res->h_cols, res->H + (size_t)(m1 + 1) * m1, 0.0);
     res->allreduces = ctx->n_allreduce - ar0;
     res->reductions = ctx->n_reduce - red0;
     TRY(timer_flush(ctx));

@@ -19,7 +19,7 @@ enum : int {
     ST_COUNT = 8
 };
 // scal slots (device doubles)
-enum : int { SC_GAMMA = 0, SC_RHO = 1, SC_NB = 2, SC_TOL = 3, SC_ONE = 4, SC_COUNT = 8 };
+enum : int { SC_GAMMA = 0, SC_RHO = 1, SC_NB = 2, SC_TOL = 3, SC_ONE = 4, SC_T0 = 5, SC_COUNT = 8 };
 
 constexpr double kEps = 2.220446049250313e-16;
 constexpr double kBreakdownC = 64.0;  // reading R12
@@ -42,6 +42,9 @@ struct Dev {
     double* y;      // [m+1] least-squares solution
     double* gam;    // [m+2] gamma of iteration p (written by crit, read by tail)
     double* dots2;  // [m+3] second reduction of Alg. 2 (two-reduce): V_{p+1}^T u
+    double* r1h;    // [(m+1) x (m+2)] r1 of iteration p (row p): the tail of iteration p reads it
+                    // while the critical step of p+1 already rewrites beta
+    double* cbd;    // [m+2] 1 if the critical step of iteration p saw a breakdown
     double* scal;   // [SC_COUNT]
     int* istate;    // [ST_COUNT]
     double* res_hist;  // [kmax+1]

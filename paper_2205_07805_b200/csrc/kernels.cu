@@ -764,8 +764,9 @@ __device__ double givens_column(const Dev& d, int j, double* col, double* scs, d
 }
 
 __global__ void __launch_bounds__(SS_THREADS)
-    small_kernel(Dev d, int stage, int gs, int p, int m, int t0) {
+    small_kernel(Dev d, int stage, int gs, int p, int m, int t0_unused) {
     extern __shared__ double sm[];
+    const int t0 = (int)d.scal[SC_T0];  // first global iteration of this cycle (graph-invariant)
     __shared__ double red[40];
     const int M = d.m;
     double* s_a = sm;               // [M+1]  r2 (Alg. 3) / a (Alg. 2)
@@ -915,6 +916,7 @@ __global__ void __launch_bounds__(SS_THREADS)
         if (!isfinite(gamma)) bd = true;
         if (tid == 0) {
             d.gam[p] = gamma;
+            d.cbd[p] = bd ? 1.0 : 0.0;
             d.scal[SC_GAMMA] = gamma;
             ist[ST_CRITBD] = bd ? p : -1;
             ist[ST_MODE] = bd ? 0 : (drain ? 1 : 3);
@@ -937,6 +939,9 @@ __global__ void __launch_bounds__(SS_THREADS)
             // Step 12 (Stephen's trick): r1 = [c ; d - L[p,:p] . c]
             const double acc = block_sum(part, red);
             if (tid == 0) d.beta[p] = dd - acc;
+            __syncthreads();
+            double* r1row = d.r1h + (int64_t)p * (M + 2);  // copy for the tail (hp, Step 15)
+            for (int i = tid; i <= p; i += blockDim.x) r1row[i] = d.beta[i];
         } else {
             // Alg. 2 Steps 8-10: c /= gamma ; c[p] /= gamma ; L[p, :p] = a / gamma
             for (int i = tid; i <= p; i += blockDim.x) {
@@ -959,7 +964,7 @@ __global__ void __launch_bounds__(SS_THREADS)
     // ---------------- SS_TAIL: Hessenberg column p-1, Givens, status, hp ------------------
     const double tol = d.scal[SC_TOL], nb = d.scal[SC_NB];
     const double gamma = d.gam[p];
-    bool bd = ist[ST_CRITBD] == p;
+    bool bd = d.cbd[p] != 0.0;
     double hn2 = 0.0;
     if (gs == 2) {
         // Step 5: r3 = (I + L_p)^{-1} r2 ; Step 14: H[:p, p-1] = hp + r3, H[p, p-1] = gamma (R3)
@@ -1005,7 +1010,7 @@ __global__ void __launch_bounds__(SS_THREADS)
             for (int c = 0; c < 8; c++) sacc += hv[c] * s_t[j + c];
         }
         for (; j < p; j++) sacc += d.H[i + (int64_t)j * d.ldh] * s_t[j];
-        d.HP[i + (int64_t)p * d.ldh] = d.beta[i] - sacc;
+        d.HP[i + (int64_t)p * d.ldh] = d.r1h[(int64_t)p * (M + 2) + i] - sacc;
     }
 }
 

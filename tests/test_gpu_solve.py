@@ -360,3 +360,21 @@ def test_next_algorithms_restarted(P, alg):
     o = oracle.gmres(prob.A, prob.b, 3000, restart=100, tol=1e-12, variant=ALG_ORACLE[alg], dot_block=4096)
     assert g["term"] == o["term"] == "converged" and abs(g["iters"] - o["iters"]) <= 2
     assert g["true_relres"] <= 1e-12
+
+
+def test_cuda_graph_cycle_matches_stream_path(P, monkeypatch):
+    """Small problems replay a captured CUDA graph of the whole cycle; it must give the same
+    bits as the stream-ordered path (same kernels, same order) and the same counters."""
+    import torch
+    prob = W.config("c3", N=48)
+    outs = {}
+    for graphs in ("1", "0"):
+        monkeypatch.setenv("IGS_GRAPHS", graphs)
+        s = P.Solver(prob.A)
+        b = torch.from_numpy(prob.b).cuda()
+        outs[graphs] = [s.solve(b, k=70, restart=30, tol=1e-10, gs_iters=gs) for gs in (2, 1)]
+        s.close()
+    for g, u in zip(outs["1"], outs["0"]):
+        assert g["iters"] == u["iters"] and g["reductions"] == u["reductions"]
+        assert g["H"].tobytes() == u["H"].tobytes()
+        assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
