@@ -934,7 +934,11 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         if (x0 && x0 != dx) CUDA_TRY(cudaMemcpyAsync(dx, x0, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         else if (!x0) CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(double) * n, st));
     }
-    const int64_t ar0 = ctx->n_allreduce, red0 = ctx->n_reduce;
+    const int64_t ar0 = ctx->n_allreduce;
+    unsigned red0 = 0;  // reductions executed on the device (block dots that ran to completion)
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned_int + 24, ctx->d_counter + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::memcpy(&red0, ctx->h_pinned_int + 24, sizeof(unsigned));
 
     // ||b|| (one reduction; also the non-finite check of b)
     double* dsc = d.scal;
@@ -1044,7 +1048,11 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     if (res->H && res->h_cols < m1)  // columns past the last completed one are unspecified on
         std::fill(res->H + (size_t)(m1 + 1) * res->h_cols, res->H + (size_t)(m1 + 1) * m1, 0.0);
     res->allreduces = ctx->n_allreduce - ar0;
-    res->reductions = ctx->n_reduce - red0;
+    {
+        unsigned red1 = 0;
+        CUDA_TRY(cudaMemcpy(&red1, ctx->d_counter + 1, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        res->reductions = (int64_t)(red1 - red0);
+    }
     TRY(timer_flush(ctx));
     return IGS_OK;
 }
@@ -1101,8 +1109,8 @@ extern "C" igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_
     double* part = nullptr;
     unsigned* counter = nullptr;
     CUDA_TRY(cudaMalloc(&part, sizeof(double) * (size_t)grid * 2 * (p + 1)));
-    CUDA_TRY(cudaMalloc(&counter, sizeof(unsigned)));
-    CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned), st));
+    CUDA_TRY(cudaMalloc(&counter, 2 * sizeof(unsigned)));
+    CUDA_TRY(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned), st));
     launch_block_dot(n, p, V, ld, u, z, out, part, counter, grid, nullptr, st);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(FU_CTA_THREADS, 1) fused_kernel(FusedArgs a) {
         for (int bb = 0; bb < (int)gridDim.x; bb++) sacc += __ldcg(a.part + (int64_t)bb * stride + i);
         a.out[i] = sacc;
     }
-    if (tid == 0) *a.counter = 0u;
+    if (tid == 0) { *a.counter = 0u; a.counter[1] += 1u; }  // [1]: reductions executed
 }
 
 static size_t fused_smem(int p) {

@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
         for (int bb = 0; bb < (int)gridDim.x; bb++) s += __ldcg(part + (int64_t)bb * stride + i);
         out[i] = s;  // layout: [V_p^T u (p), u.u, V_p^T z (p), u.z]
     }
-    if (threadIdx.x == 0) *counter = 0u;
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
 }
 
 // ------------------------------------------------------------------------------------
@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         for (int bb = 0; bb < (int)gridDim.x; bb++) sacc += __ldcg(part + (int64_t)bb * stride + i);
         out[i] = sacc;
     }
-    if (threadIdx.x == 0) *counter = 0u;
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
 }
 
 static size_t bdot_tma_smem(int p, int nv) {
