@@ -23,6 +23,7 @@
 #include <stdint.h>
 
 #include "igs_internal.cuh"
+#include "ptx_util.cuh"
 
 namespace igs {
 
@@ -115,29 +116,6 @@ __device__ __forceinline__ double2 ld2_rows(const double* col, int64_t r, int64_
     return v;
 }
 
-// mbarrier / bulk-copy helpers (same PTX as the block dot pipeline in kernels.cu)
-__device__ __forceinline__ uint32_t fsmem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
-__device__ __forceinline__ void fmbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(fsmem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fmbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fsmem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void fmbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fsmem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void fmbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(done) : "r"(fsmem_u32(bar)), "r"(parity) : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void fbulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                 ::"r"(fsmem_u32(dst)), "l"(src), "r"(bytes), "r"(fsmem_u32(bar)), "l"(pol) : "memory");
-}
-
 // CTA = 17 warps:
 //   warps 0-7   phase A consumers: update of the CTA's tiles c, c+G, ... from a shared-memory
 //               ring (warp w owns column 8g+w of column group g; cross-warp sum per row);
@@ -180,7 +158,7 @@ __global__ void __launch_bounds__(FU_CTA_THREADS, 1) fused_kernel(FusedArgs a) {
     for (int j = tid; j <= p; j += FU_CTA_THREADS) s_beta[j] = a.beta[j];
     if (tid == 0) {
         s_bdone = 0;
-        for (int i = 0; i < FU_STAGES; i++) { fmbar_init(full + i, 1); fmbar_init(empty + i, FU_WARPS); }
+        for (int i = 0; i < FU_STAGES; i++) { mbar_init(full + i, 1); mbar_init(empty + i, FU_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const double gamma = *a.gamma;
@@ -217,12 +195,12 @@ __global__ void __launch_bounds__(FU_CTA_THREADS, 1) fused_kernel(FusedArgs a) {
                 const uint32_t bytes = (uint32_t)(((rows + 1) & ~1LL) * sizeof(double));
                 for (int g = 0; g < ngroups; g++, it++) {
                     const int st = it % FU_STAGES;
-                    fmbar_wait(empty + st, ((it / FU_STAGES) & 1) ^ 1);
+                    mbar_wait(empty + st, ((it / FU_STAGES) & 1) ^ 1);
                     const int c0 = g * FU_WARPS;
                     const int nc = min(FU_WARPS, p - c0);
-                    fmbar_arrive_expect_tx(full + st, (uint32_t)nc * bytes);
+                    mbar_arrive_expect_tx(full + st, (uint32_t)nc * bytes);
                     for (int c = 0; c < nc; c++)
-                        fbulk_g2s(ring + (size_t)st * FU_STAGE_D + c * FU_T, V + (int64_t)(c0 + c) * ld + r0,
+                        bulk_g2s_hint(ring + (size_t)st * FU_STAGE_D + c * FU_T, V + (int64_t)(c0 + c) * ld + r0,
                                   bytes, full + st, keep);
                 }
             }
@@ -240,7 +218,7 @@ __global__ void __launch_bounds__(FU_CTA_THREADS, 1) fused_kernel(FusedArgs a) {
             for (int g = 0; g < ngroups; g++, it++) {
                 const int st = it % FU_STAGES;
                 const int c = g * FU_WARPS + warp;
-                fmbar_wait(full + st, (it / FU_STAGES) & 1);
+                mbar_wait(full + st, (it / FU_STAGES) & 1);
                 if (c < p) {
                     const double* cs = ring + (size_t)st * FU_STAGE_D + warp * FU_T;
                     const double al = s_alpha[c], be = s_beta[c];
@@ -253,7 +231,7 @@ __global__ void __launch_bounds__(FU_CTA_THREADS, 1) fused_kernel(FusedArgs a) {
                     }
                 }
                 __syncwarp();
-                if (lane == 0) fmbar_arrive(empty + st);
+                if (lane == 0) mbar_arrive(empty + st);
             }
             double* rw = s_red + warp * FU_T * 2;
 #pragma unroll

@@ -109,6 +109,16 @@ void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, 
 // small helpers
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
 
+// bdot_spmv.cu: SpMV + block dot of one iteration in one bulk-copy pipeline (int32 CSR whose
+// arrays are padded by >= 8 entries; every 256-row tile has <= bdot_spmv_nnz_cap() nonzeros)
+int bdot_spmv_tile_rows();
+int bdot_spmv_nnz_cap();
+bool bdot_spmv_fits(int p);
+cudaError_t launch_bdot_spmv(int64_t n, int p, const double* V, int64_t ld, const double* u, double* z,
+                             const int32_t* rowptr, const int32_t* col, const double* val,
+                             const double* ghost, double* out, double* part, unsigned* counter,
+                             int grid, const int* istate, cudaStream_t s);
+
 // fused.cu: update(p) + SpMV(p+1) + block dot(p+1) in one persistent wavefront kernel
 int fused_max_cols();
 int fused_tile_rows();

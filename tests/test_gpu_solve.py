@@ -378,3 +378,24 @@ def test_cuda_graph_cycle_matches_stream_path(P, monkeypatch):
         assert g["iters"] == u["iters"] and g["reductions"] == u["reductions"]
         assert g["H"].tobytes() == u["H"].tobytes()
         assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+def test_bdot_spmv_pipeline_parity(P, gs, monkeypatch):
+    """Opt-in kernel (IGS_BDOT_SPMV=1): SpMV folded into the bulk-copy block dot.  Same
+    iterations and H as the default path, and oracle parity."""
+    import torch
+    monkeypatch.setenv("IGS_BDOT_SPMV", "1")
+    prob = W.config("c4", N=24)
+    s = P.Solver(prob.A)
+    g = s.solve(torch.from_numpy(prob.b).cuda(), k=60, gs_iters=gs)
+    s.close()
+    monkeypatch.delenv("IGS_BDOT_SPMV")
+    s = P.Solver(prob.A)
+    u = s.solve(torch.from_numpy(prob.b).cuda(), k=60, gs_iters=gs)
+    s.close()
+    # one sweep amplifies rounding differences by ~eps*kappa(B_k) (reading R19)
+    assert oracle.column_normwise_diff(g["H"], u["H"], 60 if gs == 2 else 30) <= (1e-12 if gs == 2 else 1e-10)
+    o = oracle.gmres(prob.A, prob.b, 60, variant=VARIANT[gs], dot_block=4096)
+    d, _ = _compare_cols(g["H"], o["H"], o["res_hist"])
+    assert d <= 1e-10
