@@ -231,11 +231,7 @@ __global__ void __launch_bounds__(BS_THREADS, 1) bdot_spmv_kernel(BsArgs a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int i = threadIdx.x; i < stride; i += blockDim.x) {
-        double sacc = 0.0;
-        for (int bb = 0; bb < (int)gridDim.x; bb++) sacc += __ldcg(a.part + (int64_t)bb * stride + i);
-        a.out[i] = sacc;  // [V_p^T u (p), u.u, V_p^T z (p), u.z]
-    }
+    final_reduce(a.part, stride, (int)gridDim.x, a.out);  // [V_p^T u, u.u, V_p^T z, u.z]
     if (threadIdx.x == 0) { *a.counter = 0u; a.counter[1] += 1u; }  // [1]: reductions executed
 }
 

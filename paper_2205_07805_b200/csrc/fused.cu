@@ -384,11 +384,7 @@ __global__ void __launch_bounds__(FU_CTA_THREADS, 1) fused_kernel(FusedArgs a) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int i = tid; i < stride; i += FU_CTA_THREADS) {
-        double sacc = 0.0;
-        for (int bb = 0; bb < (int)gridDim.x; bb++) sacc += __ldcg(a.part + (int64_t)bb * stride + i);
-        a.out[i] = sacc;
-    }
+    final_reduce(a.part, stride, (int)gridDim.x, a.out);
     if (tid == 0) { *a.counter = 0u; a.counter[1] += 1u; }  // [1]: reductions executed
 }
 

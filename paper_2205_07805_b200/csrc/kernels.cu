@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "igs_internal.cuh"
 #include "ptx_util.cuh"
@@ -318,11 +319,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
     if (!s_last) return;
     __threadfence();
     // stage 2b: last CTA sums the partials in CTA order
-    for (int i = threadIdx.x; i < stride; i += BD_THREADS) {
-        double s = 0.0;
-        for (int bb = 0; bb < (int)gridDim.x; bb++) s += __ldcg(part + (int64_t)bb * stride + i);
-        out[i] = s;  // layout: [V_p^T u (p), u.u, V_p^T z (p), u.z]
-    }
+    final_reduce(part, stride, (int)gridDim.x, out);
     if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
 }
 
@@ -353,26 +350,49 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     if (!running(istate)) return;
     extern __shared__ __align__(128) double smem_bt[];
     double* ring = smem_bt;                                        // [STAGES][8][512]
-    double* acc = ring + BT_STAGES * BT_STAGE_DOUBLES;             // [NV*(p+1)]
+    double* uzslot = ring + BT_STAGES * BT_STAGE_DOUBLES;          // [2 tiles][u | z][512]
+    double* acc = uzslot + 4 * BT_ROWS;                            // [NV*(p+1)]
     const int ncols = p + 1;
     const int stride = NV * ncols;
     uint64_t* full = reinterpret_cast<uint64_t*>(acc + ((stride + 1) & ~1));
     uint64_t* empty = full + BT_STAGES;
+    uint64_t* uzfull = empty + BT_STAGES;
+    uint64_t* uzempty = uzfull + 2;
     __shared__ bool s_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] = 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < BT_STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, BT_CONS_WARPS); }
+        for (int s = 0; s < 2; s++) { mbar_init(uzfull + s, 1); mbar_init(uzempty + s, BT_CONS_WARPS); }
         mbar_fence_init();
     }
     __syncthreads();
     const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
     const int ngroups = (ncols + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
+    const int64_t nk = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (warp == BT_CONS_WARPS) {
         // ---------------- producer: one elected lane issues the bulk copies ----------------
         if (lane == 0) {
+            // u, z rows of tile k go to a double-buffered slot one tile ahead of tile k's V
+            // stream, so the consumers never wait on a global load at a tile boundary
+            auto issue_uz = [&](int64_t k) {
+                const int tb = (int)(k & 1);
+                const int64_t row0 = (blockIdx.x + k * gridDim.x) * BT_ROWS;
+                mbar_wait(uzempty + tb, (uint32_t)(((k >> 1) & 1) ^ 1));
+                if (row0 + BT_ROWS <= n) {  // full tiles only; a partial last tile is loaded directly
+                    const uint32_t b = BT_ROWS * sizeof(double);
+                    mbar_arrive_expect_tx(uzfull + tb, (NV == 2 ? 2 : 1) * b);
+                    bulk_g2s(uzslot + (2 * tb) * BT_ROWS, u + row0, b, uzfull + tb);
+                    if (NV == 2) bulk_g2s(uzslot + (2 * tb + 1) * BT_ROWS, z + row0, b, uzfull + tb);
+                } else {
+                    mbar_arrive(uzfull + tb);
+                }
+            };
+            if (nk > 0) issue_uz(0);
             uint32_t it = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for (int64_t k = 0; k < nk; k++) {
+                if (k + 1 < nk) issue_uz(k + 1);
+                const int64_t tile = blockIdx.x + k * gridDim.x;
                 const int64_t row0 = tile * BT_ROWS;
                 const int64_t rows = (n - row0 < BT_ROWS) ? n - row0 : BT_ROWS;
                 const uint32_t bytes = (uint32_t)(((rows + 1) & ~1LL) * sizeof(double));
@@ -392,17 +412,32 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     } else {
         // ---------------- consumers ----------------
         uint32_t it = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int64_t kt = 0; kt < nk; kt++) {
+            const int64_t tile = blockIdx.x + kt * gridDim.x;
             const int64_t row0 = tile * BT_ROWS;
             const bool full_tile = row0 + BT_ROWS <= n;
+            const int tb = (int)(kt & 1);
             double ur[BT_RPL], zr[BT_RPL];
+            mbar_wait(uzfull + tb, (uint32_t)((kt >> 1) & 1));
+            if (full_tile) {
+                const double* us = uzslot + (2 * tb) * BT_ROWS;
+                const double* zs = uzslot + (2 * tb + 1) * BT_ROWS;
 #pragma unroll
-            for (int k = 0; k < BT_RPL; k++) {
-                const int64_t r = row0 + lane + 32 * k;
-                const bool ok = full_tile || r < n;
-                ur[k] = ok ? __ldg(u + r) : 0.0;
-                zr[k] = (NV == 2 && ok) ? __ldg(z + r) : 0.0;
+                for (int k = 0; k < BT_RPL; k++) {
+                    ur[k] = us[lane + 32 * k];
+                    zr[k] = NV == 2 ? zs[lane + 32 * k] : 0.0;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < BT_RPL; k++) {
+                    const int64_t r = row0 + lane + 32 * k;
+                    const bool ok = r < n;
+                    ur[k] = ok ? __ldg(u + r) : 0.0;
+                    zr[k] = (NV == 2 && ok) ? __ldg(z + r) : 0.0;
+                }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(uzempty + tb);
             for (int g = 0; g < ngroups; g++, it++) {
                 const int s = it % BT_STAGES;
                 const int c = g * BT_CONS_WARPS + warp;
@@ -448,18 +483,113 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (int i = threadIdx.x; i < stride; i += blockDim.x) {
-        double sacc = 0.0;
-        for (int bb = 0; bb < (int)gridDim.x; bb++) sacc += __ldcg(part + (int64_t)bb * stride + i);
-        out[i] = sacc;
-    }
+    final_reduce(part, stride, (int)gridDim.x, out);  // [V_p^T u, u.u, V_p^T z, u.z]
     if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
+}
+
+// ------------------------------------------------------------------------------------
+// K2 (streaming variant): each warp owns a 512-row sub-range (8 chunks of 64 rows; a lane
+// owns rows 2l, 2l+1 of every chunk) and walks ALL column groups over it, accumulating 8
+// column partials per vector in registers across the 8 chunks; the butterfly reduction runs
+// once per (512 rows x 8 columns) instead of once per 128 rows.  Loads of the next chunk are
+// in flight while the current one is multiplied (16 x 16 B per lane).  u, z of the warp's
+// rows are read from shared memory.  Per-warp shared accumulators, fixed-order stage 2.
+// ------------------------------------------------------------------------------------
+constexpr int BS2_WARPS = 8;
+constexpr int BS2_CHUNKS = 8;                      // 64-row chunks per warp
+constexpr int BS2_ROWS_W = 64 * BS2_CHUNKS;        // 512 rows per warp
+constexpr int BS2_TILE = BS2_WARPS * BS2_ROWS_W;   // 4096 rows per CTA tile
+
+template <int NV>
+__global__ void __launch_bounds__(BS2_WARPS * 32, 2)
+    bdot_stream_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
+                       const double* __restrict__ u, const double* __restrict__ z,
+                       double* __restrict__ part, double* __restrict__ out, unsigned* counter,
+                       const int* istate) {
+    if (!running(istate)) return;
+    extern __shared__ __align__(16) double sst[];
+    const int ncols = p + 1;
+    const int stride = NV * ncols;
+    double* suz = sst;                                   // [NV][4096]
+    double* sacc = sst + NV * BS2_TILE;                  // [8 warps][stride]
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* acc = sacc + warp * stride;
+    for (int i = lane; i < stride; i += 32) acc[i] = 0.0;
+    const int64_t ntiles = (n + BS2_TILE - 1) / BS2_TILE;
+    const int ngroups = (ncols + 7) / 8;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t t0 = tile * BS2_TILE;
+        __syncthreads();
+        for (int i = threadIdx.x; i < BS2_TILE; i += blockDim.x) {
+            const int64_t r = t0 + i;
+            suz[i] = r < n ? __ldg(u + r) : 0.0;
+            if (NV == 2) suz[BS2_TILE + i] = r < n ? __ldg(z + r) : 0.0;
+        }
+        __syncthreads();
+        const int64_t w0 = t0 + warp * BS2_ROWS_W;     // this warp's 512 rows
+        const bool fullw = w0 + BS2_ROWS_W <= n;
+        const double* us = suz + warp * BS2_ROWS_W;
+        const double* zs = suz + BS2_TILE + warp * BS2_ROWS_W;
+        for (int g = 0; g < ngroups; g++) {
+            const double* cp[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int j = min(g * 8 + c, ncols - 1);
+                cp[c] = (j < p) ? V + (int64_t)j * ld : u;
+            }
+            double au[8], az[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) { au[c] = 0.0; az[c] = 0.0; }
+#pragma unroll 2
+            for (int ch = 0; ch < BS2_CHUNKS; ch++) {
+                const int64_t r = w0 + ch * 64 + 2 * lane;
+                double2 v[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) v[c] = fullw ? __ldg(reinterpret_cast<const double2*>(cp[c] + r)) : ld2_guard(cp[c], r, n);
+                const double2 uu = *reinterpret_cast<const double2*>(us + ch * 64 + 2 * lane);
+                double2 zz = make_double2(0.0, 0.0);
+                if (NV == 2) zz = *reinterpret_cast<const double2*>(zs + ch * 64 + 2 * lane);
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    au[c] = fma(v[c].y, uu.y, fma(v[c].x, uu.x, au[c]));
+                    if (NV == 2) az[c] = fma(v[c].y, zz.y, fma(v[c].x, zz.x, az[c]));
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 8; c++)
+                if (g * 8 + c >= ncols) { au[c] = 0.0; az[c] = 0.0; }
+            const double su = bfly8(au, lane);
+            double sz = 0.0;
+            if (NV == 2) sz = bfly8(az, lane);
+            const int j = g * 8 + (lane >> 2);
+            if ((lane & 3) == 0 && j < ncols) {
+                acc[j] += su;
+                if (NV == 2) acc[ncols + j] += sz;
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) {
+        double sacc2 = 0.0;
+#pragma unroll
+        for (int w = 0; w < BS2_WARPS; w++) sacc2 += sacc[w * stride + i];
+        part[(int64_t)blockIdx.x * stride + i] = sacc2;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    final_reduce(part, stride, (int)gridDim.x, out);  // [V_p^T u, u.u, V_p^T z, u.z]
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
 }
 
 static size_t bdot_tma_smem(int p, int nv) {
     const size_t stride = (size_t)nv * (p + 1);
-    return (size_t)BT_STAGES * BT_STAGE_DOUBLES * sizeof(double) + ((stride + 1) & ~(size_t)1) * sizeof(double) +
-           2 * BT_STAGES * sizeof(uint64_t);
+    return (size_t)(BT_STAGES * BT_STAGE_DOUBLES + 4 * BT_ROWS) * sizeof(double) +
+           ((stride + 1) & ~(size_t)1) * sizeof(double) + (2 * BT_STAGES + 4) * sizeof(uint64_t);
 }
 
 static size_t bdot_smem(int p, int nv) { return (size_t)BD_WARPS * nv * (p + 1) * sizeof(double); }
@@ -479,6 +609,29 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
     // sm_100a bulk-copy pipeline when V columns are 16-B aligned with an even ld and the
     // accumulators fit next to the 192 KB ring; the register kernel otherwise
     const size_t tsmem = bdot_tma_smem(p, nv);
+    static int variant = -1;  // IGS_BDOT=stream selects the register-streaming variant
+    if (variant < 0) {
+        const char* e = getenv("IGS_BDOT");
+        variant = (e && e[0] == 's') ? 1 : 0;
+    }
+    const size_t ssmem = (size_t)(nv * BS2_TILE + BS2_WARPS * nv * (p + 1)) * sizeof(double);
+    if (variant == 1 && p > 0 && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 && ((uintptr_t)u % 16) == 0 &&
+        ssmem <= 113 * 1024) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t ntiles = (n + BS2_TILE - 1) / BS2_TILE;
+        int g = (int)(ntiles < 2 * sms ? ntiles : 2 * sms);
+        if (g > grid) g = grid;
+        if (nv == 2) {
+            cudaFuncSetAttribute(bdot_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+            bdot_stream_kernel<2><<<g, BS2_WARPS * 32, ssmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+        } else {
+            cudaFuncSetAttribute(bdot_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+            bdot_stream_kernel<1><<<g, BS2_WARPS * 32, ssmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+        }
+        return;
+    }
     if (p > 0 && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 && tsmem <= 227 * 1024 && n >= BT_ROWS) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
