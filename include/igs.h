@@ -131,8 +131,12 @@ typedef struct {
     int basis_cols;        /* out: normalised columns of the final basis (LOO is over these)  */
     int64_t allreduces;    /* out: NCCL allreduces issued by this solve (0 when nranks == 1)  */
     int64_t reductions;    /* out: global reductions (device block dots, each followed by one
-                              allreduce when nranks > 1) issued by this solve -- the paper's
+                              allreduce when nranks > 1) executed by this solve -- the paper's
                               synchronization count                            */
+    double* lnorm_hist;    /* [k+1] host or NULL: ||L||_F of the current cycle's strictly lower
+                              Gram factor after iteration t (the paper's loss-of-orthogonality
+                              predictor, dep^2(I+L) = ||L||_F^2); lnorm_hist[0]=0;
+                              entries restart at each cycle; NaN for MGS (no L)               */
 } igs_result;
 
 /* Solve A x = b by restarted IGS-GMRES.

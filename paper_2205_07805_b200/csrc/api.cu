@@ -529,7 +529,7 @@ static size_t small_doubles(int m, int k) {
            + 4 * (m + 2)    // alpha, beta, y, gam
            + (m + 3)        // dots2
            + (size_t)(m + 1) * (m + 2) + (m + 2)  // r1h, cbd
-           + SC_COUNT + (k + 2);
+           + SC_COUNT + 2 * (k + 2);  // res_hist, lnorm
 }
 
 extern "C" size_t igs_workspace_bytes(const igs_ctx* ctx, int max_restart) {
@@ -602,6 +602,7 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.cbd = take(mm + 2);
         d.scal = take(SC_COUNT);
         d.res_hist = take(kk + 2);
+        d.lnorm = take(kk + 2);
         d.istate = ctx->d_int;
         ctx->m_cap = mm;
         ctx->k_cap = kk;
@@ -1057,6 +1058,9 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     res->basis_cols = last_basis;
     res->true_relres = rn / nb;
     if (total > 0) CUDA_TRY(cudaMemcpyAsync(hres.data() + 1, d.res_hist + 1, sizeof(double) * total, cudaMemcpyDeviceToHost, st));
+    std::vector<double> hl(k + 1, std::nan(""));
+    if (res->lnorm_hist && total > 0 && gs_iters != IGS_ALG_MGS)
+        CUDA_TRY(cudaMemcpyAsync(hl.data(), d.lnorm, sizeof(double) * (total + 1), cudaMemcpyDeviceToHost, st));
     // LOO of the final basis, diagnostic
     if (res->want_loo && last_basis > 0) {
         const int c = last_basis;
@@ -1080,6 +1084,10 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     CUDA_TRY(cudaStreamSynchronize(st));
     CUDA_TRY(cudaGetLastError());
     if (res->res_hist) std::memcpy(res->res_hist, hres.data(), sizeof(double) * (total + 1));
+    if (res->lnorm_hist) {
+        std::memcpy(res->lnorm_hist, hl.data(), sizeof(double) * (total + 1));
+        if (total == 0 || gs_iters == IGS_ALG_MGS) res->lnorm_hist[0] = std::nan("");
+    }
     if (res->H && res->h_cols < m1)  // columns past the last completed one are unspecified on
         std::fill(res->H + (size_t)(m1 + 1) * res->h_cols, res->H + (size_t)(m1 + 1) * m1, 0.0);
     res->allreduces = ctx->n_allreduce - ar0;

@@ -19,7 +19,7 @@ enum : int {
     ST_COUNT = 8
 };
 // scal slots (device doubles)
-enum : int { SC_GAMMA = 0, SC_RHO = 1, SC_NB = 2, SC_TOL = 3, SC_ONE = 4, SC_T0 = 5, SC_COUNT = 8 };
+enum : int { SC_GAMMA = 0, SC_RHO = 1, SC_NB = 2, SC_TOL = 3, SC_ONE = 4, SC_T0 = 5, SC_LCUM = 6, SC_COUNT = 8 };
 
 constexpr double kEps = 2.220446049250313e-16;
 constexpr double kBreakdownC = 64.0;  // reading R12
@@ -48,6 +48,7 @@ struct Dev {
     double* scal;   // [SC_COUNT]
     int* istate;    // [ST_COUNT]
     double* res_hist;  // [kmax+1]
+    double* lnorm;     // [kmax+1] ||L||_F of the current cycle after iteration t
 };
 
 // ---- launchers (kernels.cu) -----------------------------------------------------------

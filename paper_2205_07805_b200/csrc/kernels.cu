@@ -918,6 +918,8 @@ __global__ void __launch_bounds__(SS_THREADS)
             ist[ST_MODE] = 1;
             ist[ST_MODE_IT] = 0;
             ist[ST_CRITBD] = -1;
+            d.scal[SC_LCUM] = 0.0;
+            if (t0 == 0) d.lnorm[0] = 0.0;
         }
         return;
     }
@@ -1018,14 +1020,16 @@ __global__ void __launch_bounds__(SS_THREADS)
         // ---------------- critical path of iteration p (feeds the fused update) ----------
         for (int i = tid; i < p; i += blockDim.x) s_a[i] = dv[i];
         if (!drain) for (int i = tid; i <= p; i += blockDim.x) s_c[i] = dv[p + 1 + i];
-        double gamma;
+        double gamma, lrow2 = 0.0;
         bool bd;
         if (gs == 2) {
             // Step 6: lagged norm gamma = sqrt(||u||^2 - ||r2||^2)
             double part = 0.0;
             for (int i = tid; i < p; i += blockDim.x) part += s_a[i] * s_a[i];
-            const double t = s - block_sum(part, red);
+            const double nr2 = block_sum(part, red);
+            const double t = s - nr2;
             gamma = t > 0.0 ? sqrt(t) : 0.0;
+            lrow2 = nr2;
             bd = !(t > kBreakdownC * kEps * s);  // S:274 / reading R12 cancellation guard
             for (int i = tid; i < p; i += blockDim.x) d.alpha[i] = s_a[i];  // Step 10 uses r2
         } else {
@@ -1038,8 +1042,17 @@ __global__ void __launch_bounds__(SS_THREADS)
             }
             const double hn2 = block_sum(h2, red);
             bd = !(gamma > kBreakdownC * kEps * sqrt(hn2 + gamma * gamma));  // reading R12
+            double pa = 0.0;
+            for (int i = tid; i < p; i += blockDim.x) pa += s_a[i] * s_a[i];
+            lrow2 = block_sum(pa, red);
         }
         if (!isfinite(gamma)) bd = true;
+        if (tid == 0) {  // ||L||_F of this cycle: row p of L is (r2 or a) / gamma
+            double cum = d.scal[SC_LCUM];
+            if (!drain && !bd) cum += lrow2 / (gamma * gamma);
+            d.scal[SC_LCUM] = cum;
+            d.lnorm[t0 + p] = sqrt(cum);
+        }
         if (tid == 0) {
             d.gam[p] = gamma;
             d.cbd[p] = bd ? 1.0 : 0.0;

@@ -41,7 +41,7 @@ class igs_result(ctypes.Structure):
                 ("want_loo", ctypes.c_int), ("loo_frob", ctypes.c_double), ("iters", ctypes.c_int),
                 ("cycles", ctypes.c_int), ("term", ctypes.c_int), ("true_relres", ctypes.c_double),
                 ("h_cols", ctypes.c_int), ("basis_cols", ctypes.c_int), ("allreduces", ctypes.c_int64),
-                ("reductions", ctypes.c_int64)]
+                ("reductions", ctypes.c_int64), ("lnorm_hist", ctypes.c_void_p)]
 
 
 _lib = None
@@ -272,7 +272,9 @@ class Solver:
         m1 = restart if 0 < restart < k else k
         H = np.zeros((m1 + 1) * m1) if want_H else None
         rh = np.full(k + 1, np.nan)
+        lh = np.full(k + 1, np.nan)
         res = igs_result()
+        res.lnorm_hist = lh.ctypes.data
         res.x = _ptr(x_out)
         res.H = _ptr(H)
         res.res_hist = rh.ctypes.data
@@ -286,7 +288,7 @@ class Solver:
         out = dict(x=x_out, iters=res.iters, cycles=res.cycles, term=TERM[res.term],
                    true_relres=res.true_relres, loo=res.loo_frob, h_cols=res.h_cols,
                    basis_cols=res.basis_cols, allreduces=res.allreduces, reductions=res.reductions,
-                   res_hist=rh[:res.iters + 1], m=m1)
+                   res_hist=rh[:res.iters + 1], lnorm_hist=lh[:res.iters + 1], m=m1)
         if want_H:
             out["H"] = H.reshape(m1, m1 + 1).T
         return out
