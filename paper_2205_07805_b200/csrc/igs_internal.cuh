@@ -1,6 +1,7 @@
 // igs_internal.cuh -- device-side state and kernel launchers of libigs (sm_100a).
 // Nothing here is shared with oracle/ (the CPU reference); see DESIGN.md.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -51,6 +52,12 @@ struct Dev {
     double* lnorm;     // [kmax+1] ||L||_F of the current cycle after iteration t
 };
 
+// 2D TMA descriptors of a column-major n x ncols FP64 block with leading dimension ld
+// (api.cu builds them with cuTensorMapEncodeTiled through cudaGetDriverEntryPoint).
+// box8: (box_rows x 8 columns); box1: (box_rows x 1 column).
+bool make_tensor_map(CUtensorMap* tm, const double* base, int64_t n, int64_t ncols, int64_t ld,
+                     int box_rows, int box_cols);
+
 // ---- launchers (kernels.cu) -----------------------------------------------------------
 struct SpmvArgs {
     int64_t nrows;
@@ -70,7 +77,7 @@ void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b,
 int bdot_grid_size(int64_t n, int num_sms);
 void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                       const double* z, double* out, double* part, unsigned* counter, int grid,
-                      const int* istate, cudaStream_t s);
+                      const int* istate, cudaStream_t s, const CUtensorMap* tmV = nullptr);
 
 // Fused update (see igs.h igs_op_update).  gamma read from *gamma_dev.
 // istate/it: when istate != NULL the mode bits istate[ST_MODE] (valid iff
@@ -123,6 +130,7 @@ cudaError_t launch_bdot_spmv(int64_t n, int p, const double* V, int64_t ld, cons
 // fused.cu: update(p) + SpMV(p+1) + block dot(p+1) in one persistent wavefront kernel
 int fused_max_cols();
 int fused_tile_rows();
+int fused_nnz_cap();
 int fused_grid(int num_sms);
 cudaError_t launch_fused(int64_t n, int p, int m, const double* V, int64_t ld, double* z,
                          const double* alpha, const double* beta, const double* gamma_dev,

@@ -488,6 +488,162 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
 }
 
 // ------------------------------------------------------------------------------------
+// K2 (TMA tensor variant, the default): same structure as bdot_tma_kernel, but V is
+// streamed with 2D tensor copies -- one cp.async.bulk.tensor instruction per 8-column x
+// 256-row box (16 KB) -- because a single producer thread issuing 1D bulk copies tops out at
+// a few copies per microsecond (1-4 KB copies measured at 1.7-7 TB/s).  Rows past n and
+// columns past the map come back zero-filled.  12-stage ring (192 KB) per SM.
+// ------------------------------------------------------------------------------------
+constexpr int TM_ROWS = 256;
+constexpr int TM_RPL = TM_ROWS / 32;
+constexpr int TM_STAGES = 12;
+constexpr int TM_STAGE_D = BT_CONS_WARPS * TM_ROWS;  // 8 columns x 256 rows = 16 KB
+
+template <int NV>
+__global__ void __launch_bounds__(BT_THREADS, 1)
+    bdot_tmap_kernel(const __grid_constant__ CUtensorMap tmV, int64_t n, int p,
+                     const double* __restrict__ u, const double* __restrict__ z,
+                     double* __restrict__ part, double* __restrict__ out, unsigned* counter,
+                     const int* istate) {
+    if (!running(istate)) return;
+    extern __shared__ __align__(128) double smem_tm[];
+    double* ring = smem_tm;                                        // [STAGES][8][256]
+    double* uzslot = ring + TM_STAGES * TM_STAGE_D;                // [2 tiles][u | z][256]
+    double* acc = uzslot + 4 * TM_ROWS;                            // [NV*(p+1)]
+    const int ncols = p + 1;
+    const int stride = NV * ncols;
+    uint64_t* full = reinterpret_cast<uint64_t*>(acc + ((stride + 1) & ~1));
+    uint64_t* empty = full + TM_STAGES;
+    uint64_t* uzfull = empty + TM_STAGES;
+    uint64_t* uzempty = uzfull + 2;
+    __shared__ bool s_last;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TM_STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, BT_CONS_WARPS); }
+        for (int s = 0; s < 2; s++) { mbar_init(uzfull + s, 1); mbar_init(uzempty + s, BT_CONS_WARPS); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t ntiles = (n + TM_ROWS - 1) / TM_ROWS;
+    const int ngroups = (ncols + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
+    const int nstream = (p + BT_CONS_WARPS - 1) / BT_CONS_WARPS;  // groups holding V columns
+    const int64_t nk = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (warp == BT_CONS_WARPS) {
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            auto issue_uz = [&](int64_t k) {
+                const int tb = (int)(k & 1);
+                const int64_t row0 = (blockIdx.x + k * gridDim.x) * TM_ROWS;
+                mbar_wait(uzempty + tb, (uint32_t)(((k >> 1) & 1) ^ 1));
+                if (row0 + TM_ROWS <= n) {
+                    const uint32_t b = TM_ROWS * sizeof(double);
+                    mbar_arrive_expect_tx(uzfull + tb, (NV == 2 ? 2 : 1) * b);
+                    bulk_g2s(uzslot + (2 * tb) * TM_ROWS, u + row0, b, uzfull + tb);
+                    if (NV == 2) bulk_g2s(uzslot + (2 * tb + 1) * TM_ROWS, z + row0, b, uzfull + tb);
+                } else {
+                    mbar_arrive(uzfull + tb);
+                }
+            };
+            if (nk > 0) issue_uz(0);
+            uint32_t it = 0;
+            for (int64_t k = 0; k < nk; k++) {
+                if (k + 1 < nk) issue_uz(k + 1);
+                const int row0 = (int)((blockIdx.x + k * gridDim.x) * TM_ROWS);
+                for (int g = 0; g < nstream; g++, it++) {
+                    const int st = it % TM_STAGES;
+                    mbar_wait(empty + st, ((it / TM_STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(full + st, TM_STAGE_D * sizeof(double));
+                    tma_load_2d(ring + (size_t)st * TM_STAGE_D, &tmV, row0, g * BT_CONS_WARPS, full + st, pol);
+                }
+            }
+        }
+    } else {
+        uint32_t it = 0;
+        for (int64_t kt = 0; kt < nk; kt++) {
+            const int64_t row0 = (blockIdx.x + kt * gridDim.x) * TM_ROWS;
+            const bool full_tile = row0 + TM_ROWS <= n;
+            const int tb = (int)(kt & 1);
+            double ur[TM_RPL], zr[TM_RPL];
+            mbar_wait(uzfull + tb, (uint32_t)((kt >> 1) & 1));
+            if (full_tile) {
+                const double* us = uzslot + (2 * tb) * TM_ROWS;
+                const double* zs = uzslot + (2 * tb + 1) * TM_ROWS;
+#pragma unroll
+                for (int k = 0; k < TM_RPL; k++) {
+                    ur[k] = us[lane + 32 * k];
+                    zr[k] = NV == 2 ? zs[lane + 32 * k] : 0.0;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < TM_RPL; k++) {
+                    const int64_t r = row0 + lane + 32 * k;
+                    const bool ok = r < n;
+                    ur[k] = ok ? __ldg(u + r) : 0.0;
+                    zr[k] = (NV == 2 && ok) ? __ldg(z + r) : 0.0;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(uzempty + tb);
+            for (int g = 0; g < ngroups; g++) {
+                const int c = g * BT_CONS_WARPS + warp;
+                const bool streamed = g < nstream;
+                const int st = it % TM_STAGES;
+                if (streamed) mbar_wait(full + st, (it / TM_STAGES) & 1);
+                if (c < ncols) {
+                    double su = 0.0, sz = 0.0;
+                    if (c < p) {
+                        const double* col = ring + (size_t)st * TM_STAGE_D + warp * TM_ROWS;
+#pragma unroll
+                        for (int k = 0; k < TM_RPL; k++) {
+                            const double v = col[lane + 32 * k];   // rows >= n are zero-filled
+                            su = fma(v, ur[k], su);
+                            if (NV == 2) sz = fma(v, zr[k], sz);
+                        }
+                    } else {  // column p is u itself
+#pragma unroll
+                        for (int k = 0; k < TM_RPL; k++) {
+                            su = fma(ur[k], ur[k], su);
+                            if (NV == 2) sz = fma(ur[k], zr[k], sz);
+                        }
+                    }
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        su += __shfl_xor_sync(FULL_MASK, su, off);
+                        if (NV == 2) sz += __shfl_xor_sync(FULL_MASK, sz, off);
+                    }
+                    if (lane == 0) {
+                        acc[c] += su;
+                        if (NV == 2) acc[ncols + c] += sz;
+                    }
+                }
+                if (streamed) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + st);
+                    it++;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) part[(int64_t)blockIdx.x * stride + i] = acc[i];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    final_reduce(part, stride, (int)gridDim.x, out);  // [V_p^T u, u.u, V_p^T z, u.z]
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
+}
+
+static size_t bdot_tmap_smem(int p, int nv) {
+    const size_t stride = (size_t)nv * (p + 1);
+    return (size_t)(TM_STAGES * TM_STAGE_D + 4 * TM_ROWS) * sizeof(double) +
+           ((stride + 1) & ~(size_t)1) * sizeof(double) + (2 * TM_STAGES + 4) * sizeof(uint64_t);
+}
+
+// ------------------------------------------------------------------------------------
 // K2 (streaming variant): each warp owns a 512-row sub-range (8 chunks of 64 rows; a lane
 // owns rows 2l, 2l+1 of every chunk) and walks ALL column groups over it, accumulating 8
 // column partials per vector in registers across the 8 chunks; the butterfly reduction runs
@@ -604,8 +760,28 @@ int bdot_grid_size(int64_t n, int num_sms) {
 
 void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                       const double* z, double* out, double* part, unsigned* counter, int grid,
-                      const int* istate, cudaStream_t s) {
+                      const int* istate, cudaStream_t s, const CUtensorMap* tmV) {
     const int nv = z ? 2 : 1;
+    // default: 2D TMA tensor copies of V (tmV: box 256 rows x 8 columns over V's columns)
+    const size_t msmem = bdot_tmap_smem(p, nv);
+    if (tmV && p > 0 && msmem <= 227 * 1024 && ((uintptr_t)u % 16) == 0 && (!z || ((uintptr_t)z % 16) == 0) &&
+        n >= TM_ROWS) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t ntiles = (n + TM_ROWS - 1) / TM_ROWS;
+        const int tg = (int)(ntiles < sms ? ntiles : sms);
+        if (tg <= grid) {
+            if (nv == 2) {
+                cudaFuncSetAttribute(bdot_tmap_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+                bdot_tmap_kernel<2><<<tg, BT_THREADS, msmem, s>>>(*tmV, n, p, u, z, part, out, counter, istate);
+            } else {
+                cudaFuncSetAttribute(bdot_tmap_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+                bdot_tmap_kernel<1><<<tg, BT_THREADS, msmem, s>>>(*tmV, n, p, u, z, part, out, counter, istate);
+            }
+            return;
+        }
+    }
     // sm_100a bulk-copy pipeline when V columns are 16-B aligned with an even ld and the
     // accumulators fit next to the 192 KB ring; the register kernel otherwise
     const size_t tsmem = bdot_tma_smem(p, nv);

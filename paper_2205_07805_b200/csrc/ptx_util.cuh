@@ -2,6 +2,7 @@
 // mbarrier (init / arrive / expect_tx / try_wait.parity), cp.async.bulk global->shared with
 // mbarrier completion, L2 cache-policy creation.  (Not shared with oracle/.)
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -40,6 +41,17 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
                                               uint64_t pol) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+}
+// 2D TMA tensor copy global -> shared: box at (c0 = row, c1 = column) of the tensor map,
+// completion counted on the mbarrier; out-of-bounds rows are zero-filled by the hardware
+// (SASS: UTMALDG).  tm must live in kernel-parameter space (__grid_constant__).
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar,
+                                            uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
 }
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
     uint64_t pol;

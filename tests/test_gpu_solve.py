@@ -420,3 +420,27 @@ def test_lnorm_history_vs_oracle(P, gs):
     # projection), so like the LOO (reading R19) the bar is "within 10x"; the FMA / tree
     # reductions of the GPU give the smaller values (measured 0.25-0.45x for one sweep)
     assert np.all(got[5:] <= 10 * ref[5:] + 1e-15) and np.all(got[5:] >= ref[5:] / 10 - 1e-15)
+
+
+def test_tensor_map_block_dot_parity(P, monkeypatch):
+    """Opt-in 2D-TMA block dot (IGS_TMAP=1): same H as the default bulk-copy kernel."""
+    import torch
+    prob = W.config("c4", N=24)
+    outs = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("IGS_TMAP", v)
+        s = P.Solver(prob.A)
+        outs.append(s.solve(torch.from_numpy(prob.b).cuda(), k=60, gs_iters=2))
+        s.close()
+    assert oracle.column_normwise_diff(outs[0]["H"], outs[1]["H"], 60) <= 1e-12
+    rng = np.random.default_rng(0)
+    n, p = 5000, 37
+    V = torch.from_numpy(rng.standard_normal((p + 1) * n)).cuda()
+    z = torch.from_numpy(rng.standard_normal(n)).cuda()
+    o1 = torch.empty(2 * (p + 1), dtype=torch.float64, device="cuda")
+    o0 = torch.empty_like(o1)
+    monkeypatch.setenv("IGS_TMAP", "1")
+    P.igs_op_block_dot(n, p, V, n, V[p * n:], z, o1)
+    monkeypatch.setenv("IGS_TMAP", "0")
+    P.igs_op_block_dot(n, p, V, n, V[p * n:], z, o0)
+    assert np.allclose(o1.cpu().numpy(), o0.cpu().numpy(), rtol=1e-13, atol=1e-12)
