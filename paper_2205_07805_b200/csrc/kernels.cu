@@ -77,77 +77,104 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t nrows, const PT* __re
 // shared memory, then thread t sums row t's products left to right -- the same rounding
 // sequence as a sequential CSR row loop (product, then add), with none of the per-row
 // lane waste of vector CSR at ~7 nnz/row.
-constexpr int SPS_ROWS = 256;
-constexpr int SPS_K = 8;                     // staged nonzeros per thread (fast path)
-constexpr int SPS_CAP = SPS_ROWS * SPS_K;    // 2048 products = 16 KB of shared memory
+constexpr int SPS_THREADS = 256;
+constexpr int SPS_ROWS = 256;                // rows per CTA for R = 1 (R rows per thread)
+constexpr int SPS_K = 8;                     // staged nonzeros per thread per row of R
+constexpr int SPS_CAP = SPS_ROWS * SPS_K;    // 2048 products = 16 KB of shared memory (R = 1)
 
-template <typename IT, typename PT, bool GHOST, bool RESID>
-__global__ void __launch_bounds__(SPS_ROWS)
+template <int R, typename IT, typename PT, bool GHOST, bool RESID>
+__global__ void __launch_bounds__(SPS_THREADS)
     spmv_stream_kernel(int64_t nrows, const PT* __restrict__ rowptr, const IT* __restrict__ col,
                        const double* __restrict__ val, const double* __restrict__ x,
                        const double* __restrict__ ghost, int64_t nloc, double* __restrict__ y,
                        const double* __restrict__ b, const int* istate) {
     if (!running(istate)) return;
-    __shared__ double prod[SPS_CAP];
-    const int64_t r0 = (int64_t)blockIdx.x * SPS_ROWS;
-    const int64_t r = r0 + threadIdx.x;
-    const int64_t rl = (r0 + SPS_ROWS < nrows) ? r0 + SPS_ROWS : nrows;
+    constexpr int ROWS = SPS_ROWS * R, K = SPS_K * R, CAP = ROWS * SPS_K;
+    __shared__ double prod[CAP];
+    const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+    const int64_t rl = (r0 + ROWS < nrows) ? r0 + ROWS : nrows;
     const int64_t q0 = (int64_t)__ldg(rowptr + r0), q1 = (int64_t)__ldg(rowptr + rl);
-    const int cnt = (int)(q1 - q0 < (int64_t)SPS_CAP + 1 ? q1 - q0 : (int64_t)SPS_CAP + 1);
-    int a = 0, e = 0;
-    if (r < nrows) { a = (int)((int64_t)__ldg(rowptr + r) - q0); e = (int)((int64_t)__ldg(rowptr + r + 1) - q0); }
-    if (cnt <= SPS_CAP) {
-        // all column and value loads first, then all gathers: 3 x 8 independent loads per thread
-        int64_t cc[SPS_K];
-        double vv[SPS_K], xv[SPS_K];
+    const int cnt = (int)(q1 - q0 < (int64_t)CAP + 1 ? q1 - q0 : (int64_t)CAP + 1);
+    int ra[R], re[R];
 #pragma unroll
-        for (int k = 0; k < SPS_K; k++) {
-            const int i = threadIdx.x + k * SPS_ROWS;
+    for (int j = 0; j < R; j++) {
+        const int64_t r = r0 + threadIdx.x + j * SPS_THREADS;
+        ra[j] = re[j] = 0;
+        if (r < nrows) { ra[j] = (int)((int64_t)__ldg(rowptr + r) - q0); re[j] = (int)((int64_t)__ldg(rowptr + r + 1) - q0); }
+    }
+    if (cnt <= CAP) {
+        // all column and value loads first, then all gathers: 3 x K independent loads per thread
+        int64_t cc[K];
+        double vv[K], xv[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int i = threadIdx.x + k * SPS_THREADS;
             cc[k] = i < cnt ? (int64_t)__ldg(col + q0 + i) : 0;
             vv[k] = i < cnt ? __ldg(val + q0 + i) : 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < SPS_K; k++) {
-            const int i = threadIdx.x + k * SPS_ROWS;
+        for (int k = 0; k < K; k++) {
+            const int i = threadIdx.x + k * SPS_THREADS;
             if (GHOST && cc[k] >= nloc) xv[k] = i < cnt ? __ldg(ghost + (cc[k] - nloc)) : 0.0;
             else xv[k] = i < cnt ? __ldg(x + cc[k]) : 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < SPS_K; k++) {
-            const int i = threadIdx.x + k * SPS_ROWS;
+        for (int k = 0; k < K; k++) {
+            const int i = threadIdx.x + k * SPS_THREADS;
             if (i < cnt) prod[i] = __dmul_rn(vv[k], xv[k]);
         }
         __syncthreads();
-        if (r < nrows) {
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            const int64_t r = r0 + threadIdx.x + j * SPS_THREADS;
+            if (r < nrows) {
+                double sum = 0.0;
+                for (int q = ra[j]; q < re[j]; q++) sum = __dadd_rn(sum, prod[q]);
+                y[r] = RESID ? b[r] - sum : sum;
+            }
+        }
+    } else {  // more than SPS_K nonzeros per row on average here: row loop
+#pragma unroll
+        for (int j = 0; j < R; j++) {
+            const int64_t r = r0 + threadIdx.x + j * SPS_THREADS;
+            if (r >= nrows) continue;
             double sum = 0.0;
-            for (int q = a; q < e; q++) sum = __dadd_rn(sum, prod[q]);
+            for (int64_t q = q0 + ra[j]; q < q0 + re[j]; q++) {
+                const int64_t c = (int64_t)__ldg(col + q);
+                const double xq = (GHOST && c >= nloc) ? __ldg(ghost + (c - nloc)) : __ldg(x + c);
+                sum = __dadd_rn(sum, __dmul_rn(__ldg(val + q), xq));
+            }
             y[r] = RESID ? b[r] - sum : sum;
         }
-    } else if (r < nrows) {  // more than SPS_K nonzeros per row on average here: row loop
-        double sum = 0.0;
-        for (int64_t q = q0 + a; q < q0 + e; q++) {
-            const int64_t c = (int64_t)__ldg(col + q);
-            const double xq = (GHOST && c >= nloc) ? __ldg(ghost + (c - nloc)) : __ldg(x + c);
-            sum = __dadd_rn(sum, __dmul_rn(__ldg(val + q), xq));
-        }
-        y[r] = RESID ? b[r] - sum : sum;
+    }
+}
+
+template <int R, typename IT, typename PT>
+static void spmv_stream_r(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                          const int* istate, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((a.nrows + SPS_ROWS * R - 1) / (SPS_ROWS * R));
+    if (blocks == 0) return;
+    const PT* rp = static_cast<const PT*>(a.rowptr);
+    const IT* ci = static_cast<const IT*>(a.col);
+    if (a.ghost) {
+        if (resid) spmv_stream_kernel<R, IT, PT, true, true><<<blocks, SPS_THREADS, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+        else spmv_stream_kernel<R, IT, PT, true, false><<<blocks, SPS_THREADS, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+    } else {
+        if (resid) spmv_stream_kernel<R, IT, PT, false, true><<<blocks, SPS_THREADS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
+        else spmv_stream_kernel<R, IT, PT, false, false><<<blocks, SPS_THREADS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
     }
 }
 
 template <typename IT, typename PT>
 static void spmv_stream(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
                         const int* istate, cudaStream_t s) {
-    const unsigned blocks = (unsigned)((a.nrows + SPS_ROWS - 1) / SPS_ROWS);
-    if (blocks == 0) return;
-    const PT* rp = static_cast<const PT*>(a.rowptr);
-    const IT* ci = static_cast<const IT*>(a.col);
-    if (a.ghost) {
-        if (resid) spmv_stream_kernel<IT, PT, true, true><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
-        else spmv_stream_kernel<IT, PT, true, false><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
-    } else {
-        if (resid) spmv_stream_kernel<IT, PT, false, true><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
-        else spmv_stream_kernel<IT, PT, false, false><<<blocks, SPS_ROWS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
+    static int R = 0;  // rows per thread (IGS_SPMV_R = 1 | 2, default 1)
+    if (R == 0) {
+        const char* e = getenv("IGS_SPMV_R");
+        R = (e && atoi(e) == 2) ? 2 : 1;
     }
+    if (R == 2) spmv_stream_r<2, IT, PT>(a, x, y, b, resid, istate, s);
+    else spmv_stream_r<1, IT, PT>(a, x, y, b, resid, istate, s);
 }
 
 template <int LPR, typename IT, typename PT>

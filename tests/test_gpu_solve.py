@@ -444,3 +444,31 @@ def test_tensor_map_block_dot_parity(P, monkeypatch):
     monkeypatch.setenv("IGS_TMAP", "0")
     P.igs_op_block_dot(n, p, V, n, V[p * n:], z, o0)
     assert np.allclose(o1.cpu().numpy(), o0.cpu().numpy(), rtol=1e-13, atol=1e-12)
+
+
+def test_paper_matrices_on_gpu(P):
+    """The generator-defined Section-5 experiments through the CUDA path (tests/golden):
+    Walker alpha = 2000, Embree delta-bidiagonal, Helmert."""
+    import json, os
+    import torch
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+    # Walker n = 10: IGS(2) keeps O(eps) orthogonality on a kappa = 4e5, dep = 2000 matrix
+    A, b = W.walker(10, gold["walker"]["alpha"])
+    s = P.Solver(A)
+    g = s.solve(torch.from_numpy(b).cuda(), k=8, gs_iters=2, want_loo=True)
+    s.close()
+    o = oracle.gmres(A, b, 8, variant="igs2", want_V=True)
+    assert g["loo"] <= 1e-14 and oracle.column_normwise_diff(g["H"], o["H"], g["h_cols"]) <= 1e-10
+    # Embree n = 100, delta = 0.1: converges in <= 16 iterations (P:1332-1333)
+    A, b = W.embree(100, 0.1)
+    s = P.Solver(A)
+    g = s.solve(torch.from_numpy(b).cuda(), k=30, tol=1e-12, gs_iters=2, want_loo=True)
+    s.close()
+    assert g["term"] == "converged" and g["iters"] <= gold["embree"]["igs_iterations_to_converge"]
+    assert g["loo"] <= 1e-14
+    # Helmert(18): orthogonal A, O(eps) loss of orthogonality (P:1407-1411)
+    A, b = W.helmert(18)
+    s = P.Solver(A)
+    g = s.solve(torch.from_numpy(b).cuda(), k=16, gs_iters=2, want_loo=True)
+    s.close()
+    assert g["loo"] <= 1e-14
