@@ -55,6 +55,8 @@ def lib():
         _lib.oracle_hessenberg_lsq.restype = D
         _lib.oracle_hessenberg_lsq.argtypes = [I, P, I, D, P]
         _lib.oracle_num_threads.restype = I
+        _lib.oracle_igs_qr.restype = I
+        _lib.oracle_igs_qr.argtypes = [I64, I, P, I64, I, I64, P, I64, P, P, P]
         _lib.oracle_gemv.restype = None
         _lib.oracle_gemv.argtypes = [I64, I, P, I64, P, P]
     return _lib
@@ -177,6 +179,20 @@ def gmres(A, b, k: int, restart: int = 0, tol: float = 0.0, variant="igs2", x0=N
     if want_L:
         out["L"] = L.reshape(m1, m1).T
     return out
+
+
+def igs_qr(A, sweeps: int = 2, dot_block: int = 0):
+    """Algorithm 1: Q, R, L with A = QR.  sweeps=1: one Gauss-Seidel iteration."""
+    A = np.asfortranarray(A, dtype=np.float64)
+    n, m = A.shape
+    Q = np.zeros((n, m), order="F")
+    R = np.zeros((m, m), order="F")
+    L = np.zeros((m, m), order="F")
+    ledger = np.zeros(m, dtype=np.int64)
+    st = lib().oracle_igs_qr(n, m, _p(A), n, int(sweeps), int(dot_block), _p(Q), n, _p(R), _p(L), _p(ledger))
+    if st != 0:
+        raise ValueError(f"oracle_igs_qr status {st}")
+    return Q, R, L, ledger
 
 
 # ------------------------------------------------------------------ diagnostics

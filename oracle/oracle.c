@@ -396,6 +396,79 @@ static void cycle_alg3(ws_t* W, const double* r, int m) {
     }
 }
 
+/* ------------------------------------------- Algorithm 1: IGS Gram-Schmidt QR --- */
+/* Inverse compact WY two-reduce Gauss-Seidel Gram-Schmidt (Alg. 1), 0-based:
+ * A is n x m column-major (lda), Q n x m (ldq), R m x m upper (ldr = m), L m x m strictly
+ * lower (may be NULL), ledger[m] reductions per column (may be NULL).  sweeps = 2 is Alg. 1;
+ * sweeps = 1 drops Steps 11-13 (one Gauss-Seidel iteration).  The norm of the
+ * pending w_{k-1} (Step 5) is fused into the Step-4 reduction as in Alg. 2.
+ * Reading R22: Step 7 divides only the entry of r^(0) that belongs to the just-normalised
+ * q_{k-1} (w_{k-1}^T a_k / gamma); the printed r^(0)_{1:k-1,k} / gamma would scale the whole
+ * R column and break A = QR (the full-vector division belongs to the Arnoldi variant, where
+ * the new column is A w_{k-1} itself). */
+int oracle_igs_qr(int64_t n, int m, const double* A, int64_t lda, int sweeps, int64_t dot_block,
+                  double* Q, int64_t ldq, double* R, double* L_out, int64_t* ledger) {
+    if (n <= 0 || m <= 0 || m > n || !A || !Q || !R || (sweeps != 1 && sweeps != 2)) return OR_ERR_ARG;
+    g_block = dot_block;
+    double* L = (double*)calloc((size_t)m * m, sizeof(double));
+    double* r0 = (double*)calloc((size_t)m + 1, sizeof(double));
+    double* r1 = (double*)calloc((size_t)m + 1, sizeof(double));
+    double* r2 = (double*)calloc((size_t)m + 1, sizeof(double));
+    double* r3 = (double*)calloc((size_t)m + 1, sizeof(double));
+    double* t = (double*)malloc((size_t)n * sizeof(double));
+    if (!L || !r0 || !r1 || !r2 || !r3 || !t) return OR_ERR_OOM;
+    memset(R, 0, sizeof(double) * (size_t)m * m);
+#define QC(j) (Q + (int64_t)(j) * ldq)
+#define AC(j) (A + (int64_t)(j) * lda)
+#define RR(i, j) R[(i) + (int64_t)(j) * m]
+#define LL(i, j) L[(i) + (int64_t)(j) * m]
+    /* Step 1: w_1 = a_1, R_11 = ||w_1||, q_1 = w_1 / R_11 */
+    double r11 = sqrt(dot(n, AC(0), AC(0)));
+    if (ledger) ledger[0] = 1;
+    RR(0, 0) = r11;
+    for (int64_t i = 0; i < n; i++) QC(0)[i] = AC(0)[i] / r11;
+    if (m > 1) {
+        /* Step 2: R_12 = q_1^T a_2, w_2 = a_2 - R_12 q_1 (pending in Q's column 2) */
+        const double r12 = dot(n, QC(0), AC(1));
+        if (ledger) ledger[1] = 1;
+        RR(0, 1) = r12;
+        for (int64_t i = 0; i < n; i++) QC(1)[i] = AC(1)[i] - r12 * QC(0)[i];
+    }
+    for (int k = 2; k <= m; k++) {                  /* paper k = 3..m (+ the drain k = m) */
+        const int drain = (k == m);
+        double* w = QC(k - 1);                        /* w_{k-1}, pending */
+        /* Step 4 (+5): ONE reduction: L^T = Q_{k-2}^T w, ||w||^2, r0 = Q_{k-1}^T a_k */
+        for (int i = 0; i < k - 1; i++) r2[i] = dot(n, QC(i), w);
+        const double s = dot(n, w, w);
+        if (!drain) for (int i = 0; i < k; i++) r0[i] = dot(n, QC(i), AC(k));
+        const double gamma = sqrt(s);                 /* Step 5 */
+        RR(k - 1, k - 1) = gamma;                     /* gamma_{k-1} = R_{k-1,k-1} */
+        for (int64_t i = 0; i < n; i++) w[i] = w[i] / gamma;   /* Step 6 */
+        if (drain) break;
+        r0[k - 1] = r0[k - 1] / gamma;                /* Step 7 (reading R22) */
+        for (int i = 0; i < k - 1; i++) LL(k - 1, i) = r2[i] / gamma;   /* Step 8 */
+        oracle_forward_solve_unit(k, L, m, r0, r1);   /* Step 9 */
+        gemv_n(n, k, Q, ldq, r1, t);                  /* Step 10: u_k = a_k - Q_{k-1} r1 */
+        double* u = QC(k);
+        for (int64_t i = 0; i < n; i++) u[i] = AC(k)[i] - t[i];
+        if (sweeps == 2) {
+            for (int i = 0; i < k; i++) r2[i] = dot(n, QC(i), u);   /* Step 11 (2nd reduction) */
+            oracle_forward_solve_unit(k, L, m, r2, r3);           /* Step 12 */
+            gemv_n(n, k, Q, ldq, r3, t);                          /* Step 13 */
+            for (int64_t i = 0; i < n; i++) u[i] = u[i] - t[i];
+        }
+        for (int i = 0; i < k; i++) RR(i, k) = r1[i] + (sweeps == 2 ? r3[i] : 0.0);   /* Step 14 */
+        if (ledger) ledger[k] = sweeps;
+    }
+#undef QC
+#undef AC
+#undef RR
+#undef LL
+    if (L_out) memcpy(L_out, L, sizeof(double) * (size_t)m * m);
+    free(L); free(r0); free(r1); free(r2); free(r3); free(t);
+    return OR_OK;
+}
+
 /* ----------------------------------------------------------------- driver --- */
 /* SURVEY §8(c) "Driver".  Arrays: colind int64 (global columns), H_out (m1+1) x m1
  * column-major (first cycle, m1 = cycle capacity), res_hist [k+1], V_out n x (m1+1)

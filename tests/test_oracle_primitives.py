@@ -126,3 +126,59 @@ def test_block_dot_layout_matches_definition():
     M = np.column_stack([V, u]).T @ np.column_stack([u, z])    # [V, u]^T [u, z]
     ref = np.concatenate([M[:7, 0], [M[7, 0]], M[:7, 1], [M[7, 1]]])
     assert np.allclose(out, ref, rtol=1e-13, atol=1e-13)
+
+
+# ------------------------------------------------------------- Algorithm 1 (QR)
+def test_igs_qr_identity():
+    Q, R, L, _ = oracle.igs_qr(np.eye(12)[:, :7])
+    np.testing.assert_allclose(Q, np.eye(12)[:, :7], atol=1e-16)
+    np.testing.assert_allclose(R, np.eye(7), atol=1e-16)
+
+
+@pytest.mark.parametrize("sweeps", [1, 2])
+def test_igs_qr_vs_householder(sweeps):
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((50, 20))
+    Q, R, L, led = oracle.igs_qr(A, sweeps)
+    Qh, Rh = np.linalg.qr(A)                     # LAPACK Householder QR, signs normalised
+    Rh = np.sign(np.diag(Rh))[:, None] * Rh
+    assert np.abs(R - Rh).max() <= 1e-12 * np.abs(Rh).max()
+    assert np.allclose(np.triu(R), R)            # upper triangular, positive diagonal
+    assert np.all(np.diag(R) > 0)
+    assert np.linalg.norm(A - Q @ R) <= 1e-14 * np.linalg.norm(A)
+    assert np.linalg.norm(np.eye(20) - Q.T @ Q) <= 1e-14
+    assert list(led[:2]) == [1, 1] and np.all(led[2:] == sweeps)   # 'Global Synchronization' count
+
+
+def _graded(n=60, m=30, kappa=1e10, seed=5):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((n, m)))
+    Wm, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    return (U * np.logspace(0, -np.log10(kappa), m)) @ Wm.T
+
+
+def test_igs_qr_two_sweeps_eps_orthogonality_graded():
+    # with two Gauss-Seidel iterations the loss of orthogonality is O(eps) even for
+    # kappa(A) = 1e10; one iteration only O(eps) kappa(A)
+    A = _graded()
+    kappa = np.linalg.cond(A)
+    Q2, R2, _, _ = oracle.igs_qr(A, 2)
+    Q1, R1, _, _ = oracle.igs_qr(A, 1)
+    loo2 = np.linalg.norm(np.eye(30) - Q2.T @ Q2)
+    loo1 = np.linalg.norm(np.eye(30) - Q1.T @ Q1)
+    assert loo2 <= 1e-13
+    assert loo1 <= 10 * EPS * kappa and loo1 >= 1e3 * loo2
+    for Q, R in ((Q1, R1), (Q2, R2)):            # both are backward stable factorizations
+        assert np.linalg.norm(A - Q @ R) <= 1e-14 * np.linalg.norm(A)
+
+
+def test_igs_qr_step7_reading():
+    # reading R22: only the entry of r^(0) belonging to the lagged-normalised q_{k-1} is divided
+    # by gamma_{k-1}; dividing the whole column (the literal print) breaks A = QR
+    A = np.random.default_rng(6).standard_normal((40, 10))
+    Q, R, _, _ = oracle.igs_qr(A)
+    R_lit = R.copy()
+    for k in range(2, 10):
+        R_lit[:k - 1, k] /= R[k - 1, k - 1]
+    assert np.linalg.norm(A - Q @ R) <= 1e-14 * np.linalg.norm(A)
+    assert np.linalg.norm(A - Q @ R_lit) >= 1e-2 * np.linalg.norm(A)
