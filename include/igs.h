@@ -198,6 +198,17 @@ igs_status igs_op_update(int64_t n, int p, const double* V, int64_t ld, const do
                          const double* z, const double* alpha, const double* beta, double gamma,
                          double* v_out, double* u_next, void* cuda_stream);
 
+/* Algorithm 1 ("Inverse Compact WY Two-Reduce Gauss-Seidel Gram-Schmidt"):
+ * A = Q R for a tall-skinny A (n x m, m <= n) on the solver's kernels.  All pointers device:
+ * A (col-major, lda even >= n, 16-byte aligned, not modified), Q (out, n x m, ldq even >= n,
+ * 16-byte aligned), R (out, m x m upper triangular, col-major, ld = m, positive diagonal).
+ * sweeps = 2: two Gauss-Seidel iterations (two global reductions per column, O(eps) loss of
+ * orthogonality); sweeps = 1: one (O(eps) kappa(A)).  Step 7 reading
+ * R22.  *reductions (may be NULL) = block dots issued.  A (numerically) dependent
+ * column -> IGS_ERR_NONFINITE.  Synchronises cuda_stream before returning. */
+igs_status igs_qr(int64_t n, int m, const double* A, int64_t lda, double* Q, int64_t ldq, double* R,
+                  int sweeps, int64_t* reductions, void* cuda_stream);
+
 /* x = (I + L)^{-1} b by forward substitution; L strictly lower, col-major
  * order x order, ld = ldl (device); b, x device [order].  One CTA (the small-step solver). */
 igs_status igs_op_trisolve(int order, const double* L, int ldl, const double* b, double* x,

@@ -1210,6 +1210,93 @@ extern "C" igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_
     return IGS_OK;
 }
 
+// Algorithm 1: Q R = A with one or two Gauss-Seidel sweeps, on the solver's own
+// kernels (block dot, small step, fused update).  Reductions per column: 1 (+1 for sweeps=2).
+extern "C" igs_status igs_qr(int64_t n, int m, const double* A, int64_t lda, double* Q, int64_t ldq,
+                             double* R, int sweeps, int64_t* reductions, void* cuda_stream) {
+    ARG_CHECK(n >= 1 && m >= 1 && m <= n && A && Q && R && (sweeps == 1 || sweeps == 2), "igs_qr: bad argument");
+    ARG_CHECK(lda >= n && ldq >= n && lda % 2 == 0 && ldq % 2 == 0 && ((uintptr_t)A % 16) == 0 &&
+              ((uintptr_t)Q % 16) == 0, "igs_qr: A and Q need even leading dimensions >= n and 16-byte alignment");
+    TRY(have_device());
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = bdot_grid_size(n, sms);
+    const size_t nsd = (size_t)m * m + 2 * (m + 1) + (m + 1) + 2 * (m + 1) + 2 + (size_t)grid * 2 * (m + 1);
+    double* ws = nullptr;
+    unsigned* counter = nullptr;
+    CUDA_TRY(cudaMalloc(&ws, nsd * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&counter, 2 * sizeof(unsigned)));
+    struct Free { double* w; unsigned* c; ~Free() { cudaFree(w); cudaFree(c); } } guard{ws, counter};
+    CUDA_TRY(cudaMemsetAsync(ws, 0, nsd * sizeof(double), st));
+    CUDA_TRY(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned), st));
+    CUDA_TRY(cudaMemsetAsync(R, 0, sizeof(double) * (size_t)m * m, st));
+    QrDev q;
+    double* w = ws;
+    q.R = R;
+    q.L = w; w += (size_t)m * m;
+    q.dots = w; w += 2 * (m + 1);
+    q.dots2 = w; w += m + 1;
+    q.alpha = w; w += m + 1;
+    q.beta = w; w += m + 1;
+    q.scal = w; w += 2;
+    double* part = w;
+    auto col = [&](const double* base, int64_t ld, int j) { return base + (int64_t)j * ld; };
+    auto qcol = [&](int j) { return Q + (int64_t)j * ldq; };
+    int64_t nred = 0;
+    auto dot = [&](int p, const double* u, const double* z, double* out) {
+        launch_block_dot(n, p, Q, ldq, u, z, out, part, counter, grid, nullptr, st);
+        nred++;
+    };
+    // Step 1: R_11 = ||a_1||, q_1 = a_1 / R_11
+    dot(0, col(A, lda, 0), nullptr, q.dots);
+    launch_qr_small(q, QR_S0, 0, m, st);
+    launch_update(n, 0, Q, ldq, col(A, lda, 0), nullptr, nullptr, nullptr, q.scal, qcol(0), nullptr,
+                  nullptr, 0, st);
+    if (m > 1) {
+        // Step 2: R_12 = q_1^T a_2, w_2 = a_2 - R_12 q_1
+        dot(0, qcol(0), col(A, lda, 1), q.dots);
+        launch_qr_small(q, QR_S1, 1, m, st);
+        launch_update(n, 0, Q, ldq, qcol(0), col(A, lda, 1), nullptr, q.beta, q.scal + 1,
+                      qcol(0), qcol(1), nullptr, 0, st, q.scal + 1);
+    }
+    for (int k = 2; k <= m; k++) {
+        const bool drain = (k == m);
+        // Steps 4-5: ONE reduction [Q_{k-2}, w_{k-1}]^T [w_{k-1}, a_k]
+        dot(k - 1, qcol(k - 1), drain ? nullptr : col(A, lda, k), q.dots);
+        launch_qr_small(q, QR_CRIT, k, m, st);
+        if (drain) {  // Step 6 for the last column
+            launch_update(n, 0, Q, ldq, qcol(k - 1), nullptr, nullptr, nullptr, q.scal,
+                          qcol(k - 1), nullptr, nullptr, 0, st);
+            break;
+        }
+        // Steps 6, 10: q_{k-1} = w_{k-1} / gamma ; u_k = a_k - Q_{k-1} r1
+        launch_update(n, k - 1, Q, ldq, qcol(k - 1), col(A, lda, k), nullptr, q.beta, q.scal,
+                      qcol(k - 1), qcol(k), nullptr, 0, st, q.scal + 1);
+        if (sweeps == 2) {
+            // Steps 11-13: r2 = Q_{k-1}^T u_k (second reduction), r3 = (I+L)^{-1} r2, w_k = u_k - Q r3
+            dot(k, qcol(k), nullptr, q.dots2);
+            launch_qr_small(q, QR_CRIT2, k, m, st);
+            launch_update(n, k, Q, ldq, qcol(k), nullptr, q.alpha, nullptr, q.scal + 1, qcol(k),
+                          nullptr, nullptr, 0, st);
+        }
+    }
+    CUDA_TRY(cudaGetLastError());
+    std::vector<double> diag((size_t)m * m);
+    CUDA_TRY(cudaMemcpyAsync(diag.data(), R, sizeof(double) * (size_t)m * m, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (reductions) *reductions = nred;
+    for (int i = 0; i < m; i++) {
+        const double d = diag[i + (size_t)i * m];
+        if (!std::isfinite(d) || !(d > 0.0)) {
+            set_error("igs_qr: column " + std::to_string(i) + " is (numerically) dependent or non-finite");
+            return IGS_ERR_NONFINITE;
+        }
+    }
+    return IGS_OK;
+}
+
 extern "C" igs_status igs_op_spmv(igs_ctx* ctx, const double* x, double* y) {
     ARG_CHECK(ctx && ctx->ok && x && y, "igs_op_spmv: bad argument");
     ARG_CHECK(ctx->nranks == 1, "igs_op_spmv: single-rank contexts only");

@@ -85,7 +85,7 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
 void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
                    const double* z, const double* alpha, const double* beta,
                    const double* gamma_dev, double* v_out, double* u_next, const int* istate,
-                   int it, cudaStream_t s);
+                   int it, cudaStream_t s, const double* zdiv_dev = nullptr);
 
 // x += V[:, :p] y with p = istate[ST_PDONE]
 void launch_xupdate(int64_t n, const double* V, int64_t ld, const double* y, double* x,
@@ -100,6 +100,19 @@ enum SmallStage : int { SS_PRIME_NORM = 0, SS_PRIME_H = 1, SS_CRIT = 2, SS_TAIL 
 void launch_mgs_axpy(int64_t n, const double* v, double* z, const double* hsrc, double* Hdst,
                      const int* istate, cudaStream_t s);
 void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s);
+
+// Algorithm 1 (Gram-Schmidt QR) small steps; q.scal[0] = gamma, q.scal[1] = 1.
+struct QrDev {
+    double* R;      // m x m, col-major, ld = m
+    double* L;      // m x m strictly lower, ld = m
+    double* dots;   // [2 (m+1)]
+    double* dots2;  // [m+1]
+    double* alpha;  // [m+1]
+    double* beta;   // [m+1]
+    double* scal;   // [2]
+};
+enum QrStage : int { QR_S0 = 0, QR_S1 = 1, QR_CRIT = 2, QR_CRIT2 = 3 };
+void launch_qr_small(const QrDev& q, int stage, int k, int m, cudaStream_t s);
 
 // x = (I + L)^{-1} b (test entry point; same device routine as the small step).
 void launch_trisolve(int order, const double* L, int ldl, const double* b, double* x,

@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(UP_THREADS)
                   const double* u, const double* __restrict__ z,
                   const double* __restrict__ alpha, const double* __restrict__ beta,
                   const double* __restrict__ gamma_dev, double* v_out, double* u_next,
-                  const int* istate, int it, int default_mode) {
+                  const int* istate, int it, int default_mode, const double* __restrict__ zdiv_dev) {
     extern __shared__ double coef[];  // alpha[p] | beta[p+1]
     int mode = default_mode;
     if (istate) {
@@ -895,6 +895,7 @@ __global__ void __launch_bounds__(UP_THREADS)
         for (int j = threadIdx.x; j <= p; j += blockDim.x) sb[j] = beta[j];
     __syncthreads();
     const double gamma = *gamma_dev;
+    const double zdiv = zdiv_dev ? *zdiv_dev : gamma;  // z / gamma (Arnoldi) or z / 1 (QR)
     const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
     if (r >= n) return;
     const bool pair = (r + 1 < n);
@@ -929,8 +930,8 @@ __global__ void __launch_bounds__(UP_THREADS)
         const double2 zz = ld2_guard(z, r, n);
         const double bp = sb[p];
         double2 un;
-        un.x = zz.x / gamma - fma(v.x, bp, t2.x);
-        un.y = zz.y / gamma - fma(v.y, bp, t2.y);
+        un.x = zz.x / zdiv - fma(v.x, bp, t2.x);
+        un.y = zz.y / zdiv - fma(v.y, bp, t2.y);
         u_next[r] = un.x;
         if (pair) u_next[r + 1] = un.y;
     }
@@ -943,7 +944,7 @@ __global__ void __launch_bounds__(UP_THREADS)
 void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
                    const double* z, const double* alpha, const double* beta,
                    const double* gamma_dev, double* v_out, double* u_next, const int* istate,
-                   int it, cudaStream_t s) {
+                   int it, cudaStream_t s, const double* zdiv_dev) {
     const int64_t nthreads = (n + 1) / 2;
     const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
     if (blocks == 0) return;
@@ -951,10 +952,10 @@ void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* 
     const int dmode = 1 | (u_next ? 2 : 0);
     if (alpha) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        update_kernel<true><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode);
+        update_kernel<true><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
     } else {
         if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        update_kernel<false><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode);
+        update_kernel<false><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
     }
 }
 
@@ -1362,6 +1363,63 @@ void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStr
     const size_t smem = small_smem(d.m);
     if (smem > 48 * 1024) cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     small_kernel<<<1, SS_THREADS, smem, s>>>(d, stage, gs, p, m, t0);
+}
+
+// ------------------------------------------------------------------------------------
+// Algorithm 1 small steps, one CTA (igs_qr).  Workspace layout in QrDev.
+//   QR_S0     R_11 = ||a_1||                                  (Step 1)
+//   QR_S1     R_12 = q_1^T a_2                                (Step 2)
+//   QR_CRIT   column k >= 2: gamma_{k-1} = ||w_{k-1}|| = R_{k-1,k-1} (Step 5), L row (Step 8),
+//             r0 with only its last entry divided by gamma (Step 7, reading R22),
+//             r1 = (I + L)^{-1} r0 (Step 9), R[:k, k] = r1;  drain (k = m): gamma only
+//   QR_CRIT2  r3 = (I + L)^{-1} r2 (Step 12), R[:k, k] += r3 (Step 14), alpha = r3 (Step 13)
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(SS_THREADS) qr_small_kernel(QrDev q, int stage, int k, int m) {
+    extern __shared__ double qs[];
+    __shared__ double red[40];
+    const int tid = threadIdx.x;
+    double* R = q.R;
+    if (stage == QR_S0) {
+        if (tid == 0) { const double g = sqrt(q.dots[0]); R[0] = g; q.scal[0] = g; q.scal[1] = 1.0; }
+        return;
+    }
+    if (stage == QR_S1) {
+        if (tid == 0) { const double h = q.dots[1]; R[(int64_t)m] = h; q.beta[0] = h; }
+        return;
+    }
+    if (stage == QR_CRIT) {
+        const int p = k - 1;                   // normalised columns before w_{k-1}
+        const double* dv = q.dots;             // [Q_p^T w (p), w.w, Q_p^T a_k (p), w.a_k]
+        const double gamma = sqrt(dv[p]);
+        if (tid == 0) { R[p + (int64_t)p * m] = gamma; q.scal[0] = gamma; }
+        if (k == m) return;                    // drain: normalise the last column only
+        for (int i = tid; i < p; i += blockDim.x) {
+            q.L[p + (int64_t)i * m] = dv[i] / gamma;    // Step 8
+            qs[i] = dv[p + 1 + i];                       // Step 7: r0 entries of q_0..q_{p-1}
+        }
+        if (tid == 0) qs[p] = dv[2 * p + 1] / gamma;     // ... and of the new q_p = w / gamma
+        trisolve_smem(k, q.L, m, qs);                    // Step 9 (order k = p + 1)
+        for (int i = tid; i < k; i += blockDim.x) {
+            q.beta[i] = qs[i];
+            R[i + (int64_t)k * m] = qs[i];               // Step 14 (first part)
+        }
+        return;
+    }
+    if (stage == QR_CRIT2) {
+        for (int i = tid; i < k; i += blockDim.x) qs[i] = q.dots2[i];
+        trisolve_smem(k, q.L, m, qs);                    // Step 12
+        for (int i = tid; i < k; i += blockDim.x) {
+            R[i + (int64_t)k * m] = R[i + (int64_t)k * m] + qs[i];   // Step 14: r1 + r3
+            q.alpha[i] = qs[i];                                      // Step 13 coefficients
+        }
+        return;
+    }
+}
+
+void launch_qr_small(const QrDev& q, int stage, int k, int m, cudaStream_t s) {
+    const size_t smem = (size_t)(m + 2) * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(qr_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    qr_small_kernel<<<1, SS_THREADS, smem, s>>>(q, stage, k, m);
 }
 
 __global__ void __launch_bounds__(SS_THREADS)

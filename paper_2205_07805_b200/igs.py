@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "OK", 1: "ERR_ARG", 2: "ERR_CUDA", 3: "ERR_NCCL", 4: "ERR_OOM
 EXPORTS = ["igs_create", "igs_nccl_unique_id", "igs_workspace_bytes", "igs_bind_workspace",
            "igs_solve", "igs_solve_alg", "igs_stats", "igs_set_timing", "igs_kernel_stats", "igs_destroy",
            "igs_last_error", "igs_op_block_dot", "igs_op_spmv", "igs_op_update",
-           "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap"]
+           "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap", "igs_qr"]
 
 
 class IgsError(RuntimeError):
@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
             "igs_op_spmv": [P, P, P],
             "igs_op_update": [I64, I, P, I64, P, P, P, P, D, P, P, P],
             "igs_op_trisolve": [I, P, I, P, P, P],
+            "igs_qr": [I64, I, P, I64, P, I64, P, I, P, P],
             "igs_plan_ghosts": [I64, I64, P, P, I, I, P, P, P, P],
             "igs_plan_remap": [I64, I64, P, P, I, I64, P, P],
         }
@@ -186,6 +187,14 @@ def igs_op_update(n, p, V, ld, u, z, alpha, beta, gamma, v_out, u_next, stream=N
     _check(lib().igs_op_update(int(n), int(p), _ptr(V), int(ld), _ptr(u), _ptr(z), _ptr(alpha),
                                _ptr(beta), float(gamma), _ptr(v_out), _ptr(u_next),
                                _stream_ptr(stream)), "igs_op_update")
+
+
+def igs_qr(n, m, A, lda, Q, ldq, R, sweeps=2, stream=None) -> int:
+    """Algorithm 1 QR on the device (device tensors); returns the number of reductions."""
+    red = ctypes.c_int64(0)
+    _check(lib().igs_qr(int(n), int(m), _ptr(A), int(lda), _ptr(Q), int(ldq), _ptr(R), int(sweeps),
+                        ctypes.byref(red), _stream_ptr(stream)), "igs_qr")
+    return red.value
 
 
 def igs_op_trisolve(order, L, ldl, b, x, stream=None):

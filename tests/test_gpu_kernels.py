@@ -148,3 +148,68 @@ def test_spmv_vs_oracle(torch_cuda, name):
     bound = 4 * EPS * np.diff(A.rowptr).clip(1) * oracle.spmv(absA, np.abs(x))
     assert np.all(np.abs(y.cpu().numpy() - ref) <= bound + 1e-300)
     s.close()
+
+
+# ------------------------------------------------------------- Algorithm 1 (QR)
+def _graded_qr(n, m, kappa, seed):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((n, m)))
+    Wm, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    return (U * np.logspace(0, -np.log10(kappa), m)) @ Wm.T
+
+
+def _gpu_qr(torch, A, sweeps, pad=6):
+    import paper_2205_07805_b200 as P
+    n, m = A.shape
+    ld = n + (n % 2) + pad
+    Ah = np.full((m, ld), np.nan)
+    Ah[:, :n] = A.T                                # column-major, NaN padding never read
+    Ad = _dev(torch, Ah.reshape(-1))
+    Qd = torch.full((m * ld,), float("nan"), dtype=torch.float64, device="cuda")
+    Rd = torch.full((m * m,), float("nan"), dtype=torch.float64, device="cuda")
+    red = P.igs_qr(n, m, Ad, ld, Qd, ld, Rd, sweeps)
+    Q = Qd.cpu().numpy().reshape(m, ld)[:, :n].T
+    R = Rd.cpu().numpy().reshape(m, m).T
+    assert np.array_equal(Ad.cpu().numpy().reshape(m, ld)[:, :n], A.T)   # A untouched
+    return Q, R, red
+
+
+@pytest.mark.parametrize("sweeps", [1, 2])
+@pytest.mark.parametrize("shape", [(7, 3), (5000, 40), (70001, 12), (3000, 1)])
+def test_igs_qr_vs_oracle(torch_cuda, sweeps, shape):
+    n, m = shape
+    A = np.random.default_rng(n + m).standard_normal((n, m))
+    Q, R, red = _gpu_qr(torch_cuda, A, sweeps)
+    Qo, Ro, _, led = oracle.igs_qr(A, sweeps)
+    # one (two) reductions per column, + the drain reduction that normalises the last column
+    assert red == int(led.sum()) + (m >= 2)
+    tol = 1e-12 * np.sqrt(n)
+    assert np.abs(R - Ro).max() <= tol * np.abs(Ro).max()
+    assert np.abs(Q - Qo).max() <= tol
+    assert np.array_equal(np.tril(R, -1), np.zeros((m, m)))
+    assert np.linalg.norm(A - Q @ R) <= 1e-14 * np.sqrt(n) * np.linalg.norm(A)
+    assert np.linalg.norm(np.eye(m) - Q.T @ Q) <= 1e-13
+
+
+def test_igs_qr_graded_kappa(torch_cuda):
+    # P:792-797 (two sweeps: O(eps)) and P:697-704 (one sweep: O(eps) kappa), on the device
+    A = _graded_qr(20000, 30, 1e10, 11)
+    kappa = np.linalg.cond(A)
+    Q2, R2, _ = _gpu_qr(torch_cuda, A, 2)
+    Q1, R1, _ = _gpu_qr(torch_cuda, A, 1)
+    loo2 = np.linalg.norm(np.eye(30) - Q2.T @ Q2)
+    loo1 = np.linalg.norm(np.eye(30) - Q1.T @ Q1)
+    assert loo2 <= 1e-13
+    assert loo1 <= 10 * EPS * kappa and loo1 >= 1e3 * loo2
+    Qo, Ro, _, _ = oracle.igs_qr(A, 2)
+    assert np.abs(R2 - Ro).max() <= 1e-11 * np.abs(Ro).max()
+    for Q, R in ((Q1, R1), (Q2, R2)):
+        assert np.linalg.norm(A - Q @ R) <= 1e-13 * np.linalg.norm(A)
+
+
+def test_igs_qr_dependent_column_fails_loudly(torch_cuda):
+    import paper_2205_07805_b200 as P
+    A = np.random.default_rng(3).standard_normal((1000, 4))
+    A[:, 2] = 0.0
+    with pytest.raises(P.IgsError):
+        _gpu_qr(torch_cuda, A, 2)
