@@ -80,7 +80,8 @@ typedef enum {
     IGS_K_UPDATE = 4,    /* fused GEMV + axpy + lagged normalisation         */
     IGS_K_HALO = 5,      /* ncclSend/ncclRecv of ghost entries (G > 1)       */
     IGS_K_CYCLE = 6,     /* cycle end: y, x += V y, r = b - A x, ||r||       */
-    IGS_K_COUNT = 7
+    IGS_K_PERSIST = 7,   /* persistent cycle kernel (small n, single GPU)   */
+    IGS_K_COUNT = 8
 } igs_kernel_kind;
 
 /* Create a solver for this rank's row block of A.

@@ -141,6 +141,12 @@ struct igs_ctx {
     };
     std::map<std::pair<int, int>, CycleGraph> graphs;  // (m, alg) -> executable cycle
     int64_t n_graph_launches = 0;
+    // persistent cycle kernel (small n, single GPU, Alg. 3 / Alg. 2 one sweep)
+    bool pc_enabled = true;   // IGS_PERSIST=0 disables
+    int64_t pc_max_n = 12288;  // crossover vs the graph-replayed per-kernel path
+    int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
+    int64_t n_pcycle = 0;
+    unsigned long long* d_pcprof = nullptr;  // IGS_PC_PROF=1 phase timestamps
 };
 
 // ------------------------------------------------------------------------------ misc
@@ -349,7 +355,7 @@ static void free_ctx(igs_ctx* c) {
     cudaFree(c->d_ghost); cudaFree(c->d_send); cudaFree(c->d_send_idx);
     if (c->owns_ws) { cudaFree(c->d_V); }
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
-    cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter);
+    cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter); cudaFree(c->d_pcprof);
     cudaFree(c->d_gram);
     cudaFree(c->d_flags);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -527,6 +533,9 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         if (ctx->fused_grid > ctx->bdot_grid) ctx->bdot_grid = ctx->fused_grid;
         if (const char* e = std::getenv("IGS_FUSED")) ctx->fused_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_GRAPHS")) ctx->graphs_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_PERSIST")) ctx->pc_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_PC_GRID")) ctx->pc_grid = std::atoi(e);
+        if (const char* e = std::getenv("IGS_PC_MAX_N")) ctx->pc_max_n = std::atoll(e);
         if (const char* e = std::getenv("IGS_FUSED_L2_MB")) ctx->fused_budget = std::atof(e) * 1e6;
     }
     cudaError_t e;
@@ -656,8 +665,8 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(long long) * (ctx->fused_grid + 1), ctx->stream));
     }
     if (!ctx->d_counter) {
-        CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 4));
-        CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned) * 4, ctx->stream));
+        CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 8));  // [4..7]: persistent-kernel flags
+        CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned) * 8, ctx->stream));
     }
     if (host_vec && !ctx->d_b) {
         CUDA_TRY(cudaMalloc(&ctx->d_b, sizeof(double) * ldv));
@@ -739,6 +748,11 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0);
 
 // alg: IGS_ALG_IGS1 (1), IGS_ALG_IGS2 (2, Alg. 3), IGS_ALG_IGS2_TWO (3, Alg. 2 literal),
 // IGS_ALG_MGS (4).  Algorithms 1 and 3 share the gs = 1 small-step stages.
+static bool use_pcycle(const igs_ctx* ctx, int alg) {
+    return ctx->pc_enabled && ctx->nranks == 1 && ctx->n_local <= ctx->pc_max_n && !ctx->fused_enabled &&
+           (alg == IGS_ALG_IGS1 || alg == IGS_ALG_IGS2) && ctx->dev_state.m <= 1024;
+}
+
 static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
     if (alg == IGS_ALG_MGS) return run_cycle_mgs(ctx, m, t0);
     const int gs = alg == IGS_ALG_IGS2 ? 2 : 1;
@@ -762,6 +776,49 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
           launch_update(n, 0, ctx->d_V, ctx->ldv, Vcol(ctx, 0), ctx->d_z, nullptr, d.beta,
                         d.scal + SC_GAMMA, Vcol(ctx, 0), Vcol(ctx, 1), ist, 0, st));
 
+    if (use_pcycle(ctx, alg)) {
+        // iterations 1..m in one cooperative launch; grid sized so every CTA has >= 64 KB of
+        // the iteration's bytes (CSR + V), at most one CTA per SM
+        const double iter_bytes = spmv_bytes(ctx) + 8.0 * n * (m + 1);
+        int grid = ctx->pc_grid > 0 ? ctx->pc_grid : (int)std::ceil(iter_bytes / 32768.0) + 1;
+        grid = std::max(1, std::min(grid, ctx->num_sms));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 4 * sizeof(unsigned), st));
+        if (std::getenv("IGS_PC_PROF") && !ctx->d_pcprof) {
+            CUDA_TRY(cudaMalloc(&ctx->d_pcprof, sizeof(unsigned long long) * 8 * (size_t)(ctx->dev_state.m + 2)));
+        }
+        if (ctx->d_pcprof)
+            CUDA_TRY(cudaMemsetAsync(ctx->d_pcprof, 0, sizeof(unsigned long long) * 8 * (size_t)(ctx->dev_state.m + 2), st));
+        const double by = (double)m * spmv_bytes(ctx) + 16.0 * n * 0.5 * m * (m + 1);
+        TIMED(IGS_K_PERSIST, by, {
+            cudaError_t e_ = launch_pcycle(d, ctx->A, ctx->d_V, ctx->ldv, ctx->d_z, n, m, gs,
+                                           ctx->d_counter + 4, ctx->d_counter, grid, st, ctx->d_pcprof);
+            CUDA_TRY(e_);
+        });
+        if (ctx->d_pcprof) {  // IGS_PC_PROF=1: mean phase durations of this cycle to stderr
+            std::vector<unsigned long long> pr((size_t)(m + 1) * 8);
+            CUDA_TRY(cudaMemcpyAsync(pr.data(), ctx->d_pcprof, pr.size() * 8, cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            double acc[8] = {0};
+            int cnt = 0;
+            for (int p = 2; p < m; p++) {
+                const unsigned long long* q = pr.data() + (size_t)p * 8;
+                const unsigned long long* qn = pr.data() + (size_t)(p + 1) * 8;
+                if (!q[0] || !qn[0]) continue;
+                acc[0] += q[1] - q[0]; acc[1] += q[2] - q[1]; acc[2] += q[3] - q[2]; acc[3] += q[4] - q[3];
+                acc[4] += q[5] - q[4]; acc[5] += qn[0] - q[5]; acc[6] += q[7] - q[6]; acc[7] += qn[0] - q[0];
+                cnt++;
+            }
+            if (cnt)
+                std::fprintf(stderr, "[pcycle grid=%d m=%d] us/iter: A+bar %.2f  B+bar %.2f  C %.2f  bar %.2f  D %.2f  bar %.2f  | tail %.2f | total %.2f\n",
+                             grid, m, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
+                             acc[4] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, acc[7] / cnt / 1e3);
+        }
+        ctx->n_pcycle++;
+        ctx->n_iter += m;
+        ctx->n_reduce += m;
+        if (!ctx->capturing) CUDA_TRY(cudaStreamSynchronize(st));
+        return IGS_OK;
+    }
     const int poll_every = 16;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int ev_slot = 0, ev_pending = -1;
@@ -921,7 +978,7 @@ static igs_status launch_cycle(igs_ctx* ctx, int m, int alg, int t0) {
     ctx->h_pinned[40] = (double)t0;
     CUDA_TRY(cudaMemcpyAsync(ctx->dev_state.scal + SC_T0, ctx->h_pinned + 40, sizeof(double),
                              cudaMemcpyHostToDevice, st));
-    const bool use_graph = ctx->graphs_enabled && !ctx->timing && ctx->nranks == 1 &&
+    const bool use_graph = ctx->graphs_enabled && !ctx->timing && ctx->nranks == 1 && !use_pcycle(ctx, alg) &&
                            ctx->n_local <= ((int64_t)1 << 21) && !ctx->fused_enabled &&
                            alg != IGS_ALG_MGS && m <= 512;  // MGS: O(m^2) nodes
     if (!use_graph) return run_cycle(ctx, m, alg, t0);

@@ -1034,7 +1034,7 @@ __device__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, 
             double lrow[32];
 #pragma unroll
             for (int j = 0; j < 32; j++)
-                lrow[j] = (mine && j < lane) ? L[(kb + lane) + (int64_t)(kb + j) * ldl] : 0.0;
+                lrow[j] = (mine && j < lane) ? __ldcg(L + (kb + lane) + (int64_t)(kb + j) * ldl) : 0.0;
 #pragma unroll
             for (int j = 0; j < 32; j++) {
                 const double xj = __shfl_sync(FULL_MASK, xi, j);
@@ -1046,7 +1046,7 @@ __device__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, 
         for (int i = kb + nb + threadIdx.x; i < order; i += blockDim.x) {
             double lv[32];
 #pragma unroll
-            for (int j = 0; j < 32; j++) lv[j] = j < nb ? L[i + (int64_t)(kb + j) * ldl] : 0.0;
+            for (int j = 0; j < 32; j++) lv[j] = j < nb ? __ldcg(L + i + (int64_t)(kb + j) * ldl) : 0.0;
             double sacc = x[i];
 #pragma unroll
             for (int j = 0; j < 32; j++)
@@ -1062,8 +1062,8 @@ __device__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, 
 __device__ double givens_column(const Dev& d, int j, double* col, double* scs, double* ssn,
                                 double* red) {
     const double* Hj = d.H + (int64_t)j * d.ldh;
-    for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) col[i] = Hj[i];
-    for (int i = threadIdx.x; i < j; i += blockDim.x) { scs[i] = d.cs[i]; ssn[i] = d.sn[i]; }
+    for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) col[i] = __ldcg(Hj + i);
+    for (int i = threadIdx.x; i < j; i += blockDim.x) { scs[i] = __ldcg(d.cs + i); ssn[i] = __ldcg(d.sn + i); }
     __syncthreads();
     if (threadIdx.x == 0) {
         double carry = col[0];
@@ -1080,7 +1080,7 @@ __device__ double givens_column(const Dev& d, int j, double* col, double* scs, d
         d.sn[j] = s;
         col[j] = dd;
         col[j + 1] = 0.0;
-        const double gj = d.g[j];
+        const double gj = __ldcg(d.g + j);
         d.g[j + 1] = -s * gj;
         d.g[j] = c * gj;
         red[33] = fabs(-s * gj);
@@ -1093,11 +1093,11 @@ __device__ double givens_column(const Dev& d, int j, double* col, double* scs, d
     return res;
 }
 
-__global__ void __launch_bounds__(SS_THREADS)
-    small_kernel(Dev d, int stage, int gs, int p, int m, int t0_unused) {
-    extern __shared__ double sm[];
-    const int t0 = (int)d.scal[SC_T0];  // first global iteration of this cycle (graph-invariant)
-    __shared__ double red[40];
+// The small step on the calling CTA (any blockDim that is a multiple of 32, <= 1024).  All
+// global loads bypass L1 (ld.global.cg): the persistent cycle kernel runs this on one CTA
+// while other CTAs of the same grid produce its inputs.  sm: small_smem(d.m) bytes, red: 40.
+__device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double* sm, double* red) {
+    const int t0 = (int)__ldcg(d.scal + SC_T0);  // first global iteration of this cycle (graph-invariant)
     const int M = d.m;
     double* s_a = sm;               // [M+1]  r2 (Alg. 3) / a (Alg. 2)
     double* s_c = s_a + (M + 1);    // [M+2]  c (and d)
@@ -1111,7 +1111,7 @@ __global__ void __launch_bounds__(SS_THREADS)
 
     if (stage == SS_PRIME_NORM) {  // rho = ||r||, v_0 = r / rho
         if (tid == 0) {
-            const double s = d.dots[0];
+            const double s = __ldcg(d.dots);
             const double rho = sqrt(s);
             d.g[0] = rho;
             d.scal[SC_RHO] = rho;
@@ -1129,8 +1129,8 @@ __global__ void __launch_bounds__(SS_THREADS)
     }
     if (stage == SS_PRIME_H) {  // H_11 = v_1^T A v_1, u = A v_1 - H_11 v_1 (reading R2)
         if (tid == 0) {
-            if (ist[ST_STATUS] != RUNNING) { ist[ST_MODE] = 0; return; }
-            const double h = d.dots[1];
+            if (*(volatile int*)(ist + ST_STATUS) != RUNNING) { ist[ST_MODE] = 0; return; }
+            const double h = __ldcg(d.dots + 1);
             if (gs == 1) d.H[0] = h;
             else d.HP[0] = h;
             d.beta[0] = h;
@@ -1143,14 +1143,14 @@ __global__ void __launch_bounds__(SS_THREADS)
         return;
     }
     if (stage == SS_LSQ) {  // y = R^{-1} g  (back substitution)
-        const int pp = ist[ST_PDONE];
-        for (int i = tid; i < pp; i += blockDim.x) s_x[i] = d.g[i];
+        const int pp = *(volatile int*)(ist + ST_PDONE);
+        for (int i = tid; i < pp; i += blockDim.x) s_x[i] = __ldcg(d.g + i);
         for (int j = pp - 1; j >= 0; j--) {
             __syncthreads();
-            if (tid == 0) s_x[j] = s_x[j] / d.R[j + (int64_t)j * d.ldh];
+            if (tid == 0) s_x[j] = s_x[j] / __ldcg(d.R + j + (int64_t)j * d.ldh);
             __syncthreads();
             const double yj = s_x[j];
-            for (int i = tid; i < j; i += blockDim.x) s_x[i] = s_x[i] - d.R[i + (int64_t)j * d.ldh] * yj;
+            for (int i = tid; i < j; i += blockDim.x) s_x[i] = s_x[i] - __ldcg(d.R + i + (int64_t)j * d.ldh) * yj;
         }
         __syncthreads();
         for (int i = tid; i < pp; i += blockDim.x) d.y[i] = s_x[i];
@@ -1167,14 +1167,14 @@ __global__ void __launch_bounds__(SS_THREADS)
         // Alg. 2 two-reduce, second Gauss-Seidel sweep: r2 = V_{p+1}^T u is in
         // dots2; r3 = (I + L_{p+1})^{-1} r2 (Step 15); H[:p+1, p] = r1 + r3 (Step 17);
         // alpha = r3 for w = u - V_{p+1} r3 (Step 16)
-        if (ist[ST_MODE_IT] != p || ist[ST_MODE] != 3) {
+        if (*(volatile int*)(ist + ST_MODE_IT) != p || *(volatile int*)(ist + ST_MODE) != 3) {
             if (tid == 0) ist[ST_MODE] = 0;
             return;
         }
-        for (int i = tid; i <= p; i += blockDim.x) s_x[i] = d.dots2[i];
+        for (int i = tid; i <= p; i += blockDim.x) s_x[i] = __ldcg(d.dots2 + i);
         trisolve_smem(p + 1, d.L, M, s_x);
         for (int i = tid; i <= p; i += blockDim.x) {
-            d.H[i + (int64_t)p * d.ldh] = d.H[i + (int64_t)p * d.ldh] + s_x[i];
+            d.H[i + (int64_t)p * d.ldh] = __ldcg(d.H + i + (int64_t)p * d.ldh) + s_x[i];
             d.alpha[i] = s_x[i];
         }
         __syncthreads();
@@ -1185,11 +1185,11 @@ __global__ void __launch_bounds__(SS_THREADS)
         // MGS-GMRES: gamma = ||w|| after the j+1 projections of column
         // j = p-1; H[p, p-1] = gamma, Givens, status; v_p = w / gamma by the update kernel
         const int j = p - 1;
-        const double s2 = d.dots[0];
+        const double s2 = __ldcg(d.dots);
         const double gamma = sqrt(s2);
         double h2 = 0.0;
         for (int i = tid; i <= j; i += blockDim.x) {
-            const double h = d.H[i + (int64_t)j * d.ldh];
+            const double h = __ldcg(d.H + i + (int64_t)j * d.ldh);
             h2 += h * h;
         }
         const double hn2 = block_sum(h2, red);
@@ -1197,7 +1197,7 @@ __global__ void __launch_bounds__(SS_THREADS)
         if (tid == 0) d.H[p + (int64_t)j * d.ldh] = gamma;
         __syncthreads();
         const double res = givens_column(d, j, s_col, s_cs, s_sn, red);
-        const double tol = d.scal[SC_TOL], nb = d.scal[SC_NB];
+        const double tol = __ldcg(d.scal + SC_TOL), nb = __ldcg(d.scal + SC_NB);
         const bool nonfinite = !isfinite(s2) || !isfinite(res) || !isfinite(hn2);
         const bool conv = tol > 0.0 && res <= tol * nb;
         if (tid == 0) {
@@ -1218,12 +1218,12 @@ __global__ void __launch_bounds__(SS_THREADS)
 
     const double* dv = d.dots + (int64_t)p * d.dld;
     const bool drain = (p == m);
-    const double s = dv[p];
+    const double s = __ldcg(dv + p);
 
     if (stage == SS_CRIT) {
         // ---------------- critical path of iteration p (feeds the fused update) ----------
-        for (int i = tid; i < p; i += blockDim.x) s_a[i] = dv[i];
-        if (!drain) for (int i = tid; i <= p; i += blockDim.x) s_c[i] = dv[p + 1 + i];
+        for (int i = tid; i < p; i += blockDim.x) s_a[i] = __ldcg(dv + i);
+        if (!drain) for (int i = tid; i <= p; i += blockDim.x) s_c[i] = __ldcg(dv + p + 1 + i);
         double gamma, lrow2 = 0.0;
         bool bd;
         if (gs == 2) {
@@ -1241,7 +1241,7 @@ __global__ void __launch_bounds__(SS_THREADS)
             gamma = sqrt(s);
             double h2 = 0.0;
             for (int i = tid; i < p; i += blockDim.x) {
-                const double h = d.H[i + (int64_t)(p - 1) * d.ldh];
+                const double h = __ldcg(d.H + i + (int64_t)(p - 1) * d.ldh);
                 h2 += h * h;
             }
             const double hn2 = block_sum(h2, red);
@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(SS_THREADS)
         }
         if (!isfinite(gamma)) bd = true;
         if (tid == 0) {  // ||L||_F of this cycle: row p of L is (r2 or a) / gamma
-            double cum = d.scal[SC_LCUM];
+            double cum = __ldcg(d.scal + SC_LCUM);
             if (!drain && !bd) cum += lrow2 / (gamma * gamma);
             d.scal[SC_LCUM] = cum;
             d.lnorm[t0 + p] = sqrt(cum);
@@ -1284,7 +1284,7 @@ __global__ void __launch_bounds__(SS_THREADS)
             if (tid == 0) d.beta[p] = dd - acc;
             __syncthreads();
             double* r1row = d.r1h + (int64_t)p * (M + 2);  // copy for the tail (hp, Step 15)
-            for (int i = tid; i <= p; i += blockDim.x) r1row[i] = d.beta[i];
+            for (int i = tid; i <= p; i += blockDim.x) r1row[i] = __ldcg(d.beta + i);
         } else {
             // Alg. 2 Steps 8-10: c /= gamma ; c[p] /= gamma ; L[p, :p] = a / gamma
             for (int i = tid; i <= p; i += blockDim.x) {
@@ -1305,17 +1305,17 @@ __global__ void __launch_bounds__(SS_THREADS)
     }
 
     // ---------------- SS_TAIL: Hessenberg column p-1, Givens, status, hp ------------------
-    const double tol = d.scal[SC_TOL], nb = d.scal[SC_NB];
-    const double gamma = d.gam[p];
-    bool bd = d.cbd[p] != 0.0;
+    const double tol = __ldcg(d.scal + SC_TOL), nb = __ldcg(d.scal + SC_NB);
+    const double gamma = __ldcg(d.gam + p);
+    bool bd = __ldcg(d.cbd + p) != 0.0;
     double hn2 = 0.0;
     if (gs == 2) {
         // Step 5: r3 = (I + L_p)^{-1} r2 ; Step 14: H[:p, p-1] = hp + r3, H[p, p-1] = gamma (R3)
-        for (int i = tid; i < p; i += blockDim.x) s_x[i] = dv[i];
+        for (int i = tid; i < p; i += blockDim.x) s_x[i] = __ldcg(dv + i);
         trisolve_smem(p, d.L, M, s_x);
         double h2 = 0.0;
         for (int i = tid; i < p; i += blockDim.x) {
-            const double h = d.HP[i + (int64_t)(p - 1) * d.ldh] + s_x[i];
+            const double h = __ldcg(d.HP + i + (int64_t)(p - 1) * d.ldh) + s_x[i];
             d.H[i + (int64_t)(p - 1) * d.ldh] = h;
             h2 += h * h;
         }
@@ -1340,7 +1340,7 @@ __global__ void __launch_bounds__(SS_THREADS)
     if (gs == 1 || nonfinite || bd || conv || drain) return;
     // Step 15, derived (reading R1): hp[:p+1, p] = r1 - H[:p+1, :p] (r2 / gamma); H is upper
     // Hessenberg, so row i only meets columns j >= i-1 (the skipped terms are exact zeros)
-    for (int j = tid; j < p; j += blockDim.x) s_t[j] = d.L[p + (int64_t)j * M];
+    for (int j = tid; j < p; j += blockDim.x) s_t[j] = __ldcg(d.L + p + (int64_t)j * M);
     __syncthreads();
     for (int i = tid; i <= p; i += blockDim.x) {
         double sacc = 0.0;
@@ -1348,13 +1348,20 @@ __global__ void __launch_bounds__(SS_THREADS)
         for (; j + 8 <= p; j += 8) {
             double hv[8];
 #pragma unroll
-            for (int c = 0; c < 8; c++) hv[c] = d.H[i + (int64_t)(j + c) * d.ldh];
+            for (int c = 0; c < 8; c++) hv[c] = __ldcg(d.H + i + (int64_t)(j + c) * d.ldh);
 #pragma unroll
             for (int c = 0; c < 8; c++) sacc += hv[c] * s_t[j + c];
         }
-        for (; j < p; j++) sacc += d.H[i + (int64_t)j * d.ldh] * s_t[j];
-        d.HP[i + (int64_t)p * d.ldh] = d.r1h[(int64_t)p * (M + 2) + i] - sacc;
+        for (; j < p; j++) sacc += __ldcg(d.H + i + (int64_t)j * d.ldh) * s_t[j];
+        d.HP[i + (int64_t)p * d.ldh] = __ldcg(d.r1h + (int64_t)p * (M + 2) + i) - sacc;
     }
+}
+
+__global__ void __launch_bounds__(SS_THREADS)
+    small_kernel(Dev d, int stage, int gs, int p, int m, int t0_unused) {
+    extern __shared__ double sm[];
+    __shared__ double red[40];
+    small_body(d, stage, gs, p, m, sm, red);
 }
 
 static size_t small_smem(int M) { return (size_t)(7 * (M + 2)) * sizeof(double); }
@@ -1556,6 +1563,313 @@ __global__ void fill_kernel(double* p, int64_t n, double v) {
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
     if (n <= 0) return;
     fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, v);
+}
+
+
+// ------------------------------------------------------------------------------------
+// Persistent cycle kernel ("a persistent cooperative kernel for tiny
+// n").  Iterations p = 1..m of one cycle in ONE cooperative launch, for small single-GPU
+// problems where the 4-5 dependent launches per iteration, not bytes, set the time.  Same
+// algebra as the per-kernel path (Alg. 3 for gs = 2, Alg. 2 one sweep for gs = 1).
+// Worker CTAs 0..W-1 run the phases of iteration p separated by grid barriers:
+//   A  z = A u                  lpr lanes per row                             (Step 4)
+//   B  the 2(p+1) dots          CTA b owns a contiguous range of the columns c of
+//                               [V_p, u] and forms V_c.u and V_c.z over all n rows, so
+//                               no cross-CTA partial sums exist (deterministic) (Step 4)
+//   C  critical small step      CTA 0: small_body(SS_CRIT), or the stop decision
+//   D  fused update             32-row tiles; the warps of a CTA split tiles x columns
+// The last CTA (W = G-1 when G > 1) runs the tail small step (r3, H column, Givens,
+// residual, status, hp; SS_TAIL) of iteration p as soon as CRIT(p) is published, trailing
+// the workers by at most PC_LAG iterations (CRIT(p) waits for TAIL(p - PC_LAG)); a stop the
+// tail decides is acted on at the next C phase.  Every load of data written inside the
+// launch is ld.global.cg: L1 is not coherent across SMs.
+// flags (zeroed before launch): [0] barrier count, [1] last p whose CRIT ran, [2] p at
+// which CTA 0 stopped (0 = running), [3] last p whose TAIL ran.
+// ------------------------------------------------------------------------------------
+constexpr int PC_THREADS = 512;
+constexpr int PC_WARPS = PC_THREADS / 32;
+constexpr int PC_CB = 8;   // dot columns per register block
+constexpr int PC_LAG = 2;  // iterations the tail CTA may trail the critical step
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks, unsigned& epoch) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        epoch += 1u;
+        const unsigned target = epoch * nblocks;
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_acquire_u32(bar) < target) {
+        }
+    }
+    __syncthreads();
+}
+
+template <typename IT, typename PT>
+__global__ void __launch_bounds__(PC_THREADS, 1)
+    pcycle_kernel(Dev d, int64_t n, int m, int gs, const PT* __restrict__ rowptr,
+                  const IT* __restrict__ col, const double* __restrict__ val, int lpr, double* V,
+                  int64_t ld, double* z, unsigned* flags, unsigned* counter, unsigned long long* prof) {
+    extern __shared__ double sm[];
+    __shared__ double red[40];
+    __shared__ int s_go;
+    const int M = d.m;
+    auto stamp = [&](int p, int k) {  // phase timestamps (IGS_PC_PROF=1), CTA 0 / tail CTA
+        if (prof && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            prof[(int64_t)p * 8 + k] = t;
+        }
+    };
+    double* s_small = sm;                        // small_smem(M)
+    double* s_coef = sm + 7 * (M + 2);           // alpha [M+1] | beta [M+1]
+    double* s_red = s_coef + 2 * (M + 1);        // [PC_WARPS][2 * PC_CB] (B) / [2][PC_WARPS][32] (D)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, b = blockIdx.x;
+    const bool split = G > 1;
+    const int W = split ? G - 1 : 1;             // worker CTAs
+    const volatile int* vist = d.istate;
+
+    if (split && b == G - 1) {
+        // ---------------- tail CTA ---------------------------------------------------------
+        for (int p = 1; p <= m; p++) {
+            if (tid == 0) {
+                int go = 0;
+                while (true) {
+                    if (ld_acquire_u32(flags + 1) >= (unsigned)p) { go = 1; break; }
+                    if (ld_acquire_u32(flags + 2) != 0u) {  // stopped: CRIT(p) may still have run
+                        go = ld_acquire_u32(flags + 1) >= (unsigned)p;
+                        break;
+                    }
+                }
+                s_go = go;
+                if (go && vist[ST_STATUS] == RUNNING) counter[1] += 1u;  // reductions executed
+            }
+            __syncthreads();
+            if (!s_go) break;
+            stamp(p, 6);
+            small_body(d, SS_TAIL, gs, p, m, s_small, red);
+            stamp(p, 7);
+            __syncthreads();
+            if (tid == 0) { __threadfence(); st_release_u32(flags + 3, (unsigned)p); }
+        }
+        return;
+    }
+
+    // ---------------- worker CTAs ----------------------------------------------------------
+    unsigned epoch = 0;
+    for (int p = 1; p <= m; p++) {
+        const bool drain = (p == m);
+        const double* u = V + (int64_t)p * ld;
+        if (b == 0) stamp(p, 0);
+        // ---- A: z = A u (Step 4) ---------------------------------------------------------
+        if (!drain) {
+            const int groups = 32 / lpr, sub = lane / lpr, sl = lane % lpr;
+            const int64_t stride = (int64_t)W * PC_WARPS * groups;
+            for (int64_t r0 = ((int64_t)b * PC_WARPS + warp) * groups; r0 < n; r0 += stride) {
+                const int64_t r = r0 + sub;
+                double sum = 0.0;
+                if (r < n) {
+                    const int64_t q1 = (int64_t)__ldg(rowptr + r + 1);
+                    int64_t q = (int64_t)__ldg(rowptr + r) + sl;
+                    for (; q + 3 * lpr < q1; q += 4 * lpr) {
+                        int64_t c4[4];
+                        double v4[4], x4[4];
+#pragma unroll
+                        for (int k = 0; k < 4; k++) { c4[k] = (int64_t)__ldg(col + q + k * lpr); v4[k] = __ldg(val + q + k * lpr); }
+#pragma unroll
+                        for (int k = 0; k < 4; k++) x4[k] = __ldcg(u + c4[k]);
+#pragma unroll
+                        for (int k = 0; k < 4; k++) sum = fma(v4[k], x4[k], sum);
+                    }
+                    for (; q < q1; q += lpr) sum = fma(__ldg(val + q), __ldcg(u + (int64_t)__ldg(col + q)), sum);
+                }
+                for (int off = lpr >> 1; off > 0; off >>= 1) sum += __shfl_xor_sync(FULL_MASK, sum, off);
+                if (r < n && sl == 0) z[r] = sum;
+            }
+            grid_barrier(flags, W, epoch);
+        }
+        if (b == 0) stamp(p, 1);
+        // ---- B: dots [V_p, u]^T [u, z] -> d.dots + p*dld (Step 4, one reduction) ------
+        {
+            double* out = d.dots + (int64_t)p * d.dld;
+            const int items = p + 1;
+            const int per = (items + W - 1) / W;
+            const int c0 = b * per, c1 = min(c0 + per, items);
+            for (int cb = c0; cb < c1; cb += PC_CB) {
+                const int nc = min(PC_CB, c1 - cb);
+                double au[PC_CB], az[PC_CB];
+#pragma unroll
+                for (int c = 0; c < PC_CB; c++) { au[c] = 0.0; az[c] = 0.0; }
+                for (int64_t r = tid; r < n; r += PC_THREADS) {
+                    const double uu = __ldcg(u + r);
+                    const double zz = drain ? 0.0 : __ldcg(z + r);
+#pragma unroll
+                    for (int c = 0; c < PC_CB; c++) {
+                        if (c < nc) {
+                            const double v = __ldcg(V + (int64_t)(cb + c) * ld + r);
+                            au[c] = fma(v, uu, au[c]);
+                            az[c] = fma(v, zz, az[c]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < PC_CB; c++) {
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) {
+                        au[c] += __shfl_xor_sync(FULL_MASK, au[c], off);
+                        az[c] += __shfl_xor_sync(FULL_MASK, az[c], off);
+                    }
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int c = 0; c < PC_CB; c++) {
+                        s_red[warp * 2 * PC_CB + c] = au[c];
+                        s_red[warp * 2 * PC_CB + PC_CB + c] = az[c];
+                    }
+                }
+                __syncthreads();
+                if (tid < 2 * nc) {
+                    const int c = tid % nc, which = tid / nc;  // 0: V_c.u, 1: V_c.z
+                    double t = 0.0;
+                    for (int w = 0; w < PC_WARPS; w++) t += s_red[w * 2 * PC_CB + which * PC_CB + c];
+                    if (which == 0) out[cb + c] = t;
+                    else if (!drain) out[p + 1 + cb + c] = t;
+                }
+                __syncthreads();
+            }
+        }
+        grid_barrier(flags, W, epoch);
+        if (b == 0) stamp(p, 2);
+        // ---- C: critical small step or the stop decision (CTA 0) ---------------------------
+        if (b == 0) {
+            if (tid == 0) {
+                if (split && p > PC_LAG)
+                    while (ld_acquire_u32(flags + 3) < (unsigned)(p - PC_LAG)) {
+                    }
+                s_go = (vist[ST_STATUS] == RUNNING);
+                if (!s_go) { __threadfence(); st_release_u32(flags + 2, (unsigned)p); }
+            }
+            __syncthreads();
+            if (s_go) {
+                small_body(d, SS_CRIT, gs, p, m, s_small, red);
+                __syncthreads();
+                if (tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
+            }
+            stamp(p, 3);
+        }
+        grid_barrier(flags, W, epoch);
+        if (b == 0) stamp(p, 4);
+        if (*(volatile unsigned*)(flags + 2) != 0u) break;  // uniform: written before the barrier
+        // ---- D: fused update (Steps 10-13) -------------------------------------------------
+        {
+            int mode = (vist[ST_MODE_IT] == p) ? vist[ST_MODE] : 0;
+            mode &= drain ? 1 : 3;
+            if (mode != 0) {
+                const bool want_next = (mode & 2) != 0;
+                double* sa = s_coef;
+                double* sbt = s_coef + (M + 1);
+                if (gs == 2)
+                    for (int j = tid; j < p; j += PC_THREADS) sa[j] = __ldcg(d.alpha + j);
+                if (want_next)
+                    for (int j = tid; j <= p; j += PC_THREADS) sbt[j] = __ldcg(d.beta + j);
+                const double gamma = __ldcg(d.scal + SC_GAMMA);
+                __syncthreads();
+                double* r1s = s_red;                  // [PC_WARPS][32]
+                double* r2s = s_red + PC_WARPS * 32;  // [PC_WARPS][32]
+                const int64_t ntiles = (n + 31) / 32;
+                const int64_t mine = ntiles > b ? (ntiles - b + W - 1) / W : 0;  // tiles b, b+W, ...
+                for (int64_t g0 = 0; g0 < mine; g0 += PC_WARPS) {
+                    const int nt = (int)min((int64_t)PC_WARPS, mine - g0);
+                    const int S = PC_WARPS / nt;  // warps (column slices) per tile
+                    const int ti = warp / S, sl = warp % S;
+                    double t1 = 0.0, t2 = 0.0;
+                    if (ti < nt) {
+                        const int64_t r = (b + (g0 + ti) * W) * 32 + lane;
+                        if (r < n) {
+#pragma unroll 4
+                            for (int j = sl; j < p; j += S) {
+                                const double v = __ldcg(V + (int64_t)j * ld + r);
+                                if (gs == 2) t1 = fma(v, sa[j], t1);
+                                if (want_next) t2 = fma(v, sbt[j], t2);
+                            }
+                        }
+                    }
+                    r1s[warp * 32 + lane] = t1;
+                    r2s[warp * 32 + lane] = t2;
+                    __syncthreads();
+                    if (warp < nt) {
+                        const int64_t r = (b + (g0 + warp) * W) * 32 + lane;
+                        if (r < n) {
+                            double s1 = 0.0, s2 = 0.0;
+                            for (int k = 0; k < S; k++) { s1 += r1s[(warp * S + k) * 32 + lane]; s2 += r2s[(warp * S + k) * 32 + lane]; }
+                            const double uu = __ldcg(u + r);
+                            const double w_ = (gs == 2) ? uu - s1 : uu;
+                            const double vv = w_ / gamma;
+                            if (want_next) V[(int64_t)(p + 1) * ld + r] = __ldcg(z + r) / gamma - fma(vv, sbt[p], s2);
+                            if (mode & 1) V[(int64_t)p * ld + r] = vv;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+        if (b == 0) stamp(p, 5);
+        if (!split) {  // one CTA: the tail runs in line
+            if (tid == 0 && vist[ST_STATUS] == RUNNING) counter[1] += 1u;
+            __syncthreads();
+            stamp(p, 6);
+            small_body(d, SS_TAIL, gs, p, m, s_small, red);
+            stamp(p, 7);
+        }
+        grid_barrier(flags, W, epoch);
+    }
+}
+
+static size_t pcycle_smem(int M) {
+    return (size_t)(7 * (M + 2) + 2 * (M + 1) + 2 * PC_WARPS * 32) * sizeof(double);
+}
+
+template <typename IT, typename PT>
+static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
+                             int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
+                             unsigned long long* prof) {
+    auto fn = pcycle_kernel<IT, PT>;
+    const size_t smem = pcycle_smem(d.m);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, PC_THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    Dev dd = d;
+    const PT* rp = static_cast<const PT*>(a.rowptr);
+    const IT* ci = static_cast<const IT*>(a.col);
+    const double* va = a.val;
+    int lpr = a.lpr > 0 ? a.lpr : 4;
+    void* args[] = {&dd, &n, &m, &gs, (void*)&rp, (void*)&ci, (void*)&va, &lpr, &V, &ld, &z, &flags, &counter, &prof};
+    return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(PC_THREADS), args, smem, s);
+}
+
+int pcycle_max_grid(int num_sms) { return num_sms; }
+
+cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
+                          int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
+                          unsigned long long* prof) {
+    if (a.idx64) {
+        if (a.ptr64) return pcycle_go<int64_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
+        return pcycle_go<int64_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
+    }
+    if (a.ptr64) return pcycle_go<int32_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
+    return pcycle_go<int32_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
 }
 
 }  // namespace igs

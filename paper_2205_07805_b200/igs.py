@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_PKG, "libigs.so")
 IGS_OK, IGS_ERR_ARG, IGS_ERR_CUDA, IGS_ERR_NCCL, IGS_ERR_OOM, IGS_ERR_NONFINITE, IGS_ERR_STATE = range(7)
 IGS_MEM_HOST, IGS_MEM_DEVICE = 0, 1
 TERM = {0: "converged", 1: "maxiter", 2: "breakdown"}
-KERNEL_KINDS = ["spmv", "block_dot", "allreduce", "small", "update", "halo", "cycle"]
+KERNEL_KINDS = ["spmv", "block_dot", "allreduce", "small", "update", "halo", "cycle", "persist"]
 STATUS_NAMES = {0: "OK", 1: "ERR_ARG", 2: "ERR_CUDA", 3: "ERR_NCCL", 4: "ERR_OOM",
                 5: "ERR_NONFINITE", 6: "ERR_STATE"}
 

@@ -220,9 +220,10 @@ def test_zero_rhs(P):
     s.close()
 
 
-def test_kernel_timing_counts(P):
+def test_kernel_timing_counts(P, monkeypatch):
     import torch
     prob = W.config("c3", N=64)
+    monkeypatch.setenv("IGS_PERSIST", "0")   # the per-kernel path (the persistent kernel is one launch)
     s = P.Solver(prob.A)
     s.set_timing(2)
     s.solve(torch.from_numpy(prob.b).cuda(), k=40, gs_iters=2)
@@ -368,6 +369,7 @@ def test_cuda_graph_cycle_matches_stream_path(P, monkeypatch):
     import torch
     prob = W.config("c3", N=48)
     outs = {}
+    monkeypatch.setenv("IGS_PERSIST", "0")   # graphs replay the per-kernel path
     for graphs in ("1", "0"):
         monkeypatch.setenv("IGS_GRAPHS", graphs)
         s = P.Solver(prob.A)
@@ -472,3 +474,40 @@ def test_paper_matrices_on_gpu(P):
     g = s.solve(torch.from_numpy(b).cuda(), k=16, gs_iters=2, want_loo=True)
     s.close()
     assert g["loo"] <= 1e-14
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+@pytest.mark.parametrize("cfg,grid", [("c1", "0"), ("c1", "1"), ("c1", "2"), ("c2", "0"), ("c2", "3"), ("c3s", "0"), ("c3s", "2")])
+def test_persistent_cycle_kernel(P, cfg, grid, gs, monkeypatch):
+    """Small single-GPU problems run each cycle as ONE cooperative launch.
+    Same algebra as the per-kernel path, different reduction order: H within the parity bar
+    of the per-kernel path and of the oracle, same iterations / reductions / termination,
+    bitwise reproducible; grid=1 puts the update and the tail on the same CTA."""
+    import torch
+    prob = W.config("c3", N=48) if cfg == "c3s" else W.config(cfg)
+    k, restart, tol = (70, 30, 1e-10) if cfg == "c3s" else (prob.k, 0, 0.0)
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for persist in ("1", "0"):
+        monkeypatch.setenv("IGS_PERSIST", persist)
+        monkeypatch.setenv("IGS_PC_GRID", grid)
+        s = P.Solver(prob.A)
+        s.set_timing(1)
+        outs[persist] = [s.solve(b, k=k, restart=restart, tol=tol, gs_iters=gs, want_loo=True) for _ in range(2)]
+        launches = s.kernel_stats()["persist"]["launches"]
+        s.set_timing(0)
+        s.close()
+        assert (launches > 0) == (persist == "1")
+    pc, ref = outs["1"][0], outs["0"][0]
+    assert outs["1"][1]["H"].tobytes() == pc["H"].tobytes()          # deterministic
+    assert outs["1"][1]["x"].cpu().numpy().tobytes() == pc["x"].cpu().numpy().tobytes()
+    assert pc["iters"] == ref["iters"] and pc["term"] == ref["term"] and pc["cycles"] == ref["cycles"]
+    assert pc["reductions"] == ref["reductions"] and pc["basis_cols"] == ref["basis_cols"]
+    o = oracle.gmres(prob.A, prob.b, k, restart=restart, tol=tol, variant=VARIANT[gs], dot_block=4096)
+    d, c = _compare_cols(pc["H"], o["H"], o["res_hist"])
+    floor = oracle.column_normwise_diff(
+        oracle.gmres(prob.A, prob.b, k, restart=restart, tol=tol, variant=VARIANT[gs], dot_block=0)["H"], o["H"], c)
+    assert d <= 1e-10 or d <= 2 * floor, (d, floor)
+    np.testing.assert_allclose(pc["res_hist"], ref["res_hist"], rtol=1e-6, atol=1e-13)
+    assert _loo_close(pc["loo"], ref["loo"]) or gs == 1 and 0.01 <= pc["loo"] / ref["loo"] <= 100
+    assert pc["true_relres"] <= max(10 * ref["true_relres"], 1e-14)
