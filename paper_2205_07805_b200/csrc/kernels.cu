@@ -1721,20 +1721,12 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                         }
                     }
                 }
-#pragma unroll
-                for (int c = 0; c < PC_CB; c++) {
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
-                        au[c] += __shfl_xor_sync(FULL_MASK, au[c], off);
-                        az[c] += __shfl_xor_sync(FULL_MASK, az[c], off);
-                    }
-                }
-                if (lane == 0) {
-#pragma unroll
-                    for (int c = 0; c < PC_CB; c++) {
-                        s_red[warp * 2 * PC_CB + c] = au[c];
-                        s_red[warp * 2 * PC_CB + PC_CB + c] = az[c];
-                    }
+                static_assert(PC_CB == 8, "bfly8 reduces 8 columns");
+                const double ru = bfly8(au, lane);  // lane holds column lane >> 2
+                const double rz = bfly8(az, lane);
+                if ((lane & 3) == 0) {
+                    s_red[warp * 2 * PC_CB + (lane >> 2)] = ru;
+                    s_red[warp * 2 * PC_CB + PC_CB + (lane >> 2)] = rz;
                 }
                 __syncthreads();
                 if (tid < 2 * nc) {
@@ -1791,7 +1783,11 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                     const int nt = (int)min((int64_t)PC_WARPS, mine - g0);
                     const int S = PC_WARPS / nt;  // warps (column slices) per tile
                     const int ti = warp / S, sl = warp % S;
-                    double t1 = 0.0, t2 = 0.0;
+                    double t1 = 0.0, t2 = 0.0, uu = 0.0, zz = 0.0;
+                    if (warp < nt) {  // the epilogue's u and z, fetched ahead of the column loop
+                        const int64_t r = (b + (g0 + warp) * W) * 32 + lane;
+                        if (r < n) { uu = __ldcg(u + r); if (want_next) zz = __ldcg(z + r); }
+                    }
                     if (ti < nt) {
                         const int64_t r = (b + (g0 + ti) * W) * 32 + lane;
                         if (r < n) {
@@ -1811,10 +1807,9 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                         if (r < n) {
                             double s1 = 0.0, s2 = 0.0;
                             for (int k = 0; k < S; k++) { s1 += r1s[(warp * S + k) * 32 + lane]; s2 += r2s[(warp * S + k) * 32 + lane]; }
-                            const double uu = __ldcg(u + r);
                             const double w_ = (gs == 2) ? uu - s1 : uu;
                             const double vv = w_ / gamma;
-                            if (want_next) V[(int64_t)(p + 1) * ld + r] = __ldcg(z + r) / gamma - fma(vv, sbt[p], s2);
+                            if (want_next) V[(int64_t)(p + 1) * ld + r] = zz / gamma - fma(vv, sbt[p], s2);
                             if (mode & 1) V[(int64_t)p * ld + r] = vv;
                         }
                     }
@@ -1835,7 +1830,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
 }
 
 static size_t pcycle_smem(int M) {
-    return (size_t)(7 * (M + 2) + 2 * (M + 1) + 2 * PC_WARPS * 32) * sizeof(double);
+    return small_smem(M) + (size_t)(2 * (M + 1) + 2 * PC_WARPS * 32) * sizeof(double);
 }
 
 template <typename IT, typename PT>
