@@ -21,6 +21,7 @@
 
 #include "../../include/igs.h"
 #include "igs_internal.cuh"
+#include "xchg.cuh"
 
 namespace igs {
 static thread_local std::string g_err;
@@ -147,6 +148,14 @@ struct igs_ctx {
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
     int64_t n_pcycle = 0;
     unsigned long long* d_pcprof = nullptr;  // IGS_PC_PROF=1 phase timestamps
+    // fused block dot + allreduce over NVLink (IGS_XCHG=1): NCCL symmetric window + device comm
+    bool xchg_req = false;
+    void* xbuf = nullptr;
+    ncclWindow_t xwin = nullptr;
+    ncclDevComm dcomm{};
+    bool dcomm_ok = false;
+    XchgDev* d_xchg = nullptr;  // device copy; null = separate ncclAllReduce
+    int xslot = 0;              // slot capacity (doubles) of the registered window
 };
 
 // ------------------------------------------------------------------------------ misc
@@ -368,6 +377,10 @@ static void free_ctx(igs_ctx* c) {
     if (c->ev_g0) cudaEventDestroy(c->ev_g0);
     if (c->ev_g1) cudaEventDestroy(c->ev_g1);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
+    if (c->dcomm_ok) ncclDevCommDestroy(c->comm, &c->dcomm);
+    if (c->xwin) ncclCommWindowDeregister(c->comm, c->xwin);
+    if (c->xbuf) ncclMemFree(c->xbuf);
+    cudaFree(c->d_xchg);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
 }
@@ -433,9 +446,16 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
 
     auto fail = [&](igs_status s) { free_ctx(ctx); return s; };
-    if (nranks > 1) {
+    if (const char* e = std::getenv("IGS_XCHG")) ctx->xchg_req = std::atoi(e) != 0;
+    if (nranks > 1 || ctx->xchg_req) {
+        // (one rank + IGS_XCHG=1: a 1-rank communicator, so the fused exchange path runs on
+        //  a single GPU exactly as it does on G)
         ncclUniqueId id;
-        std::memcpy(&id, nccl_unique_id, sizeof(id));
+        if (nranks > 1) std::memcpy(&id, nccl_unique_id, sizeof(id));
+        else if (ncclGetUniqueId(&id) != ncclSuccess) {
+            set_error("ncclGetUniqueId failed");
+            return fail(IGS_ERR_NCCL);
+        }
         ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
         if (r != ncclSuccess) {
             set_error(std::string("ncclCommInitRank failed: ") + ncclGetErrorString(r));
@@ -594,6 +614,44 @@ extern "C" igs_status igs_bind_workspace(igs_ctx* ctx, void* dev_ptr, size_t byt
     return IGS_OK;
 }
 
+// Symmetric window of 2 slots x `slot` doubles + the device communicator with one LSA
+// barrier (collective over the ranks; ensure_workspace runs on every rank in step).
+static igs_status setup_xchg(igs_ctx* ctx, int slot) {
+    if (ctx->d_xchg && slot <= ctx->xslot) return IGS_OK;
+    if (ctx->xwin) { NCCL_TRY(ncclCommWindowDeregister(ctx->comm, ctx->xwin)); ctx->xwin = nullptr; }
+    if (ctx->xbuf) { NCCL_TRY(ncclMemFree(ctx->xbuf)); ctx->xbuf = nullptr; }
+    size_t bytes = (size_t)2 * slot * sizeof(double);
+    bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
+    NCCL_TRY(ncclMemAlloc(&ctx->xbuf, bytes));
+    NCCL_TRY(ncclCommWindowRegister(ctx->comm, ctx->xbuf, bytes, &ctx->xwin, NCCL_WIN_COLL_SYMMETRIC));
+    if (!ctx->dcomm_ok) {
+        ncclDevCommRequirements reqs;
+        std::memset(&reqs, 0, sizeof(reqs));
+        reqs.lsaBarrierCount = 1;
+        NCCL_TRY(ncclDevCommCreate(ctx->comm, &reqs, &ctx->dcomm));
+        ctx->dcomm_ok = true;
+    }
+    if (ctx->dcomm.lsaSize != ctx->nranks) {  // not one NVLink domain: keep ncclAllReduce
+        cudaFree(ctx->d_xchg);
+        ctx->d_xchg = nullptr;
+        return IGS_OK;
+    }
+    if (!ctx->d_xchg) {
+        CUDA_TRY(cudaMalloc(&ctx->d_xchg, sizeof(XchgDev) + 16));
+        CUDA_TRY(cudaMemset(ctx->d_xchg, 0, sizeof(XchgDev) + 16));
+    }
+    XchgDev h;
+    std::memset(&h, 0, sizeof(h));
+    h.comm = ctx->dcomm;
+    h.win = ctx->xwin;
+    h.calls = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->d_xchg) + sizeof(XchgDev));
+    h.slot_doubles = slot;
+    h.nranks = ctx->nranks;
+    CUDA_TRY(cudaMemcpy(ctx->d_xchg, &h, sizeof(h), cudaMemcpyHostToDevice));
+    ctx->xslot = slot;
+    return IGS_OK;
+}
+
 static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
     const int64_t ldv = ctx->ldv;
     if (m > ctx->m_cap || k > ctx->k_cap) {
@@ -655,6 +713,7 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.istate = ctx->d_int;
         ctx->m_cap = mm;
         ctx->k_cap = kk;
+        if (ctx->xchg_req) TRY(setup_xchg(ctx, d.dld));
     }
     if (!ctx->d_z) {
         CUDA_TRY(cudaMalloc(&ctx->d_z, sizeof(double) * ldv));
@@ -721,6 +780,16 @@ static igs_status spmv(igs_ctx* ctx, const double* x, double* y, const double* b
 static igs_status bdot(igs_ctx* ctx, int p, const double* u, const double* z, double* out,
                        const int* istate, int kind) {
     const double by = 8.0 * ctx->n_local * (p + 1 + (z ? 1 : 0));
+    if (ctx->d_xchg) {
+        // block dot with the cross-rank sum fused in; it never skips on the status word
+        // (a rank that skipped would leave its peers waiting at the LSA barrier)
+        TIMED(kind, by,
+              launch_block_dot(ctx->n_local, p, ctx->d_V, ctx->ldv, u, z, out, ctx->d_part,
+                               ctx->d_counter, ctx->bdot_grid, nullptr, ctx->stream, nullptr, ctx->d_xchg));
+        ctx->n_allreduce++;
+        ctx->n_reduce++;
+        return IGS_OK;
+    }
     TIMED(kind, by,
           launch_block_dot(ctx->n_local, p, ctx->d_V, ctx->ldv, u, z, out, ctx->d_part,
                            ctx->d_counter, ctx->bdot_grid, istate, ctx->stream,
@@ -749,7 +818,7 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0);
 // alg: IGS_ALG_IGS1 (1), IGS_ALG_IGS2 (2, Alg. 3), IGS_ALG_IGS2_TWO (3, Alg. 2 literal),
 // IGS_ALG_MGS (4).  Algorithms 1 and 3 share the gs = 1 small-step stages.
 static bool use_pcycle(const igs_ctx* ctx, int alg) {
-    return ctx->pc_enabled && ctx->nranks == 1 && ctx->n_local <= ctx->pc_max_n && !ctx->fused_enabled &&
+    return ctx->pc_enabled && ctx->nranks == 1 && !ctx->xchg_req && ctx->n_local <= ctx->pc_max_n && !ctx->fused_enabled &&
            (alg == IGS_ALG_IGS1 || alg == IGS_ALG_IGS2) && ctx->dev_state.m <= 1024;
 }
 
@@ -828,7 +897,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         const bool drain = (p == m);
         double* u = Vcol(ctx, p);
         if (!dots_ready) {
-            if (!drain && ctx->bs_ok && bdot_spmv_fits(p)) {
+            if (!drain && ctx->bs_ok && !ctx->xchg_req && bdot_spmv_fits(p)) {
                 // Step 4: z = A u and the fused block dot in one bulk-copy pipeline
                 TRY(halo(ctx, u, ist));
                 const double by = 8.0 * n * (p + 1) + spmv_bytes(ctx);
@@ -864,7 +933,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         // CTA, ahead = ceil(L / G) + 2 with L = ceil(reach / T) (fused.cu)
         const int64_t Lt = (ctx->reach + T - 1) / T, Gf = ctx->fused_grid;
         const double window = (double)(((Lt + Gf - 1) / Gf + 2) * Gf + 2) * T * (p + 3) * 8.0;
-        if (!drain && !two_reduce && ctx->nranks == 1 && ctx->fused_enabled && ctx->fused_ok && ctx->d_flags && p + 2 <= fused_max_cols() &&
+        if (!drain && !two_reduce && ctx->nranks == 1 && !ctx->xchg_req && ctx->fused_enabled && ctx->fused_ok && ctx->d_flags && p + 2 <= fused_max_cols() &&
             window <= ctx->fused_budget && n >= 4 * T) {
             // update(p) + SpMV(p+1) + block dot(p+1), V_p read from HBM once
             const int lag = (int)((ctx->reach + T - 1) / T);

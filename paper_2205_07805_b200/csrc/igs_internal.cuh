@@ -81,9 +81,11 @@ cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld
 // Fused block dot: out = [V_p^T u, u.u, V_p^T z, u.z] (z != NULL) or [V_p^T u, u.u].
 // part: [grid * 2(p+1)] scratch, counter: one zeroed unsigned (reset by the kernel).
 int bdot_grid_size(int64_t n, int num_sms);
+struct XchgDev;  // xchg.cuh: fused cross-rank sum over NVLink (NCCL device API)
 void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                       const double* z, double* out, double* part, unsigned* counter, int grid,
-                      const int* istate, cudaStream_t s, const CUtensorMap* tmV = nullptr);
+                      const int* istate, cudaStream_t s, const CUtensorMap* tmV = nullptr,
+                      const XchgDev* xc = nullptr);
 
 // Fused update (see igs.h igs_op_update).  gamma read from *gamma_dev.
 // istate/it: when istate != NULL the mode bits istate[ST_MODE] (valid iff

@@ -19,6 +19,7 @@
 
 #include "igs_internal.cuh"
 #include "ptx_util.cuh"
+#include "xchg.cuh"
 
 namespace igs {
 
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
     bdot_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
                 const double* __restrict__ u, const double* __restrict__ z,
                 double* __restrict__ part, double* __restrict__ out, unsigned* counter,
-                const int* istate) {
+                const int* istate, const XchgDev* xc) {
     if (!running(istate)) return;
     extern __shared__ double sacc[];  // [BD_WARPS][NV * ncols]
     __shared__ bool s_last;
@@ -345,8 +346,9 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // stage 2b: last CTA sums the partials in CTA order
-    final_reduce(part, stride, (int)gridDim.x, out);
+    // stage 2b: last CTA sums the partials in CTA order (+ across ranks over NVLink)
+    if (xc) final_reduce_xchg(part, stride, (int)gridDim.x, out, *xc);
+    else final_reduce(part, stride, (int)gridDim.x, out);
     if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
 }
 
@@ -373,7 +375,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     bdot_tma_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
                     const double* __restrict__ u, const double* __restrict__ z,
                     double* __restrict__ part, double* __restrict__ out, unsigned* counter,
-                    const int* istate) {
+                    const int* istate, const XchgDev* xc) {
     if (!running(istate)) return;
     extern __shared__ __align__(128) double smem_bt[];
     double* ring = smem_bt;                                        // [STAGES][8][512]
@@ -510,7 +512,9 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    final_reduce(part, stride, (int)gridDim.x, out);  // [V_p^T u, u.u, V_p^T z, u.z]
+    // [V_p^T u, u.u, V_p^T z, u.z] (+ across ranks over NVLink)
+    if (xc) final_reduce_xchg(part, stride, (int)gridDim.x, out, *xc);
+    else final_reduce(part, stride, (int)gridDim.x, out);
     if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
 }
 
@@ -787,8 +791,9 @@ int bdot_grid_size(int64_t n, int num_sms) {
 
 void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                       const double* z, double* out, double* part, unsigned* counter, int grid,
-                      const int* istate, cudaStream_t s, const CUtensorMap* tmV) {
+                      const int* istate, cudaStream_t s, const CUtensorMap* tmV, const XchgDev* xc) {
     const int nv = z ? 2 : 1;
+    if (xc) tmV = nullptr;  // the exchange is fused into the bulk-copy and register kernels only
     // default: 2D TMA tensor copies of V (tmV: box 256 rows x 8 columns over V's columns)
     const size_t msmem = bdot_tmap_smem(p, nv);
     if (tmV && p > 0 && msmem <= 227 * 1024 && ((uintptr_t)u % 16) == 0 && (!z || ((uintptr_t)z % 16) == 0) &&
@@ -818,7 +823,7 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
         variant = (e && e[0] == 's') ? 1 : 0;
     }
     const size_t ssmem = (size_t)(nv * BS2_TILE + BS2_WARPS * nv * (p + 1)) * sizeof(double);
-    if (variant == 1 && p > 0 && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 && ((uintptr_t)u % 16) == 0 &&
+    if (!xc && variant == 1 && p > 0 && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 && ((uintptr_t)u % 16) == 0 &&
         ssmem <= 113 * 1024) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -844,10 +849,10 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
         if (tg <= grid) {
             if (nv == 2) {
                 cudaFuncSetAttribute(bdot_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-                bdot_tma_kernel<2><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+                bdot_tma_kernel<2><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
             } else {
                 cudaFuncSetAttribute(bdot_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-                bdot_tma_kernel<1><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+                bdot_tma_kernel<1><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
             }
             return;
         }
@@ -855,10 +860,10 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
     const size_t smem = bdot_smem(p, nv);
     if (nv == 2) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(bdot_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        bdot_kernel<2><<<grid, BD_THREADS, smem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+        bdot_kernel<2><<<grid, BD_THREADS, smem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
     } else {
         if (smem > 48 * 1024) cudaFuncSetAttribute(bdot_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        bdot_kernel<1><<<grid, BD_THREADS, smem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
+        bdot_kernel<1><<<grid, BD_THREADS, smem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
     }
 }
 

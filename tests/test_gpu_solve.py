@@ -511,3 +511,28 @@ def test_persistent_cycle_kernel(P, cfg, grid, gs, monkeypatch):
     np.testing.assert_allclose(pc["res_hist"], ref["res_hist"], rtol=1e-6, atol=1e-13)
     assert _loo_close(pc["loo"], ref["loo"]) or gs == 1 and 0.01 <= pc["loo"] / ref["loo"] <= 100
     assert pc["true_relres"] <= max(10 * ref["true_relres"], 1e-14)
+
+
+@pytest.mark.parametrize("alg", ["igs2", "igs1", "igs2_two", "mgs"])
+@pytest.mark.parametrize("cfg", ["c3s", "c3m"])
+def test_fused_block_dot_allreduce_one_rank(P, cfg, alg, monkeypatch):
+    """IGS_XCHG=1: the block dot's last CTA sums across ranks through an NCCL symmetric window
+    and an LSA barrier (device API) instead of a separate ncclAllReduce.  On one GPU the
+    communicator has one rank, so the result must be bit-identical to the plain path, with
+    one exchange per block dot."""
+    import torch
+    prob = W.config("c3", N=48 if cfg == "c3s" else 128)
+    b = torch.from_numpy(prob.b).cuda()
+    k, restart = (60, 25) if alg != "mgs" else (30, 15)
+    outs = {}
+    for x in ("1", "0"):
+        monkeypatch.setenv("IGS_XCHG", x)
+        monkeypatch.setenv("IGS_PERSIST", "0")
+        s = P.Solver(prob.A)
+        outs[x] = [s.solve(b, k=k, restart=restart, tol=1e-10, algorithm=alg) for _ in range(2)]
+        s.close()
+    for g, u in zip(outs["1"], outs["0"]):
+        assert g["iters"] == u["iters"] and g["term"] == u["term"] and g["cycles"] == u["cycles"]
+        assert g["H"].tobytes() == u["H"].tobytes()
+        assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+        assert g["allreduces"] == g["reductions"] > 0 and u["allreduces"] == 0
