@@ -253,6 +253,11 @@ def S_norm(V, p: int) -> float:
     return float(np.linalg.norm(S, 2))
 
 
+def sigma_min(V, p: int) -> float:
+    """Smallest singular value of V_p (the plain definition, LAPACK SVD)."""
+    return float(np.linalg.svd(np.asarray(V)[:, :p], compute_uv=False)[-1])
+
+
 def column_normwise_diff(H1, H2, ncols: int) -> float:
     """max_j max_i |H1_ij - H2_ij| / max_i |H2_ij| over the first ncols columns
     (the parity metric of reading R9)."""

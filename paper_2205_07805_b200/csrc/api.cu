@@ -1231,8 +1231,10 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     std::vector<double> hl(k + 1, std::nan(""));
     if (res->lnorm_hist && total > 0 && gs_iters != IGS_ALG_MGS)
         CUDA_TRY(cudaMemcpyAsync(hl.data(), d.lnorm, sizeof(double) * (total + 1), cudaMemcpyDeviceToHost, st));
-    // LOO of the final basis, diagnostic
-    if (res->want_loo && last_basis > 0) {
+    res->s_norm = std::nan("");
+    res->sigma_min = std::nan("");
+    // LOO of the final basis, ||S||_2 and sigma_min: diagnostics from G = V^T V
+    if ((res->want_loo || res->want_basis_diag) && last_basis > 0) {
         const int c = last_basis;
         const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 4096));
         const size_t need = (size_t)splits * c * c + (size_t)c * c + 1;
@@ -1248,7 +1250,18 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         TIMED(IGS_K_CYCLE, 0.0, launch_loo_norm(c, G, G + (size_t)c * c, st));
         double loo = 0.0;
         TRY(fetch(ctx, G + (size_t)c * c, 1, &loo, nullptr, 0, nullptr));
-        res->loo_frob = loo;
+        if (res->want_loo) res->loo_frob = loo;
+        if (res->want_basis_diag) {
+            double* ws = nullptr;
+            CUDA_TRY(cudaMalloc(&ws, sizeof(double) * (basis_diag_doubles(c) + 2)));
+            TIMED(IGS_K_CYCLE, 0.0, launch_basis_diag(c, G, ws, ws + basis_diag_doubles(c), st));
+            double sd[2] = {0.0, 0.0};
+            igs_status fs = fetch(ctx, ws + basis_diag_doubles(c), 2, sd, nullptr, 0, nullptr);
+            cudaFree(ws);
+            TRY(fs);
+            res->s_norm = sd[0];
+            res->sigma_min = sd[1];
+        }
     }
     if (hostv) CUDA_TRY(cudaMemcpyAsync(res->x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -1420,6 +1433,30 @@ extern "C" igs_status igs_qr(int64_t n, int m, const double* A, int64_t lda, dou
             return IGS_ERR_NONFINITE;
         }
     }
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_op_basis_diag(int64_t n, int c, const double* V, int64_t ld, double* out3,
+                                        void* cuda_stream) {
+    ARG_CHECK(n >= 1 && c >= 1 && c <= 4096 && ld >= n && V && out3, "igs_op_basis_diag: bad argument");
+    TRY(have_device());
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 4096));
+    const size_t nd = (size_t)splits * c * c + (size_t)c * c + 1 + basis_diag_doubles(c) + 2;
+    double* ws = nullptr;
+    CUDA_TRY(cudaMalloc(&ws, nd * sizeof(double)));
+    struct Free { double* w; ~Free() { cudaFree(w); } } guard{ws};
+    double* G = ws + (size_t)splits * c * c;
+    double* loo = G + (size_t)c * c;
+    double* dws = loo + 1;
+    double* sd = dws + basis_diag_doubles(c);
+    launch_gram(n, c, V, ld, ws, splits, G, st);
+    launch_loo_norm(c, G, loo, st);
+    launch_basis_diag(c, G, dws, sd, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out3, loo, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(out3 + 1, sd, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     return IGS_OK;
 }
 

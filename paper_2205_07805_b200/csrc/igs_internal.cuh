@@ -130,6 +130,11 @@ void launch_trisolve(int order, const double* L, int ldl, const double* b, doubl
 void launch_gram(int64_t n, int c, const double* V, int64_t ld, double* part, int splits,
                  double* G, cudaStream_t s);
 void launch_loo_norm(int c, const double* G, double* out, cudaStream_t s);
+// diag.cu: ||S||_2 (S = (I+U)^{-1} U, U = strictly upper part of G) and sigma_min(V) =
+// sqrt(lambda_min(G)) from the Gram matrix G = V^T V (c x c); ws: basis_diag_doubles(c)
+// doubles of device scratch; out (device): [||S||_2, sigma_min].
+size_t basis_diag_doubles(int c);
+void launch_basis_diag(int c, const double* G, double* ws, double* out, cudaStream_t s);
 
 // halo pack: buf[i] = x[idx[i]]
 void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, const int* istate,

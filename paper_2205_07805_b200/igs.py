@@ -27,7 +27,8 @@ STATUS_NAMES = {0: "OK", 1: "ERR_ARG", 2: "ERR_CUDA", 3: "ERR_NCCL", 4: "ERR_OOM
 EXPORTS = ["igs_create", "igs_nccl_unique_id", "igs_workspace_bytes", "igs_bind_workspace",
            "igs_solve", "igs_solve_alg", "igs_stats", "igs_set_timing", "igs_kernel_stats", "igs_destroy",
            "igs_last_error", "igs_op_block_dot", "igs_op_spmv", "igs_op_update",
-           "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap", "igs_qr"]
+           "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap", "igs_qr",
+           "igs_op_basis_diag"]
 
 
 class IgsError(RuntimeError):
@@ -41,7 +42,9 @@ class igs_result(ctypes.Structure):
                 ("want_loo", ctypes.c_int), ("loo_frob", ctypes.c_double), ("iters", ctypes.c_int),
                 ("cycles", ctypes.c_int), ("term", ctypes.c_int), ("true_relres", ctypes.c_double),
                 ("h_cols", ctypes.c_int), ("basis_cols", ctypes.c_int), ("allreduces", ctypes.c_int64),
-                ("reductions", ctypes.c_int64), ("lnorm_hist", ctypes.c_void_p)]
+                ("reductions", ctypes.c_int64), ("lnorm_hist", ctypes.c_void_p),
+                ("want_basis_diag", ctypes.c_int), ("s_norm", ctypes.c_double),
+                ("sigma_min", ctypes.c_double)]
 
 
 _lib = None
@@ -72,6 +75,7 @@ def lib() -> ctypes.CDLL:
             "igs_op_update": [I64, I, P, I64, P, P, P, P, D, P, P, P],
             "igs_op_trisolve": [I, P, I, P, P, P],
             "igs_qr": [I64, I, P, I64, P, I64, P, I, P, P],
+            "igs_op_basis_diag": [I64, I, P, I64, P, P],
             "igs_plan_ghosts": [I64, I64, P, P, I, I, P, P, P, P],
             "igs_plan_remap": [I64, I64, P, P, I, I64, P, P],
         }
@@ -189,6 +193,14 @@ def igs_op_update(n, p, V, ld, u, z, alpha, beta, gamma, v_out, u_next, stream=N
                                _stream_ptr(stream)), "igs_op_update")
 
 
+def igs_op_basis_diag(n, c, V, ld, stream=None):
+    """[||I - V^T V||_F, ||S||_2, sigma_min(V)] of a device block V (n x c, col-major)."""
+    out = np.zeros(3)
+    _check(lib().igs_op_basis_diag(int(n), int(c), _ptr(V), int(ld), out.ctypes.data, _stream_ptr(stream)),
+           "igs_op_basis_diag")
+    return out
+
+
 def igs_qr(n, m, A, lda, Q, ldq, R, sweeps=2, stream=None) -> int:
     """Algorithm 1 QR on the device (device tensors); returns the number of reductions."""
     red = ctypes.c_int64(0)
@@ -269,7 +281,7 @@ class Solver:
 
     def solve(self, b, *, k: int, restart: int = 0, tol: float = 0.0, gs_iters: int = 2,
               x0=None, x_out=None, want_loo: bool = False, want_H: bool = True,
-              algorithm: Optional[str] = None) -> dict:
+              algorithm: Optional[str] = None, want_diag: bool = False) -> dict:
         """b/x0/x_out: torch CUDA tensors (IGS_MEM_DEVICE) or host arrays/tensors
         (IGS_MEM_HOST: the H2D/D2H copies happen inside the call).  algorithm in
         {'igs1','igs2','igs2_two','mgs'} overrides gs_iters (igs_solve_alg)."""
@@ -288,6 +300,7 @@ class Solver:
         res.H = _ptr(H)
         res.res_hist = rh.ctypes.data
         res.want_loo = int(want_loo)
+        res.want_basis_diag = int(want_diag)
         if algorithm is None:
             igs_solve(self.ctx, IGS_MEM_DEVICE if dev else IGS_MEM_HOST, b, x0, k, restart, tol,
                       gs_iters, res)
@@ -297,7 +310,8 @@ class Solver:
         out = dict(x=x_out, iters=res.iters, cycles=res.cycles, term=TERM[res.term],
                    true_relres=res.true_relres, loo=res.loo_frob, h_cols=res.h_cols,
                    basis_cols=res.basis_cols, allreduces=res.allreduces, reductions=res.reductions,
-                   res_hist=rh[:res.iters + 1], lnorm_hist=lh[:res.iters + 1], m=m1)
+                   res_hist=rh[:res.iters + 1], lnorm_hist=lh[:res.iters + 1], m=m1,
+                   s_norm=res.s_norm, sigma_min=res.sigma_min)
         if want_H:
             out["H"] = H.reshape(m1, m1 + 1).T
         return out

@@ -213,3 +213,51 @@ def test_igs_qr_dependent_column_fails_loudly(torch_cuda):
     A[:, 2] = 0.0
     with pytest.raises(P.IgsError):
         _gpu_qr(torch_cuda, A, 2)
+
+
+# ------------------------------------------------------------- basis diagnostics (NEXT-4)
+def _normalized_graded(n, c, kappa, seed):
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((n, c)))
+    Wm, _ = np.linalg.qr(rng.standard_normal((c, c)))
+    V = (U * np.logspace(0, -np.log10(kappa), c)) @ Wm.T
+    return V / np.linalg.norm(V, axis=0)
+
+
+@pytest.mark.parametrize("case", ["orth", "graded", "graded_odd", "repeated", "one", "wide"])
+def test_basis_diag_vs_oracle(torch_cuda, case):
+    """igs_op_basis_diag: [||I - V^T V||_F, ||S||_2, sigma_min(V)] on the same V as the
+    oracle's definitions."""
+    import paper_2205_07805_b200 as P
+    rng = np.random.default_rng(len(case))
+    n = 5003
+    if case == "orth":
+        V, _ = np.linalg.qr(rng.standard_normal((n, 40)))
+    elif case == "graded":
+        V = _normalized_graded(n, 30, 1e3, 1)
+    elif case == "graded_odd":
+        V = _normalized_graded(n, 31, 1e5, 2)
+    elif case == "repeated":
+        Q, _ = np.linalg.qr(rng.standard_normal((n, 12)))
+        V = np.column_stack([Q, Q[:, 3]])
+    elif case == "one":
+        V = rng.standard_normal((n, 1)); V /= np.linalg.norm(V)
+    else:
+        V, _ = np.linalg.qr(rng.standard_normal((n, 257)))
+        V[:, 200] = (V[:, 200] + 1e-3 * V[:, 10]) / np.linalg.norm(V[:, 200] + 1e-3 * V[:, 10])
+    c = V.shape[1]
+    ld = n + 5
+    Vh = np.zeros((c, ld)); Vh[:, :n] = V.T
+    Vd = _dev(torch_cuda, Vh.reshape(-1))
+    loo, s2, smin = P.igs_op_basis_diag(n, c, Vd, ld)
+    lo = oracle.loss_of_orthogonality(V)
+    so = oracle.S_norm(V, c)
+    mo = oracle.sigma_min(V, c)
+    # G = V^T V entries carry ~sqrt(n) eps of reduction-order noise: eps-level values agree
+    # to an absolute 1e-12, larger ones to 1e-10 relative
+    assert abs(loo - lo) <= 1e-10 * lo + 1e-12, (loo, lo)
+    assert abs(s2 - so) <= 1e-10 * so + 1e-12, (s2, so)
+    # sigma_min through the Gram matrix: absolute accuracy ~ c eps / sigma_min (reading R23)
+    assert abs(smin - mo) <= 1e-10 * mo + 64 * c * EPS / max(mo, 1e-8), (smin, mo)
+    if case == "repeated":
+        assert abs(s2 - 1.0) <= 1e-10 and smin <= 1e-7

@@ -536,3 +536,23 @@ def test_fused_block_dot_allreduce_one_rank(P, cfg, alg, monkeypatch):
         assert g["H"].tobytes() == u["H"].tobytes()
         assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
         assert g["allreduces"] == g["reductions"] > 0 and u["allreduces"] == 0
+
+
+def test_basis_diagnostics_simoncini(P):
+    """P:1274-1283 on the device: after 98 iterations on the Simoncini matrix MGS has lost
+    orthogonality (||S_k||_2 -> 1, sigma_min(V) -> 0) while the two-sweep IGS keeps
+    ||S_k||_2 at rounding level; both against the oracle's definitions on its own V."""
+    import torch
+    A, b = W.simoncini(100, 0)
+    s = P.Solver(A)
+    bd = torch.from_numpy(b).cuda()
+    g_mgs = s.solve(bd, k=98, algorithm="mgs", want_diag=True, want_loo=True)
+    g_igs = s.solve(bd, k=98, algorithm="igs2", want_diag=True, want_loo=True)
+    g_one = s.solve(bd, k=30, algorithm="igs2", want_diag=True)
+    s.close()
+    assert g_mgs["s_norm"] >= 0.99 and g_mgs["sigma_min"] <= 1e-3
+    assert g_igs["s_norm"] <= 1e-12 and abs(g_igs["sigma_min"] - 1.0) <= 1e-12
+    o = oracle.gmres(A, b, 98, variant="mgs", want_V=True)
+    c = o["basis_cols"]
+    assert abs(g_mgs["s_norm"] - oracle.S_norm(o["V"], c)) <= 1e-3
+    assert np.isfinite(g_one["s_norm"]) and g_one["s_norm"] <= 1e-13

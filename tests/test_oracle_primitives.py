@@ -182,3 +182,27 @@ def test_igs_qr_step7_reading():
         R_lit[:k - 1, k] /= R[k - 1, k - 1]
     assert np.linalg.norm(A - Q @ R) <= 1e-14 * np.linalg.norm(A)
     assert np.linalg.norm(A - Q @ R_lit) >= 1e-2 * np.linalg.norm(A)
+
+
+# ------------------------------------------------------------- basis diagnostics
+def test_S_norm_closed_forms():
+    # orthonormal basis: S = 0; two columns at angle theta: U = [[0, cos]], S = U, ||S|| = |cos|;
+    # a repeated column (orthogonality lost): ||S||_2 = 1 exactly (Paige)
+    rng = np.random.default_rng(8)
+    Q, _ = np.linalg.qr(rng.standard_normal((40, 6)))
+    assert oracle.S_norm(Q, 6) <= 1e-15
+    th = 0.3
+    V = np.zeros((5, 2)); V[0, 0] = 1.0; V[0, 1] = np.cos(th); V[1, 1] = np.sin(th)
+    assert abs(oracle.S_norm(V, 2) - np.cos(th)) <= 1e-15
+    W = np.column_stack([Q[:, 0], Q[:, 1], Q[:, 0]])
+    assert abs(oracle.S_norm(W, 3) - 1.0) <= 1e-14
+
+
+def test_sigma_min_known_spectrum():
+    rng = np.random.default_rng(9)
+    U, _ = np.linalg.qr(rng.standard_normal((50, 7)))
+    Wm, _ = np.linalg.qr(rng.standard_normal((7, 7)))
+    s = np.array([3.0, 2.0, 1.0, 0.5, 0.1, 1e-3, 2.5])
+    V = (U * s) @ Wm.T
+    assert abs(oracle.sigma_min(V, 7) - 1e-3) <= 1e-14
+    assert abs(oracle.sigma_min(U, 7) - 1.0) <= 1e-14
