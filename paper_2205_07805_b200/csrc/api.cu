@@ -148,6 +148,12 @@ struct igs_ctx {
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
     int64_t n_pcycle = 0;
     unsigned long long* d_pcprof = nullptr;  // IGS_PC_PROF=1 phase timestamps
+    // SELL-32 copy of A (short rows)
+    int64_t* d_sell_ptr = nullptr;
+    uint8_t* d_sell_len = nullptr;
+    double* d_sell_val = nullptr;
+    void* d_sell_col = nullptr;
+    int64_t sell_entries = 0;
     // fused block dot + allreduce over NVLink (IGS_XCHG=1): NCCL symmetric window + device comm
     bool xchg_req = false;
     void* xbuf = nullptr;
@@ -365,6 +371,7 @@ static void free_ctx(igs_ctx* c) {
     if (c->owns_ws) { cudaFree(c->d_V); }
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
     cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter); cudaFree(c->d_pcprof);
+    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col);
     cudaFree(c->d_gram);
     cudaFree(c->d_flags);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -383,6 +390,50 @@ static void free_ctx(igs_ctx* c) {
     cudaFree(c->d_xchg);
     if (c->comm) ncclCommDestroy(c->comm);
     delete c;
+}
+
+// SELL-32 (slices of 32 rows, entries of a slice interleaved by row) from the host CSR.
+static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vector<int64_t>& local_col,
+                             const double* values, bool idx64) {
+    const int64_t n = ctx->n_local, ns = (n + 31) / 32;
+    std::vector<int64_t> sp((size_t)ns + 1, 0);
+    std::vector<uint8_t> len((size_t)n);
+    for (int64_t s = 0; s < ns; s++) {
+        int64_t mx = 0;
+        for (int64_t r = 32 * s; r < std::min<int64_t>(n, 32 * s + 32); r++) {
+            const int64_t l = rowptr[r + 1] - rowptr[r];
+            if (l > 255) return IGS_OK;  // long rows: keep the CSR kernels
+            len[(size_t)r] = (uint8_t)l;
+            mx = std::max(mx, l);
+        }
+        sp[(size_t)s + 1] = sp[(size_t)s] + 32 * mx;
+    }
+    const int64_t tot = std::max<int64_t>(sp[(size_t)ns], 1);
+    std::vector<double> sv((size_t)tot, 0.0);
+    std::vector<char> sc((size_t)tot * (idx64 ? 8 : 4), 0);
+    for (int64_t r = 0; r < n; r++) {
+        const int64_t base = sp[(size_t)(r >> 5)] + (r & 31);
+        for (int64_t q = rowptr[r], k = 0; q < rowptr[r + 1]; q++, k++) {
+            const int64_t at = base + 32 * k;
+            sv[(size_t)at] = values[q];
+            if (idx64) reinterpret_cast<int64_t*>(sc.data())[at] = local_col[(size_t)q];
+            else reinterpret_cast<int32_t*>(sc.data())[at] = (int32_t)local_col[(size_t)q];
+        }
+    }
+    CUDA_TRY(cudaMalloc(&ctx->d_sell_ptr, sizeof(int64_t) * sp.size()));
+    CUDA_TRY(cudaMalloc(&ctx->d_sell_len, len.size()));
+    CUDA_TRY(cudaMalloc(&ctx->d_sell_val, sizeof(double) * sv.size()));
+    CUDA_TRY(cudaMalloc(&ctx->d_sell_col, sc.size()));
+    CUDA_TRY(cudaMemcpy(ctx->d_sell_ptr, sp.data(), sizeof(int64_t) * sp.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->d_sell_len, len.data(), len.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->d_sell_val, sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->d_sell_col, sc.data(), sc.size(), cudaMemcpyHostToDevice));
+    ctx->A.sell_ptr = ctx->d_sell_ptr;
+    ctx->A.sell_len = ctx->d_sell_len;
+    ctx->A.sell_val = ctx->d_sell_val;
+    ctx->A.sell_col = ctx->d_sell_col;
+    ctx->sell_entries = tot;
+    return IGS_OK;
 }
 
 extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_begin,
@@ -515,6 +566,12 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         int lpr = 1;
         while (lpr < 32 && lpr < avg) lpr *= 2;
         ctx->A.lpr = avg <= 8.0 ? 0 : lpr;
+        // SELL-32 copy for short rows (coalesced per-thread rows)
+        const char* es = std::getenv("IGS_SELL");
+        if (ctx->A.lpr == 0 && n_local > 0 && !(es && std::atoi(es) == 0)) {
+            igs_status ss = build_sell(ctx, rowptr, local_col, values, idx64);
+            if (ss != IGS_OK) return fail(ss);
+        }
         // every 256-row tile within the staged-nonzero cap, 32-bit CSR -> fused SpMV + dot
         if (!idx64 && !ptr64) {
             bool ok = true;

@@ -67,6 +67,13 @@ struct SpmvArgs {
     int ptr64, idx64, lpr;
     int64_t nloc;
     const double* ghost;  // NULL when no ghosts
+    // SELL-32 copy of the same matrix (short rows; built by igs_create, IGS_SELL=0 disables):
+    // slice s holds rows 32s..32s+31; entry k of row 32s+l at sell_ptr[s] + 32k + l, in the
+    // CSR order of the row; rows shorter than the slice's longest are padded (never read)
+    const int64_t* sell_ptr = nullptr;  // [nslices + 1]
+    const uint8_t* sell_len = nullptr;  // [nrows] nonzeros of each row (<= 255)
+    const double* sell_val = nullptr;
+    const void* sell_col = nullptr;     // int32 or int64 (idx64), local column space
 };
 // y = A x  (resid: y = b - A x).  istate may be NULL (no status check).
 void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,

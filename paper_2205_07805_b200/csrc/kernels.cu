@@ -150,6 +150,68 @@ __global__ void __launch_bounds__(SPS_THREADS)
     }
 }
 
+// ------------------------------------------------------------------------------------
+// K1 (default for short rows): SELL-32.  One thread per row; the k-th nonzero of the 32
+// rows of a slice are 32 consecutive entries, so the column / value loads of a warp are
+// fully coalesced and, for stencil rows, the x gathers of a warp are one contiguous range
+// per k.  No shared memory, no barrier.  The row is summed left to right in CSR order with
+// separate multiply and add (bitwise equal to the oracle's row loop, like the CSR-stream
+// kernel).  8 entries per batch are loaded before use (memory-level parallelism).
+// ------------------------------------------------------------------------------------
+constexpr int SELL_THREADS = 256;
+
+template <typename IT, bool GHOST, bool RESID>
+__global__ void __launch_bounds__(SELL_THREADS)
+    spmv_sell_kernel(int64_t nrows, const int64_t* __restrict__ sptr, const uint8_t* __restrict__ slen,
+                     const IT* __restrict__ col, const double* __restrict__ val,
+                     const double* __restrict__ x, const double* __restrict__ ghost, int64_t nloc,
+                     double* __restrict__ y, const double* __restrict__ b, const int* istate) {
+    if (!running(istate)) return;
+    const int64_t r = (int64_t)blockIdx.x * SELL_THREADS + threadIdx.x;
+    if (r >= nrows) return;
+    const int len = __ldg(slen + r);
+    const int64_t base = __ldg(sptr + (r >> 5)) + (r & 31);
+    double sum = 0.0;
+    for (int k0 = 0; k0 < len; k0 += 8) {
+        int64_t cc[8];
+        double vv[8], xv[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const bool in = k0 + k < len;
+            cc[k] = in ? (int64_t)__ldg(col + base + 32 * (int64_t)(k0 + k)) : 0;
+            vv[k] = in ? __ldg(val + base + 32 * (int64_t)(k0 + k)) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (k0 + k < len) {
+                if (GHOST && cc[k] >= nloc) xv[k] = __ldg(ghost + (cc[k] - nloc));
+                else xv[k] = __ldg(x + cc[k]);
+            } else {
+                xv[k] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            if (k0 + k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
+    }
+    y[r] = RESID ? b[r] - sum : sum;
+}
+
+template <typename IT>
+static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                      const int* istate, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((a.nrows + SELL_THREADS - 1) / SELL_THREADS);
+    if (blocks == 0) return;
+    const IT* ci = static_cast<const IT*>(a.sell_col);
+    if (a.ghost) {
+        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate);
+        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate);
+    } else {
+        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate);
+        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate);
+    }
+}
+
 template <int R, typename IT, typename PT>
 static void spmv_stream_r(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
                           const int* istate, cudaStream_t s) {
@@ -212,6 +274,11 @@ static void spmv_dispatch_l(const SpmvArgs& a, const double* x, double* y, const
 
 void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
                  const int* istate, cudaStream_t s) {
+    if (a.sell_ptr) {
+        if (a.idx64) spmv_sell<int64_t>(a, x, y, b, resid, istate, s);
+        else spmv_sell<int32_t>(a, x, y, b, resid, istate, s);
+        return;
+    }
     if (a.idx64) {
         if (a.ptr64) spmv_dispatch_l<int64_t, int64_t>(a, x, y, b, resid, istate, s);
         else spmv_dispatch_l<int64_t, int32_t>(a, x, y, b, resid, istate, s);
