@@ -1392,8 +1392,8 @@ extern "C" igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_
     double* part = nullptr;
     unsigned* counter = nullptr;
     CUDA_TRY(cudaMalloc(&part, sizeof(double) * (size_t)grid * 2 * (p + 1)));
-    CUDA_TRY(cudaMalloc(&counter, 2 * sizeof(unsigned)));
-    CUDA_TRY(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned), st));
+    CUDA_TRY(cudaMalloc(&counter, 4 * sizeof(unsigned)));
+    CUDA_TRY(cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned), st));
     CUtensorMap tm;
     const char* etm = std::getenv("IGS_TMAP");
     const bool tmok = etm && std::atoi(etm) != 0 && p > 0 && make_tensor_map(&tm, V, n, p, ld, 256, 8);
@@ -1423,10 +1423,10 @@ extern "C" igs_status igs_qr(int64_t n, int m, const double* A, int64_t lda, dou
     double* ws = nullptr;
     unsigned* counter = nullptr;
     CUDA_TRY(cudaMalloc(&ws, nsd * sizeof(double)));
-    CUDA_TRY(cudaMalloc(&counter, 2 * sizeof(unsigned)));
+    CUDA_TRY(cudaMalloc(&counter, 4 * sizeof(unsigned)));
     struct Free { double* w; unsigned* c; ~Free() { cudaFree(w); cudaFree(c); } } guard{ws, counter};
     CUDA_TRY(cudaMemsetAsync(ws, 0, nsd * sizeof(double), st));
-    CUDA_TRY(cudaMemsetAsync(counter, 0, 2 * sizeof(unsigned), st));
+    CUDA_TRY(cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned), st));
     CUDA_TRY(cudaMemsetAsync(R, 0, sizeof(double) * (size_t)m * m, st));
     QrDev q;
     double* w = ws;

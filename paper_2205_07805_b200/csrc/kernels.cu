@@ -454,7 +454,6 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     uint64_t* empty = full + BT_STAGES;
     uint64_t* uzfull = empty + BT_STAGES;
     uint64_t* uzempty = uzfull + 2;
-    __shared__ bool s_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] = 0.0;
     if (threadIdx.x == 0) {
@@ -575,14 +574,42 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     for (int i = threadIdx.x; i < stride; i += blockDim.x) part[(int64_t)blockIdx.x * stride + i] = acc[i];
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    // stage 2 on the last K CTAs to finish (the grid is co-resident: one CTA per SM), each
+    // summing a contiguous slice of the 2(p+1) outputs in CTA order -- the same order as one
+    // finisher, K times the parallelism (c3, p = 300: 602 outputs x 148 partials)
+    const int G = (int)gridDim.x;
+    const int K = xc ? 1 : min(G, max(1, min(16, stride / 32)));
+    __shared__ unsigned s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(counter, 1u);
     __syncthreads();
-    if (!s_last) return;
+    const int t = (int)s_ticket;
+    if (t < G - K) return;
+    if (K > 1) {
+        if (threadIdx.x == 0) {
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+            } while (v < (unsigned)G);
+        }
+        __syncthreads();
+    }
     __threadfence();
     // [V_p^T u, u.u, V_p^T z, u.z] (+ across ranks over NVLink)
-    if (xc) final_reduce_xchg(part, stride, (int)gridDim.x, out, *xc);
-    else final_reduce(part, stride, (int)gridDim.x, out);
-    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
+    if (xc) final_reduce_xchg(part, stride, G, out, *xc);
+    else {
+        const int f = t - (G - K), per = (stride + K - 1) / K;
+        const int i0 = min(stride, f * per), i1 = min(stride, i0 + per);
+        final_reduce_range(part, stride, G, out, i0, i1);
+    }
+    if (K == 1) {
+        if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
+        return;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // [2]: finishers done; the last one resets the tickets
+        __threadfence();
+        if (atomicAdd(counter + 2, 1u) == (unsigned)(K - 1)) { counter[0] = 0u; counter[2] = 0u; counter[1] += 1u; }
+    }
 }
 
 // ------------------------------------------------------------------------------------

@@ -71,6 +71,18 @@ __device__ __forceinline__ void named_barrier(int id, int nthreads) {
 // done by the last CTA.  Warp w takes outputs w, w+nw, ...; lane l sums partials l, l+32, ...
 // in order, then a fixed xor-shuffle tree -- the same order on every run, and ~nparts/32
 // dependent loads deep instead of nparts.
+__device__ __forceinline__ void final_reduce_range(const double* __restrict__ part, int stride, int nparts,
+                                                   double* out, int i0, int i1) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = i0 + warp; i < i1; i += nw) {
+        double s = 0.0;
+        for (int b = lane; b < nparts; b += 32) s += __ldcg(part + (int64_t)b * stride + i);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) out[i] = s;
+    }
+}
+
 __device__ __forceinline__ void final_reduce(const double* __restrict__ part, int stride, int nparts,
                                              double* out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;

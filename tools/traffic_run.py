@@ -1,6 +1,10 @@
 #!/usr/bin/env python3
-"""One c4 solve of k = 60 iterations (no restart) for ncu: the n-th launch of each
-iteration kernel is iteration p = n (see tools/profile_traffic.sh)."""
+"""One unrestarted Alg. 3 solve for ncu (default c4, k = 60): the n-th launch of each
+iteration kernel is iteration p = n (see tools/profile_traffic_v3.sh for the skip counts).
+
+  python tools/traffic_run.py [--config c4] [--k 60]
+"""
+import argparse
 import os
 import sys
 
@@ -9,12 +13,16 @@ sys.path.insert(0, ROOT)
 
 
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--k", type=int, default=60)
+    a = ap.parse_args()
     import torch
     import paper_2205_07805_b200 as P
     import workloads as W
-    prob = W.config("c4")
+    prob = W.config(a.config)
     s = P.Solver(prob.A)
-    r = s.solve(torch.from_numpy(prob.b).cuda(), k=60, gs_iters=2, want_H=False)
+    r = s.solve(torch.from_numpy(prob.b).cuda(), k=a.k, gs_iters=2, want_H=False)
     print("iters", r["iters"], "relres", r["true_relres"])
     s.close()
 
