@@ -541,12 +541,21 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                     double su = 0.0, sz = 0.0;
                     if (c < p) {
                         const double* col = ring + (size_t)s * BT_STAGE_DOUBLES + warp * BT_ROWS;
+                        if (full_tile) {  // no row mask: ~100 of the ~240 instructions per stage
 #pragma unroll
-                        for (int k = 0; k < BT_RPL; k++) {
-                            double v = col[lane + 32 * k];
-                            if (!full_tile && row0 + lane + 32 * k >= n) v = 0.0;
-                            su = fma(v, ur[k], su);
-                            if (NV == 2) sz = fma(v, zr[k], sz);
+                            for (int k = 0; k < BT_RPL; k++) {
+                                const double v = col[lane + 32 * k];
+                                su = fma(v, ur[k], su);
+                                if (NV == 2) sz = fma(v, zr[k], sz);
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < BT_RPL; k++) {
+                                double v = col[lane + 32 * k];
+                                if (row0 + lane + 32 * k >= n) v = 0.0;
+                                su = fma(v, ur[k], su);
+                                if (NV == 2) sz = fma(v, zr[k], sz);
+                            }
                         }
                     } else {  // column p is u itself
 #pragma unroll
