@@ -173,19 +173,19 @@ __global__ void __launch_bounds__(SELL_THREADS)
     const int64_t base = __ldg(sptr + (r >> 5)) + (r & 31);
     double sum = 0.0;
     for (int k0 = 0; k0 < len; k0 += 8) {
-        int64_t cc[8];
+        IT cc[8];
         double vv[8], xv[8];
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             const bool in = k0 + k < len;
-            cc[k] = in ? (int64_t)__ldg(col + base + 32 * (int64_t)(k0 + k)) : 0;
+            cc[k] = in ? __ldg(col + base + 32 * (int64_t)(k0 + k)) : (IT)0;
             vv[k] = in ? __ldg(val + base + 32 * (int64_t)(k0 + k)) : 0.0;
         }
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             if (k0 + k < len) {
-                if (GHOST && cc[k] >= nloc) xv[k] = __ldg(ghost + (cc[k] - nloc));
-                else xv[k] = __ldg(x + cc[k]);
+                if (GHOST && (int64_t)cc[k] >= nloc) xv[k] = __ldg(ghost + ((int64_t)cc[k] - nloc));
+                else xv[k] = __ldg(x + (int64_t)cc[k]);
             } else {
                 xv[k] = 0.0;
             }
@@ -1049,10 +1049,152 @@ __global__ void __launch_bounds__(UP_THREADS)
     }
 }
 
+// ------------------------------------------------------------------------------------
+// K5 (sm_100a pipeline): the same fused update with V_p streamed by the bulk-copy engine,
+// as in bdot_tma_kernel: persistent CTA per SM = 8 consumer warps + 1 producer warp, 512-row
+// tiles, 8 columns x 512 rows per stage, 6-stage ring.  Consumer warp w owns rows
+// 64w + 2l, 64w + 2l + 1 of the tile (one 16-B shared load per column) and accumulates
+// t1 = V alpha, t2 = V beta over the columns in ascending order -- the same FMA sequence as
+// update_kernel, so the results are bitwise identical; no cross-lane reduction exists.  u
+// and z of the tile are fetched into registers when the tile starts and used in the
+// epilogue.  Opt-in (IGS_UPDATE_TMA=1): in the c4 bench it streams 6.5 TB/s against the
+// register kernel's 6.9 TB/s.
+// ------------------------------------------------------------------------------------
+template <bool HAS_ALPHA>
+__global__ void __launch_bounds__(BT_THREADS, 1)
+    update_tma_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
+                      const double* u, const double* __restrict__ z,
+                      const double* __restrict__ alpha, const double* __restrict__ beta,
+                      const double* __restrict__ gamma_dev, double* v_out, double* u_next,
+                      const int* istate, int it, int default_mode, const double* __restrict__ zdiv_dev) {
+    int mode = default_mode;
+    if (istate) {
+        const volatile int* vs = istate;
+        mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
+        mode &= default_mode;
+    }
+    if (mode == 0) return;
+    const bool want_next = (mode & 2) != 0;
+    extern __shared__ __align__(128) double smem_ut[];
+    double* ring = smem_ut;                                  // [STAGES][8][512]
+    double* sa = ring + BT_STAGES * BT_STAGE_DOUBLES;        // alpha [p]
+    double* sb = sa + ((p + 1) & ~1);                        // beta [p+1]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + ((p + 2) & ~1));
+    uint64_t* empty = full + BT_STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (HAS_ALPHA)
+        for (int j = threadIdx.x; j < p; j += blockDim.x) sa[j] = alpha[j];
+    if (want_next)
+        for (int j = threadIdx.x; j <= p; j += blockDim.x) sb[j] = beta[j];
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < BT_STAGES; st++) { mbar_init(full + st, 1); mbar_init(empty + st, BT_CONS_WARPS); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
+    const int ngroups = (p + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
+    const int64_t nk = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (warp == BT_CONS_WARPS) {
+        if (lane == 0) {
+            uint32_t itg = 0;
+            for (int64_t k = 0; k < nk; k++) {
+                const int64_t row0 = (blockIdx.x + k * gridDim.x) * BT_ROWS;
+                const int64_t rows = (n - row0 < BT_ROWS) ? n - row0 : BT_ROWS;
+                const uint32_t bytes = (uint32_t)(((rows + 1) & ~1LL) * sizeof(double));
+                for (int g = 0; g < ngroups; g++, itg++) {
+                    const int st = itg % BT_STAGES;
+                    mbar_wait(empty + st, ((itg / BT_STAGES) & 1) ^ 1);
+                    const int c0 = g * BT_CONS_WARPS;
+                    const int nc = min(BT_CONS_WARPS, p - c0);
+                    mbar_arrive_expect_tx(full + st, (uint32_t)nc * bytes);
+                    for (int c = 0; c < nc; c++)
+                        bulk_g2s(ring + (size_t)st * BT_STAGE_DOUBLES + c * BT_ROWS,
+                                 V + (int64_t)(c0 + c) * ld + row0, bytes, full + st);
+                }
+            }
+        }
+        return;
+    }
+    const double gamma = *gamma_dev;
+    const double zdiv = zdiv_dev ? *zdiv_dev : gamma;
+    const int rl = 64 * warp + 2 * lane;  // this lane's two rows within the tile
+    uint32_t itg = 0;
+    for (int64_t kt = 0; kt < nk; kt++) {
+        const int64_t row0 = (blockIdx.x + kt * gridDim.x) * BT_ROWS;
+        const int64_t r = row0 + rl;
+        const bool pair = r + 1 < n;
+        // epilogue operands, in flight while the tile streams
+        const double2 uu = ld2_guard(u, r, n);
+        const double2 zz = want_next ? ld2_guard(z, r, n) : make_double2(0.0, 0.0);
+        double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
+        for (int g = 0; g < ngroups; g++, itg++) {
+            const int st = itg % BT_STAGES;
+            mbar_wait(full + st, (itg / BT_STAGES) & 1);
+            const int c0 = g * BT_CONS_WARPS;
+            const int nc = min(BT_CONS_WARPS, p - c0);
+            const double* stg = ring + (size_t)st * BT_STAGE_DOUBLES + rl;
+#pragma unroll
+            for (int c = 0; c < BT_CONS_WARPS; c++) {
+                if (c < nc) {
+                    const double2 v = *reinterpret_cast<const double2*>(stg + c * BT_ROWS);
+                    if (HAS_ALPHA) { t1.x = fma(v.x, sa[c0 + c], t1.x); t1.y = fma(v.y, sa[c0 + c], t1.y); }
+                    if (want_next) { t2.x = fma(v.x, sb[c0 + c], t2.x); t2.y = fma(v.y, sb[c0 + c], t2.y); }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + st);
+        }
+        if (r < n) {
+            double2 w = uu;
+            if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
+            double2 v;
+            v.x = w.x / gamma;
+            v.y = w.y / gamma;
+            if (want_next) {
+                const double bp = sb[p];
+                u_next[r] = zz.x / zdiv - fma(v.x, bp, t2.x);
+                if (pair) u_next[r + 1] = zz.y / zdiv - fma(v.y, bp, t2.y);
+            }
+            if (mode & 1) {
+                v_out[r] = v.x;
+                if (pair) v_out[r + 1] = v.y;
+            }
+        }
+    }
+}
+
+static size_t update_tma_smem(int p) {
+    return (size_t)(BT_STAGES * BT_STAGE_DOUBLES + ((p + 1) & ~1) + ((p + 2) & ~1)) * sizeof(double) +
+           2 * BT_STAGES * sizeof(uint64_t);
+}
+
 void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
                    const double* z, const double* alpha, const double* beta,
                    const double* gamma_dev, double* v_out, double* u_next, const int* istate,
                    int it, cudaStream_t s, const double* zdiv_dev) {
+    static int tma = -1;  // IGS_UPDATE_TMA=1: bulk-copy variant (measured slower in the bench:
+    if (tma < 0) {        // 113 vs 106 ms per c4 step)
+        const char* e = getenv("IGS_UPDATE_TMA");
+        tma = (e && atoi(e) == 1) ? 1 : 0;
+    }
+    const size_t usmem = update_tma_smem(p);
+    if (tma && p >= BT_CONS_WARPS && n >= BT_ROWS && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 &&
+        ((uintptr_t)u % 16) == 0 && (!z || ((uintptr_t)z % 16) == 0) && usmem <= 227 * 1024) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
+        const int tg = (int)(ntiles < sms ? ntiles : sms);
+        const int dmode = 1 | (u_next ? 2 : 0);
+        if (alpha) {
+            cudaFuncSetAttribute(update_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
+            update_tma_kernel<true><<<tg, BT_THREADS, usmem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
+        } else {
+            cudaFuncSetAttribute(update_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
+            update_tma_kernel<false><<<tg, BT_THREADS, usmem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
+        }
+        return;
+    }
     const int64_t nthreads = (n + 1) / 2;
     const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
     if (blocks == 0) return;
