@@ -170,10 +170,25 @@ def run_reference(args, rank, world):
             "data": "synthetic (seeded generators, workloads/)",
             "config": bench_config(args.gs, world),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
-                             "gbs": gbs},
+                             "gbs": gbs, **host_cpu()},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def host_cpu() -> dict:
+    """Model name and socket count of the host the oracle runs on (/proc/cpuinfo)."""
+    model, sockets = None, set()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name") and model is None:
+                    model = line.split(":", 1)[1].strip()
+                elif line.startswith("physical id"):
+                    sockets.add(line.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    return {"cpu_model": model, "sockets": len(sockets) or None, "nproc": os.cpu_count()}
 
 
 def cpu_baseline_ours(prob, seconds_cap=40.0):
@@ -193,7 +208,7 @@ def cpu_baseline_ours(prob, seconds_cap=40.0):
             "sample": (f"first {CPU_SAMPLE_ITERS} iterations of one c4 GMRES(100) cycle (Alg. 3, "
                        f"blocked FP64 dots), {t:.1f} s wall; projected to the cycle-average "
                        f"iteration by the byte model ({CPU_SAMPLE_ITERS / t:.3f} it/s raw, {gbs:.1f} GB/s)"),
-            "gbs": gbs}
+            "gbs": gbs, **host_cpu()}
 
 
 def main():
@@ -257,16 +272,19 @@ def main():
     solver.set_timing(2)
     barrier()
     clocks.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    e0, e1 = ev[0], ev[-1]
     e0.record(stream)
     iters = 0
-    for _ in range(args.steps):
+    for i in range(args.steps):
         iters += step_dev()["iters"]
-    e1.record(stream)
+        ev[i + 1].record(stream)
     e1.synchronize()
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1))
+    step_ms = sorted(ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps))
+    ms_median = max_over_ranks(step_ms[len(step_ms) // 2])
     ks = solver.kernel_stats()
     solver.set_timing(0)
     value = iters / (ms / 1e3)
@@ -323,7 +341,8 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "ms_per_step_median": ms_median,
+            "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generators, workloads/)",
             "config": bench_config(args.gs, world),
