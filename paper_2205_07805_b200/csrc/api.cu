@@ -156,6 +156,7 @@ struct igs_ctx {
     int64_t sell_entries = 0;
     // fused block dot + allreduce over NVLink (IGS_XCHG=1): NCCL symmetric window + device comm
     bool xchg_req = false;
+    bool force_nccl = false;  // IGS_FORCE_NCCL=1: a 1-rank communicator and real ncclAllReduce calls
     void* xbuf = nullptr;
     ncclWindow_t xwin = nullptr;
     ncclDevComm dcomm{};
@@ -498,7 +499,8 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
 
     auto fail = [&](igs_status s) { free_ctx(ctx); return s; };
     if (const char* e = std::getenv("IGS_XCHG")) ctx->xchg_req = std::atoi(e) != 0;
-    if (nranks > 1 || ctx->xchg_req) {
+    if (const char* e = std::getenv("IGS_FORCE_NCCL")) ctx->force_nccl = nranks == 1 && std::atoi(e) != 0;
+    if (nranks > 1 || ctx->xchg_req || ctx->force_nccl) {
         // (one rank + IGS_XCHG=1: a 1-rank communicator, so the fused exchange path runs on
         //  a single GPU exactly as it does on G)
         ncclUniqueId id;
@@ -803,7 +805,7 @@ static double spmv_bytes(const igs_ctx* c) {
 }
 
 static igs_status allreduce(igs_ctx* ctx, double* buf, int64_t count) {
-    if (ctx->nranks == 1) return IGS_OK;
+    if (ctx->nranks == 1 && !ctx->force_nccl) return IGS_OK;
     TIMED(IGS_K_ALLREDUCE, 0.0,
           { NCCL_TRY(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm, ctx->stream)); });
     ctx->n_allreduce++;
@@ -875,7 +877,7 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0);
 // alg: IGS_ALG_IGS1 (1), IGS_ALG_IGS2 (2, Alg. 3), IGS_ALG_IGS2_TWO (3, Alg. 2 literal),
 // IGS_ALG_MGS (4).  Algorithms 1 and 3 share the gs = 1 small-step stages.
 static bool use_pcycle(const igs_ctx* ctx, int alg) {
-    return ctx->pc_enabled && ctx->nranks == 1 && !ctx->xchg_req && ctx->n_local <= ctx->pc_max_n && !ctx->fused_enabled &&
+    return ctx->pc_enabled && ctx->nranks == 1 && !ctx->xchg_req && !ctx->force_nccl && ctx->n_local <= ctx->pc_max_n && !ctx->fused_enabled &&
            (alg == IGS_ALG_IGS1 || alg == IGS_ALG_IGS2) && ctx->dev_state.m <= 1024;
 }
 
@@ -1104,7 +1106,8 @@ static igs_status launch_cycle(igs_ctx* ctx, int m, int alg, int t0) {
     ctx->h_pinned[40] = (double)t0;
     CUDA_TRY(cudaMemcpyAsync(ctx->dev_state.scal + SC_T0, ctx->h_pinned + 40, sizeof(double),
                              cudaMemcpyHostToDevice, st));
-    const bool use_graph = ctx->graphs_enabled && !ctx->timing && ctx->nranks == 1 && !use_pcycle(ctx, alg) &&
+    const bool use_graph = ctx->graphs_enabled && !ctx->timing && ctx->nranks == 1 && !ctx->force_nccl &&
+                           !use_pcycle(ctx, alg) &&
                            ctx->n_local <= ((int64_t)1 << 21) && !ctx->fused_enabled &&
                            alg != IGS_ALG_MGS && m <= 512;  // MGS: O(m^2) nodes
     if (!use_graph) return run_cycle(ctx, m, alg, t0);

@@ -556,3 +556,25 @@ def test_basis_diagnostics_simoncini(P):
     c = o["basis_cols"]
     assert abs(g_mgs["s_norm"] - oracle.S_norm(o["V"], c)) <= 1e-3
     assert np.isfinite(g_one["s_norm"]) and g_one["s_norm"] <= 1e-13
+
+
+@pytest.mark.parametrize("alg", ["igs2", "igs1", "igs2_two", "mgs"])
+def test_nccl_allreduce_path_one_rank(P, alg, monkeypatch):
+    """IGS_FORCE_NCCL=1: the multi-GPU code path's ncclAllReduce after every block dot runs on a
+    1-rank communicator (the pool has one GPU): same bits as the single-GPU path, and exactly
+    one allreduce per global reduction (the paper's synchronization count)."""
+    import torch
+    prob = W.config("c3", N=48)
+    b = torch.from_numpy(prob.b).cuda()
+    k, restart = (60, 25) if alg != "mgs" else (30, 15)
+    outs = {}
+    for f in ("1", "0"):
+        monkeypatch.setenv("IGS_FORCE_NCCL", f)
+        monkeypatch.setenv("IGS_PERSIST", "0")
+        s = P.Solver(prob.A)
+        outs[f] = s.solve(b, k=k, restart=restart, tol=1e-10, algorithm=alg)
+        s.close()
+    g, u = outs["1"], outs["0"]
+    assert g["iters"] == u["iters"] and g["H"].tobytes() == u["H"].tobytes()
+    assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+    assert g["allreduces"] == g["reductions"] > 0 and u["allreduces"] == 0
