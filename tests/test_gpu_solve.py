@@ -578,3 +578,26 @@ def test_nccl_allreduce_path_one_rank(P, alg, monkeypatch):
     assert g["iters"] == u["iters"] and g["H"].tobytes() == u["H"].tobytes()
     assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
     assert g["allreduces"] == g["reductions"] > 0 and u["allreduces"] == 0
+
+
+def test_bound_workspace(P):
+    """igs_workspace_bytes / igs_bind_workspace: V lives in a torch-owned buffer; same bits as
+    the library-allocated workspace; a too-small buffer is a status code, not a crash."""
+    import torch
+    prob = W.config("c3", N=64)
+    b = torch.from_numpy(prob.b).cuda()
+    ref = P.Solver(prob.A)
+    r0 = ref.solve(b, k=50, restart=20, tol=1e-10, gs_iters=2)
+    ref.close()
+    s = P.Solver(prob.A)
+    nbytes = P.igs_workspace_bytes(s.ctx, 20)
+    assert nbytes >= 21 * prob.A.n_rows * 8
+    buf = torch.empty(nbytes + 256, dtype=torch.uint8, device="cuda")
+    ptr = (buf.data_ptr() + 255) // 256 * 256
+    P.igs_bind_workspace(s.ctx, ptr, nbytes)
+    r1 = s.solve(b, k=50, restart=20, tol=1e-10, gs_iters=2)
+    assert r1["iters"] == r0["iters"] and r1["H"].tobytes() == r0["H"].tobytes()
+    assert r1["x"].cpu().numpy().tobytes() == r0["x"].cpu().numpy().tobytes()
+    with pytest.raises(P.IgsError):
+        s.solve(b, k=60, restart=40, tol=1e-10, gs_iters=2)   # needs a 41-column V
+    s.close()
