@@ -138,7 +138,8 @@ typedef struct {
                               Gram factor after iteration t (the paper's loss-of-orthogonality
                               predictor, dep^2(I+L) = ||L||_F^2); lnorm_hist[0]=0;
                               entries restart at each cycle; NaN for MGS (no L)               */
-    int want_basis_diag;   /* in: compute s_norm and sigma_min of the final basis             */
+    int want_basis_diag;   /* in: compute s_norm and sigma_min of the final basis (NaN when it
+                              has more than IGS_BASIS_DIAG_MAX columns)                       */
     double s_norm;         /* out: ||S||_2, S = (I + U)^{-1} U, U = strictly upper part of
                               V^T V (Paige's S; 1 when orthogonality is lost); NaN
                               if !want_basis_diag                                             */
@@ -216,7 +217,11 @@ igs_status igs_op_update(int64_t n, int p, const double* V, int64_t ld, const do
 igs_status igs_qr(int64_t n, int m, const double* A, int64_t lda, double* Q, int64_t ldq, double* R,
                   int sweeps, int64_t* reductions, void* cuda_stream);
 
-/* Basis diagnostics of a device block V (n x c, col-major, ld >= n; c <= 4096):
+/* Largest basis the on-device ||S||_2 / sigma_min diagnostics accept (cyclic Jacobi on one
+ * CTA is O(c^3) per sweep); igs_solve reports NaN for larger bases. */
+#define IGS_BASIS_DIAG_MAX 1024
+
+/* Basis diagnostics of a device block V (n x c, col-major, ld >= n; c <= IGS_BASIS_DIAG_MAX):
  * out3 (host) = [||I - V^T V||_F, ||S||_2, sigma_min(V)].  Same kernels
  * as igs_solve's want_loo / want_basis_diag.  Synchronises cuda_stream. */
 igs_status igs_op_basis_diag(int64_t n, int c, const double* V, int64_t ld, double* out3, void* cuda_stream);

@@ -1311,7 +1311,7 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         double loo = 0.0;
         TRY(fetch(ctx, G + (size_t)c * c, 1, &loo, nullptr, 0, nullptr));
         if (res->want_loo) res->loo_frob = loo;
-        if (res->want_basis_diag) {
+        if (res->want_basis_diag && c <= IGS_BASIS_DIAG_MAX) {  // larger bases: NaN (one-CTA Jacobi)
             double* ws = nullptr;
             CUDA_TRY(cudaMalloc(&ws, sizeof(double) * (basis_diag_doubles(c) + 2)));
             TIMED(IGS_K_CYCLE, 0.0, launch_basis_diag(c, G, ws, ws + basis_diag_doubles(c), st));
@@ -1498,7 +1498,7 @@ extern "C" igs_status igs_qr(int64_t n, int m, const double* A, int64_t lda, dou
 
 extern "C" igs_status igs_op_basis_diag(int64_t n, int c, const double* V, int64_t ld, double* out3,
                                         void* cuda_stream) {
-    ARG_CHECK(n >= 1 && c >= 1 && c <= 4096 && ld >= n && V && out3, "igs_op_basis_diag: bad argument");
+    ARG_CHECK(n >= 1 && c >= 1 && c <= IGS_BASIS_DIAG_MAX && ld >= n && V && out3, "igs_op_basis_diag: bad argument");
     TRY(have_device());
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 4096));
