@@ -498,6 +498,9 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
 
     auto fail = [&](igs_status s) { free_ctx(ctx); return s; };
+    // the fused block dot + NVLink exchange is the G > 1 default (IGS_XCHG=0: a separate
+    // ncclAllReduce after each block dot; IGS_XCHG=1 also on one GPU, via a 1-rank comm)
+    ctx->xchg_req = nranks > 1;
     if (const char* e = std::getenv("IGS_XCHG")) ctx->xchg_req = std::atoi(e) != 0;
     if (const char* e = std::getenv("IGS_FORCE_NCCL")) ctx->force_nccl = nranks == 1 && std::atoi(e) != 0;
     if (nranks > 1 || ctx->xchg_req || ctx->force_nccl) {
@@ -840,11 +843,16 @@ static igs_status bdot(igs_ctx* ctx, int p, const double* u, const double* z, do
                        const int* istate, int kind) {
     const double by = 8.0 * ctx->n_local * (p + 1 + (z ? 1 : 0));
     if (ctx->d_xchg) {
-        // block dot with the cross-rank sum fused in; it never skips on the status word
-        // (a rank that skipped would leave its peers waiting at the LSA barrier)
+        // block dot with the cross-rank sum fused in.  Every rank must take the same skip
+        // decision (a rank that skipped would leave its peers at the LSA barrier), so the
+        // status word it reads must be final: join the side-stream tail of the previous
+        // iteration first (it had the update and the SpMV to finish).  Outside graphs only;
+        // graphs are single-rank.
+        if (istate && !ctx->capturing) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_tail, 0));
         TIMED(kind, by,
               launch_block_dot(ctx->n_local, p, ctx->d_V, ctx->ldv, u, z, out, ctx->d_part,
-                               ctx->d_counter, ctx->bdot_grid, nullptr, ctx->stream, nullptr, ctx->d_xchg));
+                               ctx->d_counter, ctx->bdot_grid, ctx->capturing ? nullptr : istate, ctx->stream,
+                               nullptr, ctx->d_xchg));
         ctx->n_allreduce++;
         ctx->n_reduce++;
         return IGS_OK;

@@ -535,7 +535,9 @@ def test_fused_block_dot_allreduce_one_rank(P, cfg, alg, monkeypatch):
         assert g["iters"] == u["iters"] and g["term"] == u["term"] and g["cycles"] == u["cycles"]
         assert g["H"].tobytes() == u["H"].tobytes()
         assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
-        assert g["allreduces"] == g["reductions"] > 0 and u["allreduces"] == 0
+        # every issued exchange that ran is a reduction; after a stop the block dots (and
+        # their exchange, uniformly on all ranks) are skipped
+        assert 0 < g["reductions"] <= g["allreduces"] and u["allreduces"] == 0
 
 
 def test_basis_diagnostics_simoncini(P):
