@@ -1590,19 +1590,34 @@ __device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double
     if (gs == 1 || nonfinite || bd || conv || drain) return;
     // Step 15, derived (reading R1): hp[:p+1, p] = r1 - H[:p+1, :p] (r2 / gamma); H is upper
     // Hessenberg, so row i only meets columns j >= i-1 (the skipped terms are exact zeros)
+    // Each row's columns are split into S contiguous chunks (S threads per row, up to 3:
+    // the thread count exceeds p + 1), partial sums combined in chunk order -- the longest
+    // dependent load chain drops from p/8 to p/(8S) L2 round trips.
     for (int j = tid; j < p; j += blockDim.x) s_t[j] = __ldcg(d.L + p + (int64_t)j * M);
+    const int rows = p + 1;
+    const int S = max(1, min(3, (int)blockDim.x / rows));
+    double* s_part = s_col;  // s_col | s_cs | s_sn: 3M + 4 >= S (p + 1) doubles, free after Givens
     __syncthreads();
-    for (int i = tid; i <= p; i += blockDim.x) {
+    for (int w = tid; w < rows * S; w += blockDim.x) {
+        const int i = w % rows, sidx = w / rows;
+        const int j0 = i > 0 ? i - 1 : 0, len = p - j0;
+        int j = j0 + len * sidx / S;
+        const int e = j0 + len * (sidx + 1) / S;
         double sacc = 0.0;
-        int j = i > 0 ? i - 1 : 0;
-        for (; j + 8 <= p; j += 8) {
+        for (; j + 8 <= e; j += 8) {
             double hv[8];
 #pragma unroll
             for (int c = 0; c < 8; c++) hv[c] = __ldcg(d.H + i + (int64_t)(j + c) * d.ldh);
 #pragma unroll
             for (int c = 0; c < 8; c++) sacc += hv[c] * s_t[j + c];
         }
-        for (; j < p; j++) sacc += __ldcg(d.H + i + (int64_t)j * d.ldh) * s_t[j];
+        for (; j < e; j++) sacc += __ldcg(d.H + i + (int64_t)j * d.ldh) * s_t[j];
+        s_part[sidx * rows + i] = sacc;
+    }
+    __syncthreads();
+    for (int i = tid; i < rows; i += blockDim.x) {
+        double sacc = s_part[i];
+        for (int k = 1; k < S; k++) sacc += s_part[k * rows + i];
         d.HP[i + (int64_t)p * d.ldh] = __ldcg(d.r1h + (int64_t)p * (M + 2) + i) - sacc;
     }
 }
