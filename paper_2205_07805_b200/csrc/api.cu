@@ -154,6 +154,10 @@ struct igs_ctx {
     double* d_sell_val = nullptr;
     void* d_sell_col = nullptr;
     int64_t sell_entries = 0;
+    // G > 1 with SELL: rows touching ghost columns run after the halo, the rest during it
+    int64_t* d_bnd_rows = nullptr;
+    cudaStream_t hstream = nullptr;  // halo exchange stream
+    cudaEvent_t ev_x = nullptr, ev_h = nullptr;
     // fused block dot + allreduce over NVLink (IGS_XCHG=1): NCCL symmetric window + device comm
     bool xchg_req = false;
     bool force_nccl = false;  // IGS_FORCE_NCCL=1: a 1-rank communicator and real ncclAllReduce calls
@@ -373,6 +377,10 @@ static void free_ctx(igs_ctx* c) {
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
     cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter); cudaFree(c->d_pcprof);
     cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col);
+    cudaFree(c->d_bnd_rows);
+    if (c->hstream) cudaStreamDestroy(c->hstream);
+    if (c->ev_x) cudaEventDestroy(c->ev_x);
+    if (c->ev_h) cudaEventDestroy(c->ev_h);
     cudaFree(c->d_gram);
     cudaFree(c->d_flags);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
@@ -399,11 +407,25 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     const int64_t n = ctx->n_local, ns = (n + 31) / 32;
     std::vector<int64_t> sp((size_t)ns + 1, 0);
     std::vector<uint8_t> len((size_t)n);
+    // G > 1: rows that touch a ghost column are left to the boundary pass (row-list kernel,
+    // after the halo); the SELL pass runs while the halo is in flight and skips them
+    // (row length SELL_BOUNDARY, no entries stored)
+    std::vector<int64_t> bnd;
+    for (int64_t r = 0; r < n && ctx->n_ghost > 0; r++)
+        for (int64_t q = rowptr[r]; q < rowptr[r + 1]; q++)
+            if (local_col[(size_t)q] >= n) { bnd.push_back(r); break; }
+    // test hook (one GPU): IGS_TEST_BND_EVERY=k routes every k-th row through the boundary
+    // pass, so the split interior / boundary SpMV of G > 1 is checked on a single device
+    if (const char* e = std::getenv("IGS_TEST_BND_EVERY"))
+        if (ctx->nranks == 1 && std::atoi(e) > 0)
+            for (int64_t r = 0; r < n; r += std::atoi(e)) bnd.push_back(r);
+    size_t bi = 0;
     for (int64_t s = 0; s < ns; s++) {
         int64_t mx = 0;
         for (int64_t r = 32 * s; r < std::min<int64_t>(n, 32 * s + 32); r++) {
+            if (bi < bnd.size() && bnd[bi] == r) { len[(size_t)r] = SELL_BOUNDARY; bi++; continue; }
             const int64_t l = rowptr[r + 1] - rowptr[r];
-            if (l > 255) return IGS_OK;  // long rows: keep the CSR kernels
+            if (l >= SELL_BOUNDARY) return IGS_OK;  // long rows: keep the CSR kernels
             len[(size_t)r] = (uint8_t)l;
             mx = std::max(mx, l);
         }
@@ -413,6 +435,7 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     std::vector<double> sv((size_t)tot, 0.0);
     std::vector<char> sc((size_t)tot * (idx64 ? 8 : 4), 0);
     for (int64_t r = 0; r < n; r++) {
+        if (len[(size_t)r] == SELL_BOUNDARY) continue;
         const int64_t base = sp[(size_t)(r >> 5)] + (r & 31);
         for (int64_t q = rowptr[r], k = 0; q < rowptr[r + 1]; q++, k++) {
             const int64_t at = base + 32 * k;
@@ -434,6 +457,15 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     ctx->A.sell_val = ctx->d_sell_val;
     ctx->A.sell_col = ctx->d_sell_col;
     ctx->sell_entries = tot;
+    if (!bnd.empty()) {
+        CUDA_TRY(cudaMalloc(&ctx->d_bnd_rows, sizeof(int64_t) * bnd.size()));
+        CUDA_TRY(cudaMemcpy(ctx->d_bnd_rows, bnd.data(), sizeof(int64_t) * bnd.size(), cudaMemcpyHostToDevice));
+        ctx->A.bnd_rows = ctx->d_bnd_rows;
+        ctx->A.n_bnd = (int64_t)bnd.size();
+        CUDA_TRY(cudaStreamCreateWithFlags(&ctx->hstream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_h, cudaEventDisableTiming));
+    }
     return IGS_OK;
 }
 
@@ -815,27 +847,45 @@ static igs_status allreduce(igs_ctx* ctx, double* buf, int64_t count) {
     return IGS_OK;
 }
 
-static igs_status halo(igs_ctx* ctx, const double* x, const int* istate) {
-    if (ctx->nranks == 1 || ctx->peers.empty()) return IGS_OK;
-    TIMED(IGS_K_HALO, 16.0 * ctx->n_send + 8.0 * ctx->n_ghost, {
-        launch_pack(ctx->n_send, ctx->d_send_idx, x, ctx->d_send, istate, ctx->stream);
-        NCCL_TRY(ncclGroupStart());
-        for (size_t i = 0; i < ctx->peers.size(); i++) {
-            if (ctx->send_cnt[i]) NCCL_TRY(ncclSend(ctx->d_send + ctx->send_off[i], ctx->send_cnt[i], ncclDouble, ctx->peers[i], ctx->comm, ctx->stream));
-            if (ctx->recv_cnt[i]) NCCL_TRY(ncclRecv(ctx->d_ghost + ctx->recv_off[i], ctx->recv_cnt[i], ncclDouble, ctx->peers[i], ctx->comm, ctx->stream));
-        }
-        NCCL_TRY(ncclGroupEnd());
-    });
+static igs_status halo_on(igs_ctx* ctx, const double* x, const int* istate, cudaStream_t st) {
+    launch_pack(ctx->n_send, ctx->d_send_idx, x, ctx->d_send, istate, st);
+    NCCL_TRY(ncclGroupStart());
+    for (size_t i = 0; i < ctx->peers.size(); i++) {
+        if (ctx->send_cnt[i]) NCCL_TRY(ncclSend(ctx->d_send + ctx->send_off[i], ctx->send_cnt[i], ncclDouble, ctx->peers[i], ctx->comm, st));
+        if (ctx->recv_cnt[i]) NCCL_TRY(ncclRecv(ctx->d_ghost + ctx->recv_off[i], ctx->recv_cnt[i], ncclDouble, ctx->peers[i], ctx->comm, st));
+    }
+    NCCL_TRY(ncclGroupEnd());
     ctx->n_halo += (int64_t)ctx->peers.size();
     return IGS_OK;
 }
 
-// z = A x (with halo) ; resid: y = b - A x
+static igs_status halo(igs_ctx* ctx, const double* x, const int* istate) {
+    if (ctx->nranks == 1 || ctx->peers.empty()) return IGS_OK;
+    TIMED(IGS_K_HALO, 16.0 * ctx->n_send + 8.0 * ctx->n_ghost, { TRY(halo_on(ctx, x, istate, ctx->stream)); });
+    return IGS_OK;
+}
+
+// z = A x (with halo) ; resid: y = b - A x.  G > 1 with SELL: the halo runs on its own
+// stream while the interior rows (no ghost column) are multiplied; the boundary rows follow
+// once the ghosts have arrived (halo overlapped with the interior SpMV).
 static igs_status spmv(igs_ctx* ctx, const double* x, double* y, const double* b, bool resid,
                        const int* istate, int kind) {
+    const double by = spmv_bytes(ctx) + (resid ? 8.0 * ctx->n_local : 0.0);
+    if (ctx->A.n_bnd > 0 && ctx->hstream) {
+        CUDA_TRY(cudaEventRecord(ctx->ev_x, ctx->stream));
+        CUDA_TRY(cudaStreamWaitEvent(ctx->hstream, ctx->ev_x, 0));
+        if (!ctx->peers.empty()) TRY(halo_on(ctx, x, istate, ctx->hstream));
+        CUDA_TRY(cudaEventRecord(ctx->ev_h, ctx->hstream));
+        TIMED(kind, by, {
+            launch_spmv(ctx->A, x, y, b, resid, istate, ctx->stream);            // interior rows
+            cudaError_t e_ = cudaStreamWaitEvent(ctx->stream, ctx->ev_h, 0);
+            CUDA_TRY(e_);
+            launch_spmv_rows(ctx->A, x, y, b, resid, istate, ctx->stream);       // boundary rows
+        });
+        return IGS_OK;
+    }
     TRY(halo(ctx, x, istate));
-    TIMED(kind, spmv_bytes(ctx) + (resid ? 8.0 * ctx->n_local : 0.0),
-          launch_spmv(ctx->A, x, y, b, resid, istate, ctx->stream));
+    TIMED(kind, by, launch_spmv(ctx->A, x, y, b, resid, istate, ctx->stream));
     return IGS_OK;
 }
 
@@ -1533,6 +1583,7 @@ extern "C" igs_status igs_op_spmv(igs_ctx* ctx, const double* x, double* y) {
     ARG_CHECK(ctx->nranks == 1, "igs_op_spmv: single-rank contexts only");
     CUDA_TRY(cudaSetDevice(ctx->dev));
     launch_spmv(ctx->A, x, y, nullptr, false, nullptr, ctx->stream);
+    if (ctx->A.n_bnd > 0) launch_spmv_rows(ctx->A, x, y, nullptr, false, nullptr, ctx->stream);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     return IGS_OK;

@@ -74,7 +74,15 @@ struct SpmvArgs {
     const uint8_t* sell_len = nullptr;  // [nrows] nonzeros of each row (<= 255)
     const double* sell_val = nullptr;
     const void* sell_col = nullptr;     // int32 or int64 (idx64), local column space
+    // G > 1: rows with a ghost column (sell_len == SELL_BOUNDARY, not in the SELL arrays),
+    // multiplied from the CSR arrays by launch_spmv_rows once the halo has arrived
+    const int64_t* bnd_rows = nullptr;
+    int64_t n_bnd = 0;
 };
+constexpr uint8_t SELL_BOUNDARY = 255;
+// y[r] = (b[r] -) A[r,:] x for the rows in a.bnd_rows (CSR arrays, ghosts), left-to-right
+void launch_spmv_rows(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                      const int* istate, cudaStream_t s);
 // y = A x  (resid: y = b - A x).  istate may be NULL (no status check).
 void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
                  const int* istate, cudaStream_t s);

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(SELL_THREADS)
     const int64_t r = (int64_t)blockIdx.x * SELL_THREADS + threadIdx.x;
     if (r >= nrows) return;
     const int len = __ldg(slen + r);
+    if (len == SELL_BOUNDARY) return;  // G > 1 boundary row: launch_spmv_rows, after the halo
     const int64_t base = __ldg(sptr + (r >> 5)) + (r & 31);
     double sum = 0.0;
     for (int k0 = 0; k0 < len; k0 += 8) {
@@ -209,6 +210,50 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
     } else {
         if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate);
         else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate);
+    }
+}
+
+// Boundary rows (G > 1): one thread per listed row, CSR arrays, ghosts for columns >= nloc,
+// separate multiply and add left to right (the same rounding as the SELL / CSR kernels).
+template <typename IT, typename PT, bool RESID>
+__global__ void __launch_bounds__(256)
+    spmv_rows_kernel(int64_t nb, const int64_t* __restrict__ rows, const PT* __restrict__ rowptr,
+                     const IT* __restrict__ col, const double* __restrict__ val,
+                     const double* __restrict__ x, const double* __restrict__ ghost, int64_t nloc,
+                     double* __restrict__ y, const double* __restrict__ b, const int* istate) {
+    if (!running(istate)) return;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nb) return;
+    const int64_t r = __ldg(rows + t);
+    double sum = 0.0;
+    const int64_t q1 = (int64_t)__ldg(rowptr + r + 1);
+    for (int64_t q = (int64_t)__ldg(rowptr + r); q < q1; q++) {
+        const int64_t c = (int64_t)__ldg(col + q);
+        const double xv = c >= nloc ? __ldg(ghost + (c - nloc)) : __ldg(x + c);
+        sum = __dadd_rn(sum, __dmul_rn(__ldg(val + q), xv));
+    }
+    y[r] = RESID ? b[r] - sum : sum;
+}
+
+template <typename IT, typename PT>
+static void spmv_rows_t(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                        const int* istate, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((a.n_bnd + 255) / 256);
+    if (blocks == 0) return;
+    const PT* rp = static_cast<const PT*>(a.rowptr);
+    const IT* ci = static_cast<const IT*>(a.col);
+    if (resid) spmv_rows_kernel<IT, PT, true><<<blocks, 256, 0, s>>>(a.n_bnd, a.bnd_rows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+    else spmv_rows_kernel<IT, PT, false><<<blocks, 256, 0, s>>>(a.n_bnd, a.bnd_rows, rp, ci, a.val, x, a.ghost, a.nloc, y, b, istate);
+}
+
+void launch_spmv_rows(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                      const int* istate, cudaStream_t s) {
+    if (a.idx64) {
+        if (a.ptr64) spmv_rows_t<int64_t, int64_t>(a, x, y, b, resid, istate, s);
+        else spmv_rows_t<int64_t, int32_t>(a, x, y, b, resid, istate, s);
+    } else {
+        if (a.ptr64) spmv_rows_t<int32_t, int64_t>(a, x, y, b, resid, istate, s);
+        else spmv_rows_t<int32_t, int32_t>(a, x, y, b, resid, istate, s);
     }
 }
 

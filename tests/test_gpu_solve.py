@@ -603,3 +603,26 @@ def test_bound_workspace(P):
     with pytest.raises(P.IgsError):
         s.solve(b, k=60, restart=40, tol=1e-10, gs_iters=2)   # needs a 41-column V
     s.close()
+
+
+def test_split_interior_boundary_spmv_one_gpu(P, monkeypatch):
+    """G > 1 splits the SpMV into interior rows (SELL, during the halo) and rows with ghost
+    columns (row-list kernel, after it).  IGS_TEST_BND_EVERY=k routes every k-th row through
+    the boundary pass on one GPU: the solve must keep the same bits."""
+    import torch
+    prob = W.config("c3", N=64)
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for every in ("7", "0"):
+        monkeypatch.setenv("IGS_TEST_BND_EVERY", every)
+        monkeypatch.setenv("IGS_PERSIST", "0")
+        s = P.Solver(prob.A)
+        outs[every] = s.solve(b, k=60, restart=20, tol=1e-10, gs_iters=2)
+        y = torch.empty(prob.A.n_rows, dtype=torch.float64, device="cuda")
+        x = torch.from_numpy(np.random.default_rng(1).standard_normal(prob.A.n_rows)).cuda()
+        s.spmv(x, y)
+        outs[every]["y"] = y.cpu().numpy()
+        s.close()
+    g, u = outs["7"], outs["0"]
+    assert g["H"].tobytes() == u["H"].tobytes() and g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+    assert g["y"].tobytes() == u["y"].tobytes()
