@@ -626,3 +626,24 @@ def test_split_interior_boundary_spmv_one_gpu(P, monkeypatch):
     g, u = outs["7"], outs["0"]
     assert g["H"].tobytes() == u["H"].tobytes() and g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
     assert g["y"].tobytes() == u["y"].tobytes()
+
+
+@pytest.mark.parametrize("persist", ["1", "0"])
+@pytest.mark.parametrize("k,restart", [(1, 0), (2, 0), (3, 1), (5, 2), (7, 3)])
+@pytest.mark.parametrize("gs", [1, 2])
+def test_tiny_k_and_restart_edges(P, persist, k, restart, gs, monkeypatch):
+    """Degenerate cycle lengths (m = 1, 2, 3; a drain-only cycle; short restarts) on the
+    persistent kernel and the per-kernel path, against the oracle."""
+    import torch
+    monkeypatch.setenv("IGS_PERSIST", persist)
+    rng = np.random.default_rng(k * 10 + restart)
+    D = np.diag(rng.uniform(2.0, 4.0, 40)) + np.triu(rng.standard_normal((40, 40)) * 0.1, 1)
+    A = W.dense_to_csr(D)
+    b = rng.standard_normal(40)
+    s = P.Solver(A)
+    g = s.solve(torch.from_numpy(b).cuda(), k=k, restart=restart, tol=0.0, gs_iters=gs)
+    s.close()
+    o = oracle.gmres(A, b, k, restart=restart, tol=0.0, variant=VARIANT[gs], dot_block=4096)
+    assert g["iters"] == o["iters"] == k and g["cycles"] == o["cycles"]
+    np.testing.assert_allclose(g["x"].cpu().numpy(), o["x"], rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-10, atol=1e-15)
