@@ -146,6 +146,7 @@ struct igs_ctx {
     bool pc_enabled = true;   // IGS_PERSIST=0 disables
     int64_t pc_max_n = 12288;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
+    int64_t pc_rowsplit_n = 8192;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
     int64_t n_pcycle = 0;
     unsigned long long* d_pcprof = nullptr;  // IGS_PC_PROF=1 phase timestamps
     // SELL-32 copy of A (short rows)
@@ -650,6 +651,7 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         if (const char* e = std::getenv("IGS_PERSIST")) ctx->pc_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PC_GRID")) ctx->pc_grid = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_MAX_N")) ctx->pc_max_n = std::atoll(e);
+        if (const char* e = std::getenv("IGS_PC_ROWSPLIT_N")) ctx->pc_rowsplit_n = std::atoll(e);
         if (const char* e = std::getenv("IGS_FUSED_L2_MB")) ctx->fused_budget = std::atof(e) * 1e6;
     }
     cudaError_t e;
@@ -976,8 +978,10 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             CUDA_TRY(cudaMemsetAsync(ctx->d_pcprof, 0, sizeof(unsigned long long) * 8 * (size_t)(ctx->dev_state.m + 2), st));
         const double by = (double)m * spmv_bytes(ctx) + 16.0 * n * 0.5 * m * (m + 1);
         TIMED(IGS_K_PERSIST, by, {
+            // row-block dots above pc_rowsplit_n rows (each CTA would otherwise re-read u, z)
+            double* part = (n >= ctx->pc_rowsplit_n && grid - 1 <= ctx->bdot_grid) ? ctx->d_part : nullptr;
             cudaError_t e_ = launch_pcycle(d, ctx->A, ctx->d_V, ctx->ldv, ctx->d_z, n, m, gs,
-                                           ctx->d_counter + 4, ctx->d_counter, grid, st, ctx->d_pcprof);
+                                           ctx->d_counter + 4, ctx->d_counter, grid, st, ctx->d_pcprof, part);
             CUDA_TRY(e_);
         });
         if (ctx->d_pcprof) {  // IGS_PC_PROF=1: mean phase durations of this cycle to stderr

@@ -91,7 +91,8 @@ void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b,
 // one-sweep (gs = 1) cycle in one cooperative launch, single GPU.  flags: 4 zeroed unsigned.
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                          unsigned long long* prof = nullptr);
+                          unsigned long long* prof = nullptr, double* part = nullptr);
+// (part != nullptr: row-block dots with grid x 2(m+1) partials, for larger n)
 
 // Fused block dot: out = [V_p^T u, u.u, V_p^T z, u.z] (z != NULL) or [V_p^T u, u.u].
 // part: [grid * 2(p+1)] scratch, counter: one zeroed unsigned (reset by the kernel).

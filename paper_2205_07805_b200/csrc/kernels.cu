@@ -1927,7 +1927,8 @@ template <typename IT, typename PT>
 __global__ void __launch_bounds__(PC_THREADS, 1)
     pcycle_kernel(Dev d, int64_t n, int m, int gs, const PT* __restrict__ rowptr,
                   const IT* __restrict__ col, const double* __restrict__ val, int lpr, double* V,
-                  int64_t ld, double* z, unsigned* flags, unsigned* counter, unsigned long long* prof) {
+                  int64_t ld, double* z, unsigned* flags, unsigned* counter, unsigned long long* prof,
+                  double* part) {
     extern __shared__ double sm[];
     __shared__ double red[40];
     __shared__ int s_go;
@@ -2009,7 +2010,55 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         }
         if (b == 0) stamp(p, 1);
         // ---- B: dots [V_p, u]^T [u, z] -> d.dots + p*dld (Step 4, one reduction) ------
-        {
+        if (part) {
+            // larger n: CTA b owns a contiguous row block and all 2(p+1) partial dots of it
+            // (u and z read once overall); after a barrier, warp i of the grid sums output i
+            // over the partials in CTA order (the block dot's stage 2, spread over the grid)
+            double* out = d.dots + (int64_t)p * d.dld;
+            const int items = p + 1, stride = 2 * items;
+            const int64_t rpb = ((n + W - 1) / W + 31) / 32 * 32;
+            const int64_t rb0 = min((int64_t)b * rpb, n), rb1 = min(rb0 + rpb, n);
+            for (int cb = 0; cb < items; cb += PC_CB) {
+                const int nc = min(PC_CB, items - cb);
+                double au[PC_CB], az[PC_CB];
+#pragma unroll
+                for (int c = 0; c < PC_CB; c++) { au[c] = 0.0; az[c] = 0.0; }
+                for (int64_t r = rb0 + tid; r < rb1; r += PC_THREADS) {
+                    const double uu = __ldcg(u + r);
+                    const double zz = drain ? 0.0 : __ldcg(z + r);
+#pragma unroll
+                    for (int c = 0; c < PC_CB; c++) {
+                        if (c < nc) {
+                            const double v = __ldcg(V + (int64_t)(cb + c) * ld + r);
+                            au[c] = fma(v, uu, au[c]);
+                            az[c] = fma(v, zz, az[c]);
+                        }
+                    }
+                }
+                const double ru = bfly8(au, lane);
+                const double rz = bfly8(az, lane);
+                if ((lane & 3) == 0) {
+                    s_red[warp * 2 * PC_CB + (lane >> 2)] = ru;
+                    s_red[warp * 2 * PC_CB + PC_CB + (lane >> 2)] = rz;
+                }
+                __syncthreads();
+                if (tid < 2 * nc) {
+                    const int c = tid % nc, which = tid / nc;
+                    double t = 0.0;
+                    for (int w = 0; w < PC_WARPS; w++) t += s_red[w * 2 * PC_CB + which * PC_CB + c];
+                    part[(int64_t)b * stride + which * items + cb + c] = t;
+                }
+                __syncthreads();
+            }
+            grid_barrier(flags, W, epoch);
+            for (int i = b * PC_WARPS + warp; i < (drain ? items : stride); i += W * PC_WARPS) {
+                double t = 0.0;
+                for (int q = lane; q < W; q += 32) t += __ldcg(part + (int64_t)q * stride + i);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(FULL_MASK, t, off);
+                if (lane == 0) out[i] = t;  // [V_p^T u, u.u | V_p^T z, u.z]: same layout
+            }
+        } else {
             double* out = d.dots + (int64_t)p * d.dld;
             const int items = p + 1;
             const int per = (items + W - 1) / W;
@@ -2146,7 +2195,7 @@ static size_t pcycle_smem(int M) {
 template <typename IT, typename PT>
 static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                              int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                             unsigned long long* prof) {
+                             unsigned long long* prof, double* part) {
     auto fn = pcycle_kernel<IT, PT>;
     const size_t smem = pcycle_smem(d.m);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2160,7 +2209,8 @@ static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t
     const IT* ci = static_cast<const IT*>(a.col);
     const double* va = a.val;
     int lpr = a.lpr > 0 ? a.lpr : 4;
-    void* args[] = {&dd, &n, &m, &gs, (void*)&rp, (void*)&ci, (void*)&va, &lpr, &V, &ld, &z, &flags, &counter, &prof};
+    void* args[] = {&dd, &n, &m, &gs, (void*)&rp, (void*)&ci, (void*)&va, &lpr, &V, &ld, &z, &flags, &counter, &prof,
+                    &part};
     return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(PC_THREADS), args, smem, s);
 }
 
@@ -2168,13 +2218,13 @@ int pcycle_max_grid(int num_sms) { return num_sms; }
 
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                          unsigned long long* prof) {
+                          unsigned long long* prof, double* part) {
     if (a.idx64) {
-        if (a.ptr64) return pcycle_go<int64_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
-        return pcycle_go<int64_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
+        if (a.ptr64) return pcycle_go<int64_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
+        return pcycle_go<int64_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
     }
-    if (a.ptr64) return pcycle_go<int32_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
-    return pcycle_go<int32_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof);
+    if (a.ptr64) return pcycle_go<int32_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
+    return pcycle_go<int32_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
 }
 
 }  // namespace igs

@@ -477,15 +477,20 @@ def test_paper_matrices_on_gpu(P):
 
 
 @pytest.mark.parametrize("gs", [1, 2])
-@pytest.mark.parametrize("cfg,grid", [("c1", "0"), ("c1", "1"), ("c1", "2"), ("c2", "0"), ("c2", "3"), ("c3s", "0"), ("c3s", "2")])
+@pytest.mark.parametrize("cfg,grid", [("c1", "0"), ("c1", "1"), ("c1", "2"), ("c2", "0"), ("c2", "3"), ("c3s", "0"),
+                                      ("c3s", "2"), ("c3r", "0"), ("c3r", "5"), ("c3m", "0")])
 def test_persistent_cycle_kernel(P, cfg, grid, gs, monkeypatch):
     """Small single-GPU problems run each cycle as ONE cooperative launch.
     Same algebra as the per-kernel path, different reduction order: H within the parity bar
     of the per-kernel path and of the oracle, same iterations / reductions / termination,
     bitwise reproducible; grid=1 puts the update and the tail on the same CTA."""
     import torch
-    prob = W.config("c3", N=48) if cfg == "c3s" else W.config(cfg)
-    k, restart, tol = (70, 30, 1e-10) if cfg == "c3s" else (prob.k, 0, 0.0)
+    # c3m (n = 16384) takes the row-block dot phase of the kernel (c3r: n = 4096, forced below)
+    sizes = {"c3s": 48, "c3r": 64, "c3m": 128}
+    prob = W.config("c3", N=sizes[cfg]) if cfg in sizes else W.config(cfg)
+    k, restart, tol = (70, 30, 1e-10) if cfg in sizes else (prob.k, 0, 0.0)
+    monkeypatch.setenv("IGS_PC_MAX_N", "100000")
+    monkeypatch.setenv("IGS_PC_ROWSPLIT_N", "4096" if cfg == "c3r" else "8192")
     b = torch.from_numpy(prob.b).cuda()
     outs = {}
     for persist in ("1", "0"):
