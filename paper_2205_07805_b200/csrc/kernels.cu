@@ -2018,37 +2018,28 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             const int items = p + 1, stride = 2 * items;
             const int64_t rpb = ((n + W - 1) / W + 31) / 32 * 32;
             const int64_t rb0 = min((int64_t)b * rpb, n), rb1 = min(rb0 + rpb, n);
-            for (int cb = 0; cb < items; cb += PC_CB) {
-                const int nc = min(PC_CB, items - cb);
-                double au[PC_CB], az[PC_CB];
+            // warp w: 4 columns at a time over the CTA's rows (lane = row), one butterfly for
+            // the 8 sums, no block-wide synchronisation
+            for (int cb = 4 * warp; cb < items; cb += 4 * PC_WARPS) {
+                const int nc = min(4, items - cb);
+                double a[8];
 #pragma unroll
-                for (int c = 0; c < PC_CB; c++) { au[c] = 0.0; az[c] = 0.0; }
-                for (int64_t r = rb0 + tid; r < rb1; r += PC_THREADS) {
+                for (int c = 0; c < 8; c++) a[c] = 0.0;
+                for (int64_t r = rb0 + lane; r < rb1; r += 32) {
                     const double uu = __ldcg(u + r);
                     const double zz = drain ? 0.0 : __ldcg(z + r);
 #pragma unroll
-                    for (int c = 0; c < PC_CB; c++) {
+                    for (int c = 0; c < 4; c++) {
                         if (c < nc) {
                             const double v = __ldcg(V + (int64_t)(cb + c) * ld + r);
-                            au[c] = fma(v, uu, au[c]);
-                            az[c] = fma(v, zz, az[c]);
+                            a[c] = fma(v, uu, a[c]);
+                            a[4 + c] = fma(v, zz, a[4 + c]);
                         }
                     }
                 }
-                const double ru = bfly8(au, lane);
-                const double rz = bfly8(az, lane);
-                if ((lane & 3) == 0) {
-                    s_red[warp * 2 * PC_CB + (lane >> 2)] = ru;
-                    s_red[warp * 2 * PC_CB + PC_CB + (lane >> 2)] = rz;
-                }
-                __syncthreads();
-                if (tid < 2 * nc) {
-                    const int c = tid % nc, which = tid / nc;
-                    double t = 0.0;
-                    for (int w = 0; w < PC_WARPS; w++) t += s_red[w * 2 * PC_CB + which * PC_CB + c];
-                    part[(int64_t)b * stride + which * items + cb + c] = t;
-                }
-                __syncthreads();
+                const double t = bfly8(a, lane);  // lane holds value lane >> 2
+                const int idx = lane >> 2, c = idx & 3, which = idx >> 2;
+                if ((lane & 3) == 0 && c < nc) part[(int64_t)b * stride + which * items + cb + c] = t;
             }
             grid_barrier(flags, W, epoch);
             for (int i = b * PC_WARPS + warp; i < (drain ? items : stride); i += W * PC_WARPS) {

@@ -240,6 +240,7 @@ def test_fused_wavefront_matches_unfused(P, gs, monkeypatch):
     same iterations, H to rounding, and both against the oracle."""
     import torch
     prob = W.config("c4", N=40)             # reach = 1600 rows: lag 14 tiles, 500 tiles
+    monkeypatch.setenv("IGS_PERSIST", "0")  # the three-kernel path, not the persistent cycle
     outs = {}
     for fused in ("1", "0"):
         monkeypatch.setenv("IGS_FUSED", fused)
