@@ -146,7 +146,7 @@ struct igs_ctx {
     bool pc_enabled = true;   // IGS_PERSIST=0 disables
     int64_t pc_max_n = 65536;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
-    int64_t pc_rowsplit_n = 8192;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
+    int64_t pc_rowsplit_n = 4096;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
     int64_t n_pcycle = 0;
     unsigned long long* d_pcprof = nullptr;  // IGS_PC_PROF=1 phase timestamps
     // SELL-32 copy of A (short rows)

@@ -491,7 +491,7 @@ def test_persistent_cycle_kernel(P, cfg, grid, gs, monkeypatch):
     prob = W.config("c3", N=sizes[cfg]) if cfg in sizes else W.config(cfg)
     k, restart, tol = (70, 30, 1e-10) if cfg in sizes else (prob.k, 0, 0.0)
     monkeypatch.setenv("IGS_PC_MAX_N", "100000")
-    monkeypatch.setenv("IGS_PC_ROWSPLIT_N", "4096" if cfg == "c3r" else "8192")
+    monkeypatch.setenv("IGS_PC_ROWSPLIT_N", "0" if cfg == "c3r" else "4096")
     b = torch.from_numpy(prob.b).cuda()
     outs = {}
     for persist in ("1", "0"):
