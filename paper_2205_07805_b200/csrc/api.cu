@@ -820,8 +820,8 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(long long) * (ctx->fused_grid + 1), ctx->stream));
     }
     if (!ctx->d_counter) {
-        CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 8));  // [4..7]: persistent-kernel flags
-        CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned) * 8, ctx->stream));
+        CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 12));  // [4..8]: persistent-kernel flags
+        CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned) * 12, ctx->stream));
     }
     if (host_vec && !ctx->d_b) {
         CUDA_TRY(cudaMalloc(&ctx->d_b, sizeof(double) * ldv));
@@ -970,7 +970,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         const double iter_bytes = spmv_bytes(ctx) + 8.0 * n * (m + 1);
         int grid = ctx->pc_grid > 0 ? ctx->pc_grid : (int)std::ceil(iter_bytes / 32768.0) + 1;
         grid = std::max(1, std::min(grid, ctx->num_sms));
-        CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 4 * sizeof(unsigned), st));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 5 * sizeof(unsigned), st));
         if (std::getenv("IGS_PC_PROF") && !ctx->d_pcprof) {
             CUDA_TRY(cudaMalloc(&ctx->d_pcprof, sizeof(unsigned long long) * 8 * (size_t)(ctx->dev_state.m + 2)));
         }

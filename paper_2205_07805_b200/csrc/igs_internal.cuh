@@ -88,7 +88,7 @@ void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b,
                  const int* istate, cudaStream_t s);
 
 // Persistent cycle kernel (kernels.cu): iterations 1..m of one Alg. 3 (gs = 2) or Alg. 2
-// one-sweep (gs = 1) cycle in one cooperative launch, single GPU.  flags: 4 zeroed unsigned.
+// one-sweep (gs = 1) cycle in one cooperative launch, single GPU.  flags: 5 zeroed unsigned.
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
                           unsigned long long* prof = nullptr, double* part = nullptr);

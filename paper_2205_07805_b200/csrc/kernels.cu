@@ -1391,7 +1391,12 @@ __device__ double givens_column(const Dev& d, int j, double* col, double* scs, d
 // The small step on the calling CTA (any blockDim that is a multiple of 32, <= 1024).  All
 // global loads bypass L1 (ld.global.cg): the persistent cycle kernel runs this on one CTA
 // while other CTAs of the same grid produce its inputs.  sm: small_smem(d.m) bytes, red: 40.
-__device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double* sm, double* red) {
+// publish = false (persistent kernel, worker CTAs other than 0): the Alg. 3 critical step is
+// computed without any global write, and without the live status check, from the same
+// reduced dots -- bitwise the coefficients CTA 0 publishes; loc (shared, >= p + 3 doubles)
+// receives gamma, the update mode and beta (alpha stays in sm[0..p)).
+__device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double* sm, double* red,
+                           bool publish = true, double* loc = nullptr) {
     const int t0 = (int)__ldcg(d.scal + SC_T0);  // first global iteration of this cycle (graph-invariant)
     const int M = d.m;
     double* s_a = sm;               // [M+1]  r2 (Alg. 3) / a (Alg. 2)
@@ -1456,7 +1461,7 @@ __device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double
         if (tid == 0) ist[ST_MODE] = 0;  // the second update must not run either
         return;
     }
-    if (*(volatile int*)(ist + ST_STATUS) != RUNNING) return;
+    if (publish && *(volatile int*)(ist + ST_STATUS) != RUNNING) return;
 
     if (stage == SS_CRIT2) {
         // Alg. 2 two-reduce, second Gauss-Seidel sweep: r2 = V_{p+1}^T u is in
@@ -1530,7 +1535,8 @@ __device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double
             gamma = t > 0.0 ? sqrt(t) : 0.0;
             lrow2 = nr2;
             bd = !(t > kBreakdownC * kEps * s);  // S:274 / reading R12 cancellation guard
-            for (int i = tid; i < p; i += blockDim.x) d.alpha[i] = s_a[i];  // Step 10 uses r2
+            if (publish)
+                for (int i = tid; i < p; i += blockDim.x) d.alpha[i] = s_a[i];  // Step 10 uses r2
         } else {
             // Alg. 2 Step 6: gamma = ||w_{k-1}|| (fused into the single reduction)
             gamma = sqrt(s);
@@ -1546,13 +1552,21 @@ __device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double
             lrow2 = block_sum(pa, red);
         }
         if (!isfinite(gamma)) bd = true;
-        if (tid == 0) {  // ||L||_F of this cycle: row p of L is (r2 or a) / gamma
+        if (loc && tid == 0) {
+            loc[0] = gamma;
+            loc[1] = bd ? 0.0 : (drain ? 1.0 : 3.0);  // update mode (as ST_MODE)
+        }
+        if (!publish) {
+            __syncthreads();
+            if (bd || drain) return;
+        }
+        if (publish && tid == 0) {  // ||L||_F of this cycle: row p of L is (r2 or a) / gamma
             double cum = __ldcg(d.scal + SC_LCUM);
             if (!drain && !bd) cum += lrow2 / (gamma * gamma);
             d.scal[SC_LCUM] = cum;
             d.lnorm[t0 + p] = sqrt(cum);
         }
-        if (tid == 0) {
+        if (publish && tid == 0) {
             d.gam[p] = gamma;
             d.cbd[p] = bd ? 1.0 : 0.0;
             d.scal[SC_GAMMA] = gamma;
@@ -1570,16 +1584,24 @@ __device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double
             for (int i = tid; i < p; i += blockDim.x) {
                 const double ci = s_c[i] / gamma;
                 const double li = s_a[i] / gamma;
-                d.L[p + (int64_t)i * M] = li;
-                d.beta[i] = ci;
+                if (publish) {
+                    d.L[p + (int64_t)i * M] = li;
+                    d.beta[i] = ci;
+                }
+                if (loc) loc[2 + i] = ci;
                 part += li * ci;
             }
             // Step 12 (Stephen's trick): r1 = [c ; d - L[p,:p] . c]
             const double acc = block_sum(part, red);
-            if (tid == 0) d.beta[p] = dd - acc;
+            if (tid == 0) {
+                if (publish) d.beta[p] = dd - acc;
+                if (loc) loc[2 + p] = dd - acc;
+            }
             __syncthreads();
-            double* r1row = d.r1h + (int64_t)p * (M + 2);  // copy for the tail (hp, Step 15)
-            for (int i = tid; i <= p; i += blockDim.x) r1row[i] = __ldcg(d.beta + i);
+            if (publish) {
+                double* r1row = d.r1h + (int64_t)p * (M + 2);  // copy for the tail (hp, Step 15)
+                for (int i = tid; i <= p; i += blockDim.x) r1row[i] = __ldcg(d.beta + i);
+            }
         } else {
             // Alg. 2 Steps 8-10: c /= gamma ; c[p] /= gamma ; L[p, :p] = a / gamma
             for (int i = tid; i <= p; i += blockDim.x) {
@@ -1894,7 +1916,8 @@ void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
 // tail decides is acted on at the next C phase.  Every load of data written inside the
 // launch is ld.global.cg: L1 is not coherent across SMs.
 // flags (zeroed before launch): [0] barrier count, [1] last p whose CRIT ran, [2] p at
-// which CTA 0 stopped (0 = running), [3] last p whose TAIL ran.
+// which CTA 0 stopped (0 = running), [3] last p whose TAIL ran, [4] first p whose TAIL
+// left the status not RUNNING.
 // ------------------------------------------------------------------------------------
 constexpr int PC_THREADS = 512;
 constexpr int PC_WARPS = PC_THREADS / 32;
@@ -1970,13 +1993,22 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             small_body(d, SS_TAIL, gs, p, m, s_small, red);
             stamp(p, 7);
             __syncthreads();
-            if (tid == 0) { __threadfence(); st_release_u32(flags + 3, (unsigned)p); }
+            if (tid == 0) {
+                __threadfence();
+                // first iteration at which the status left RUNNING (the workers' stop rule)
+                if (vist[ST_STATUS] != RUNNING && ld_acquire_u32(flags + 4) == 0u) st_release_u32(flags + 4, (unsigned)p);
+                st_release_u32(flags + 3, (unsigned)p);
+            }
         }
         return;
     }
 
     // ---------------- worker CTAs ----------------------------------------------------------
     unsigned epoch = 0;
+    if (vist[ST_STATUS] != RUNNING) {  // stopped by the cycle priming (final at launch: uniform)
+        if (b == 0 && tid == 0) { __threadfence(); st_release_u32(flags + 2, 1u); }
+        return;
+    }
     for (int p = 1; p <= m; p++) {
         const bool drain = (p == m);
         const double* u = V + (int64_t)p * ld;
@@ -2091,39 +2123,73 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         }
         grid_barrier(flags, W, epoch);
         if (b == 0) stamp(p, 2);
-        // ---- C: critical small step or the stop decision (CTA 0) ---------------------------
-        if (b == 0) {
+        // ---- C: critical small step ----------------------------------------------------------
+        // Alg. 3 (gs = 2): every worker computes the critical step from the same reduced dots
+        // (bitwise the coefficients CTA 0 publishes for the tail), so no barrier separates it
+        // from the update; the stop decision is uniform: a stop the tail recorded at an
+        // iteration <= p - PC_LAG (final once tail_done >= p - PC_LAG).  Alg. 2 one sweep:
+        // CTA 0 (its forward substitution reads L rows other CTAs do not have), a barrier.
+        bool local_coef = false;
+        if (gs == 2) {
             if (tid == 0) {
                 if (split && p > PC_LAG)
                     while (ld_acquire_u32(flags + 3) < (unsigned)(p - PC_LAG)) {
                     }
-                s_go = (vist[ST_STATUS] == RUNNING);
-                if (!s_go) { __threadfence(); st_release_u32(flags + 2, (unsigned)p); }
+                int go;
+                if (split) {
+                    const unsigned sa = ld_acquire_u32(flags + 4);
+                    go = !(sa != 0u && (int)sa <= p - PC_LAG);
+                } else {
+                    go = (vist[ST_STATUS] == RUNNING);
+                }
+                s_go = go;
+                if (!go && b == 0) { __threadfence(); st_release_u32(flags + 2, (unsigned)p); }
+                s_coef[1] = 0.0;  // mode 0 unless the critical step below completes
             }
             __syncthreads();
-            if (s_go) {
-                small_body(d, SS_CRIT, gs, p, m, s_small, red);
+            if (!s_go) break;
+            small_body(d, SS_CRIT, gs, p, m, s_small, red, /*publish=*/b == 0, /*loc=*/s_coef);
+            __syncthreads();
+            if (b == 0 && tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
+            if (b == 0) { stamp(p, 3); stamp(p, 4); }
+            local_coef = true;
+        } else {
+            if (b == 0) {
+                if (tid == 0) {
+                    if (split && p > PC_LAG)
+                        while (ld_acquire_u32(flags + 3) < (unsigned)(p - PC_LAG)) {
+                        }
+                    s_go = (vist[ST_STATUS] == RUNNING);
+                    if (!s_go) { __threadfence(); st_release_u32(flags + 2, (unsigned)p); }
+                }
                 __syncthreads();
-                if (tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
+                if (s_go) {
+                    small_body(d, SS_CRIT, gs, p, m, s_small, red);
+                    __syncthreads();
+                    if (tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
+                }
+                stamp(p, 3);
             }
-            stamp(p, 3);
+            grid_barrier(flags, W, epoch);
+            if (b == 0) stamp(p, 4);
+            if (*(volatile unsigned*)(flags + 2) != 0u) break;  // uniform: written before the barrier
         }
-        grid_barrier(flags, W, epoch);
-        if (b == 0) stamp(p, 4);
-        if (*(volatile unsigned*)(flags + 2) != 0u) break;  // uniform: written before the barrier
         // ---- D: fused update (Steps 10-13) -------------------------------------------------
         {
-            int mode = (vist[ST_MODE_IT] == p) ? vist[ST_MODE] : 0;
+            int mode = local_coef ? (int)s_coef[1] : ((vist[ST_MODE_IT] == p) ? vist[ST_MODE] : 0);
             mode &= drain ? 1 : 3;
             if (mode != 0) {
                 const bool want_next = (mode & 2) != 0;
-                double* sa = s_coef;
-                double* sbt = s_coef + (M + 1);
-                if (gs == 2)
-                    for (int j = tid; j < p; j += PC_THREADS) sa[j] = __ldcg(d.alpha + j);
-                if (want_next)
-                    for (int j = tid; j <= p; j += PC_THREADS) sbt[j] = __ldcg(d.beta + j);
-                const double gamma = __ldcg(d.scal + SC_GAMMA);
+                // local: alpha = r2 in small_body's s_a, [gamma, mode, beta...] in s_coef
+                double* sa = local_coef ? s_small : s_coef;
+                double* sbt = local_coef ? s_coef + 2 : s_coef + (M + 1);
+                if (!local_coef) {
+                    if (gs == 2)
+                        for (int j = tid; j < p; j += PC_THREADS) sa[j] = __ldcg(d.alpha + j);
+                    if (want_next)
+                        for (int j = tid; j <= p; j += PC_THREADS) sbt[j] = __ldcg(d.beta + j);
+                }
+                const double gamma = local_coef ? s_coef[0] : __ldcg(d.scal + SC_GAMMA);
                 __syncthreads();
                 double* r1s = s_red;                  // [PC_WARPS][32]
                 double* r2s = s_red + PC_WARPS * 32;  // [PC_WARPS][32]
