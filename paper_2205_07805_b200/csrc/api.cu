@@ -809,7 +809,15 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.istate = ctx->d_int;
         ctx->m_cap = mm;
         ctx->k_cap = kk;
-        if (ctx->xchg_req) TRY(setup_xchg(ctx, d.dld));
+        if (ctx->xchg_req && setup_xchg(ctx, d.dld) != IGS_OK) {
+            // symmetric memory / device communicator unavailable: keep ncclAllReduce (the
+            // window registration is collective, so every rank takes the same branch)
+            std::fprintf(stderr, "[igs] fused NVLink exchange unavailable (%s); using ncclAllReduce\n",
+                         igs_last_error());
+            cudaFree(ctx->d_xchg);
+            ctx->d_xchg = nullptr;
+            ctx->xchg_req = false;
+        }
     }
     if (!ctx->d_z) {
         CUDA_TRY(cudaMalloc(&ctx->d_z, sizeof(double) * ldv));
