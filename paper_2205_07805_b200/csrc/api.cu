@@ -149,6 +149,7 @@ struct igs_ctx {
     int64_t pc_rowsplit_n = 4096;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
     int64_t n_pcycle = 0;
     unsigned long long* d_pcprof = nullptr;  // IGS_PC_PROF=1 phase timestamps
+
     // SELL-32 copy of A (short rows)
     int64_t* d_sell_ptr = nullptr;
     uint8_t* d_sell_len = nullptr;
@@ -689,7 +690,7 @@ static size_t small_doubles(int m, int k) {
            + (m + 1) * dld  // dots
            + 4 * (m + 2)    // alpha, beta, y, gam
            + (m + 3)        // dots2
-           + (size_t)(m + 1) * (m + 2) + (m + 2)  // r1h, cbd
+           + 2 * (size_t)(m + 1) * (m + 2) + (m + 2)  // r1h, r3h, cbd
            + SC_COUNT + 2 * (k + 2);  // res_hist, lnorm
 }
 
@@ -802,6 +803,7 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.gam = take(mm + 2);
         d.dots2 = take(mm + 3);
         d.r1h = take((size_t)(mm + 1) * (mm + 2));
+        d.r3h = take((size_t)(mm + 1) * (mm + 2));
         d.cbd = take(mm + 2);
         d.scal = take(SC_COUNT);
         d.res_hist = take(kk + 2);
@@ -978,7 +980,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         const double iter_bytes = spmv_bytes(ctx) + 8.0 * n * (m + 1);
         int grid = ctx->pc_grid > 0 ? ctx->pc_grid : (int)std::ceil(iter_bytes / 32768.0) + 1;
         grid = std::max(1, std::min(grid, ctx->num_sms));
-        CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 5 * sizeof(unsigned), st));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 7 * sizeof(unsigned), st));
         if (std::getenv("IGS_PC_PROF") && !ctx->d_pcprof) {
             CUDA_TRY(cudaMalloc(&ctx->d_pcprof, sizeof(unsigned long long) * 8 * (size_t)(ctx->dev_state.m + 2)));
         }

@@ -45,6 +45,8 @@ struct Dev {
     double* dots2;  // [m+3] second reduction of Alg. 2 (two-reduce): V_{p+1}^T u
     double* r1h;    // [(m+1) x (m+2)] r1 of iteration p (row p): the tail of iteration p reads it
                     // while the critical step of p+1 already rewrites beta
+    double* r3h;    // [(m+1) x (m+2)] r3 = (I+L_p)^{-1} r2 of iteration p, computed ahead of
+                    // the tail by the persistent kernel's forward-substitution CTA (Alg. 3)
     double* cbd;    // [m+2] 1 if the critical step of iteration p saw a breakdown
     double* scal;   // [SC_COUNT]
     int* istate;    // [ST_COUNT]
@@ -88,7 +90,7 @@ void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b,
                  const int* istate, cudaStream_t s);
 
 // Persistent cycle kernel (kernels.cu): iterations 1..m of one Alg. 3 (gs = 2) or Alg. 2
-// one-sweep (gs = 1) cycle in one cooperative launch, single GPU.  flags: 5 zeroed unsigned.
+// one-sweep (gs = 1) cycle in one cooperative launch, single GPU.  flags: 7 zeroed unsigned.
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
                           unsigned long long* prof = nullptr, double* part = nullptr);

@@ -1396,7 +1396,7 @@ __device__ double givens_column(const Dev& d, int j, double* col, double* scs, d
 // reduced dots -- bitwise the coefficients CTA 0 publishes; loc (shared, >= p + 3 doubles)
 // receives gamma, the update mode and beta (alpha stays in sm[0..p)).
 __device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double* sm, double* red,
-                           bool publish = true, double* loc = nullptr) {
+                           bool publish = true, double* loc = nullptr, bool r3_ready = false) {
     const int t0 = (int)__ldcg(d.scal + SC_T0);  // first global iteration of this cycle (graph-invariant)
     const int M = d.m;
     double* s_a = sm;               // [M+1]  r2 (Alg. 3) / a (Alg. 2)
@@ -1628,8 +1628,12 @@ __device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double
     double hn2 = 0.0;
     if (gs == 2) {
         // Step 5: r3 = (I + L_p)^{-1} r2 ; Step 14: H[:p, p-1] = hp + r3, H[p, p-1] = gamma (R3)
-        for (int i = tid; i < p; i += blockDim.x) s_x[i] = __ldcg(dv + i);
-        trisolve_smem(p, d.L, M, s_x);
+        if (r3_ready) {  // computed ahead by the persistent kernel's forward-substitution CTA
+            for (int i = tid; i < p; i += blockDim.x) s_x[i] = __ldcg(d.r3h + (int64_t)p * (M + 2) + i);
+        } else {
+            for (int i = tid; i < p; i += blockDim.x) s_x[i] = __ldcg(dv + i);
+            trisolve_smem(p, d.L, M, s_x);
+        }
         double h2 = 0.0;
         for (int i = tid; i < p; i += blockDim.x) {
             const double h = __ldcg(d.HP + i + (int64_t)(p - 1) * d.ldh) + s_x[i];
@@ -1917,7 +1921,8 @@ void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
 // launch is ld.global.cg: L1 is not coherent across SMs.
 // flags (zeroed before launch): [0] barrier count, [1] last p whose CRIT ran, [2] p at
 // which CTA 0 stopped (0 = running), [3] last p whose TAIL ran, [4] first p whose TAIL
-// left the status not RUNNING.
+// left the status not RUNNING, [5] last p whose dots are final, [6] last p whose r3 is
+// computed (forward-substitution CTA, Alg. 3).
 // ------------------------------------------------------------------------------------
 constexpr int PC_THREADS = 512;
 constexpr int PC_WARPS = PC_THREADS / 32;
@@ -1969,8 +1974,39 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, b = blockIdx.x;
     const bool split = G > 1;
-    const int W = split ? G - 1 : 1;             // worker CTAs
+    // Alg. 3 with >= 3 CTAs: CTA G-2 computes the Step 5 forward substitution r3 of iteration
+    // p as soon as its dots and L row p-1 are final, ahead of the tail (which then only does
+    // H, Givens and the Step 15 GEMV)
+    const bool tri = gs == 2 && G >= 3;
+    const int W = split ? G - 1 - (tri ? 1 : 0) : 1;  // worker CTAs
     const volatile int* vist = d.istate;
+
+    if (tri && b == G - 2) {
+        // ---------------- forward-substitution CTA ---------------------------------------
+        double* s_x = s_small + (M + 1) + (M + 2);  // small_body's s_x slot
+        for (int p = 1; p <= m; p++) {
+            if (tid == 0) {
+                int go = 0;
+                while (true) {
+                    if (ld_acquire_u32(flags + 5) >= (unsigned)p && ld_acquire_u32(flags + 1) + 1u >= (unsigned)p) { go = 1; break; }
+                    if (ld_acquire_u32(flags + 2) != 0u) {
+                        go = ld_acquire_u32(flags + 5) >= (unsigned)p && ld_acquire_u32(flags + 1) + 1u >= (unsigned)p;
+                        break;
+                    }
+                }
+                s_go = go;
+            }
+            __syncthreads();
+            if (!s_go) break;
+            const double* dv = d.dots + (int64_t)p * d.dld;
+            for (int i = tid; i < p; i += PC_THREADS) s_x[i] = __ldcg(dv + i);
+            trisolve_smem(p, d.L, M, s_x);
+            for (int i = tid; i < p; i += PC_THREADS) d.r3h[(int64_t)p * (M + 2) + i] = s_x[i];
+            __syncthreads();
+            if (tid == 0) { __threadfence(); st_release_u32(flags + 6, (unsigned)p); }
+        }
+        return;
+    }
 
     if (split && b == G - 1) {
         // ---------------- tail CTA ---------------------------------------------------------
@@ -1978,9 +2014,12 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             if (tid == 0) {
                 int go = 0;
                 while (true) {
-                    if (ld_acquire_u32(flags + 1) >= (unsigned)p) { go = 1; break; }
+                    if (ld_acquire_u32(flags + 1) >= (unsigned)p && (!tri || ld_acquire_u32(flags + 6) >= (unsigned)p)) { go = 1; break; }
                     if (ld_acquire_u32(flags + 2) != 0u) {  // stopped: CRIT(p) may still have run
                         go = ld_acquire_u32(flags + 1) >= (unsigned)p;
+                        if (go && tri)  // its r3 follows: the dots of p were final before CRIT(p)
+                            while (ld_acquire_u32(flags + 6) < (unsigned)p) {
+                            }
                         break;
                     }
                 }
@@ -1990,7 +2029,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             __syncthreads();
             if (!s_go) break;
             stamp(p, 6);
-            small_body(d, SS_TAIL, gs, p, m, s_small, red);
+            small_body(d, SS_TAIL, gs, p, m, s_small, red, true, nullptr, /*r3_ready=*/tri);
             stamp(p, 7);
             __syncthreads();
             if (tid == 0) {
@@ -2123,6 +2162,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         }
         grid_barrier(flags, W, epoch);
         if (b == 0) stamp(p, 2);
+        if (tri && b == 0 && tid == 0) { __threadfence(); st_release_u32(flags + 5, (unsigned)p); }  // dots of p final
         // ---- C: critical small step ----------------------------------------------------------
         // Alg. 3 (gs = 2): every worker computes the critical step from the same reduced dots
         // (bitwise the coefficients CTA 0 publishes for the tail), so no barrier separates it
@@ -2238,7 +2278,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             if (tid == 0 && vist[ST_STATUS] == RUNNING) counter[1] += 1u;
             __syncthreads();
             stamp(p, 6);
-            small_body(d, SS_TAIL, gs, p, m, s_small, red);
+            small_body(d, SS_TAIL, gs, p, m, s_small, red, true, nullptr, /*r3_ready=*/tri);
             stamp(p, 7);
         }
         grid_barrier(flags, W, epoch);
