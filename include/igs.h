@@ -11,7 +11,9 @@
  * Alg. 2 Steps 1-13 + 17 with r^(3)=0, i.e. one Gauss-Seidel sweep, reading R8):
  *   z = A u                                   sparse matvec (Alg. 3 Step 4)
  *   [V_p, u]^T [u, z]  -> 2(p+1) scalars       ONE fused block dot
- *   ncclAllReduce of those 2(p+1) doubles      the single "Global Synchronization"
+ *   sum of those 2(p+1) doubles over the ranks the single "Global Synchronization": fused
+ *                                             into the block dot over NVLink peer memory (NCCL
+ *                                             device API) by default, or one ncclAllReduce
  *   (I+L)^{-1} correction, lagged norm, Stephen's trick, Hessenberg column, Givens
  *   v_p = (u - V_p r2)/gamma ; u' = z/gamma - V_{p+1} r1   fused update
  *
