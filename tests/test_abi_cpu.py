@@ -71,3 +71,35 @@ def test_plan_rejects_bad_input(P):
     assert list(ghosts) == [500]
     with pytest.raises(P.IgsError):                       # column missing from the ghost list
         P.igs_plan_remap(0, 500, A.rowptr[:501], A.colind, np.zeros(0, dtype=np.int64))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_plan_random_partitions(P, seed):
+    """igs_plan_ghosts / igs_plan_remap on random sparse rows and uneven row blocks (int32
+    and int64 columns) against a direct numpy construction: the ghosts are the sorted
+    distinct columns outside the block, counted per owning rank; local columns map to
+    col - row_begin, ghost g to n_local + (its position)."""
+    rng = np.random.default_rng(seed)
+    n, G = int(rng.integers(50, 400)), int(rng.integers(2, 6))
+    cuts = np.sort(rng.choice(np.arange(1, n), G - 1, replace=False))
+    bounds = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    lens = rng.integers(0, 9, n)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=rowptr[1:])
+    cols = np.concatenate([np.sort(rng.choice(n, int(l), replace=False)) for l in lens]) if lens.sum() else np.zeros(0)
+    for dt in (np.int32, np.int64):
+        colind = cols.astype(dt)
+        for r in range(G):
+            r0, r1 = int(bounds[r]), int(bounds[r + 1])
+            rp = rowptr[r0:r1 + 1] - rowptr[r0]
+            ci = colind[rowptr[r0]:rowptr[r1]]
+            ghosts, cnt = P.igs_plan_ghosts(r0, r1 - r0, rp, ci, G, bounds)
+            outside = np.unique(ci[(ci < r0) | (ci >= r1)].astype(np.int64))
+            assert np.array_equal(ghosts, outside)
+            owners = np.searchsorted(bounds, outside, side="right") - 1
+            assert np.array_equal(cnt, np.bincount(owners, minlength=G)) and cnt[r] == 0
+            loc = P.igs_plan_remap(r0, r1 - r0, rp, ci, ghosts)
+            c64 = ci.astype(np.int64)
+            inside = (c64 >= r0) & (c64 < r1)
+            assert np.array_equal(loc[inside], c64[inside] - r0)
+            assert np.array_equal(loc[~inside], (r1 - r0) + np.searchsorted(ghosts, c64[~inside]))
