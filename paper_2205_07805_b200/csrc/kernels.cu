@@ -2120,6 +2120,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                 double a[8];
 #pragma unroll
                 for (int c = 0; c < 8; c++) a[c] = 0.0;
+#pragma unroll 4
                 for (int64_t r = rb0 + lane; r < rb1; r += 32) {
                     const double uu = __ldcg(u + r);
                     const double zz = drain ? 0.0 : __ldcg(z + r);
@@ -2271,7 +2272,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                     if (ti < nt) {
                         const int64_t r = (b + (g0 + ti) * W) * 32 + lane;
                         if (r < n) {
-#pragma unroll 4
+#pragma unroll 8
                             for (int j = sl; j < p; j += S) {
                                 const double v = __ldcg(V + (int64_t)j * ld + r);
                                 if (gs == 2) t1 = fma(v, sa[j], t1);
