@@ -144,7 +144,7 @@ struct igs_ctx {
     int64_t n_graph_launches = 0;
     // persistent cycle kernel (small n, single GPU, Alg. 3 / Alg. 2 one sweep)
     bool pc_enabled = true;   // IGS_PERSIST=0 disables
-    int64_t pc_max_n = 65536;  // crossover vs the graph-replayed per-kernel path
+    int64_t pc_max_n = 160000;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
     int64_t pc_rowsplit_n = 4096;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
     int64_t n_pcycle = 0;

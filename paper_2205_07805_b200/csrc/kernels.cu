@@ -1980,7 +1980,8 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     pcycle_kernel(Dev d, int64_t n, int m, int gs, const PT* __restrict__ rowptr,
                   const IT* __restrict__ col, const double* __restrict__ val, int lpr, double* V,
                   int64_t ld, double* z, unsigned* flags, unsigned* counter, unsigned long long* prof,
-                  double* part) {
+                  double* part, const int64_t* __restrict__ sell_ptr, const uint8_t* __restrict__ sell_len,
+                  const IT* __restrict__ sell_col, const double* __restrict__ sell_val) {
     extern __shared__ double sm[];
     __shared__ double red[40];
     __shared__ int s_go;
@@ -2077,7 +2078,32 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         const double* u = V + (int64_t)p * ld;
         if (b == 0) stamp(p, 0);
         // ---- A: z = A u (Step 4) ---------------------------------------------------------
-        if (!drain) {
+        if (!drain && sell_ptr) {
+            // SELL-32 copy (short rows): one thread per row, coalesced entries, left-to-right
+            // separate multiply and add (bitwise the oracle's row loop, like spmv_sell_kernel)
+            for (int64_t r = (int64_t)b * PC_THREADS + tid; r < n; r += (int64_t)W * PC_THREADS) {
+                const int len = __ldg(sell_len + r);
+                const int64_t base = __ldg(sell_ptr + (r >> 5)) + (r & 31);
+                double sum = 0.0;
+                for (int k0 = 0; k0 < len; k0 += 8) {
+                    IT cc[8];
+                    double vv[8], xv[8];
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        const bool in = k0 + k < len;
+                        cc[k] = in ? __ldg(sell_col + base + 32 * (int64_t)(k0 + k)) : (IT)0;
+                        vv[k] = in ? __ldg(sell_val + base + 32 * (int64_t)(k0 + k)) : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 8; k++) xv[k] = k0 + k < len ? __ldcg(u + (int64_t)cc[k]) : 0.0;
+#pragma unroll
+                    for (int k = 0; k < 8; k++)
+                        if (k0 + k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
+                }
+                z[r] = sum;
+            }
+            grid_barrier(flags, W, epoch);
+        } else if (!drain) {
             const int groups = 32 / lpr, sub = lane / lpr, sl = lane % lpr;
             const int64_t stride = (int64_t)W * PC_WARPS * groups;
             for (int64_t r0 = ((int64_t)b * PC_WARPS + warp) * groups; r0 < n; r0 += stride) {
@@ -2331,8 +2357,12 @@ static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t
     const IT* ci = static_cast<const IT*>(a.col);
     const double* va = a.val;
     int lpr = a.lpr > 0 ? a.lpr : 4;
+    const int64_t* sp = a.sell_ptr;
+    const uint8_t* sl = a.sell_len;
+    const IT* sc = static_cast<const IT*>(a.sell_col);
+    const double* sv = a.sell_val;
     void* args[] = {&dd, &n, &m, &gs, (void*)&rp, (void*)&ci, (void*)&va, &lpr, &V, &ld, &z, &flags, &counter, &prof,
-                    &part};
+                    &part, (void*)&sp, (void*)&sl, (void*)&sc, (void*)&sv};
     return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(PC_THREADS), args, smem, s);
 }
 
