@@ -653,3 +653,26 @@ def test_tiny_k_and_restart_edges(P, persist, k, restart, gs, monkeypatch):
     assert g["iters"] == o["iters"] == k and g["cycles"] == o["cycles"]
     np.testing.assert_allclose(g["x"].cpu().numpy(), o["x"], rtol=1e-12, atol=1e-14)
     np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-10, atol=1e-15)
+
+
+@pytest.mark.parametrize("gs", [2, 1])
+def test_c3_full_size_full_k(P, gs):
+    """BASELINE config c3 as specified (n = 1,048,576, k = 300 unrestarted) against the
+    oracle on the same inputs: H column-normwise over the first 30 columns (reading R9),
+    final backward error within 10x (or <= 1e-14), LOO within 10x for two sweeps and within
+    the reduction-order band for one sweep (reading R19)."""
+    prob = W.config("c3")
+    g, o = run_pair(P, prob, gs, k=300, want_loo=True)
+    assert g["iters"] == o["iters"] == 300
+    d, c = _compare_cols(g["H"], o["H"], o["res_hist"])
+    floor = 0.0 if gs == 2 else oracle.column_normwise_diff(
+        oracle.gmres(prob.A, prob.b, 30, variant=VARIANT[gs], dot_block=0)["H"], o["H"][:31, :30], min(c, 30))
+    assert d <= 1e-10 or d <= 2 * floor, (d, floor)
+    normA = oracle.norm2_estimate(prob.A)
+    bg, bo = _beta(prob, g["x"].cpu().numpy(), normA), _beta(prob, o["x"], normA)
+    assert bg <= 1e-14 or bo / 10 <= bg <= 10 * bo, (bg, bo)
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    if gs == 2:
+        assert _loo_close(g["loo"], lo), (g["loo"], lo)
+    else:
+        assert lo / 100 <= g["loo"] <= 10 * lo, (g["loo"], lo)
