@@ -1,5 +1,12 @@
-import numpy as np, torch, sys
-sys.path.insert(0, '/root/repo')
+#!/usr/bin/env python3
+"""igs_op_trisolve latency for orders 1..300 (call + launch + sync), for the small-step
+forward-substitution experiments."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np, torch
 import paper_2205_07805_b200 as P
 rng = np.random.default_rng(0)
 M = 320
