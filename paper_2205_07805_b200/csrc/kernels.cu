@@ -2008,21 +2008,25 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
 
     if (tri && b == G - 2) {
         // ---------------- forward-substitution CTA ---------------------------------------
+        // also the published copy of the critical step (L row, r1, gamma, lnorm, mode
+        // words), so no worker pays for those global writes; the workers compute the same
+        // coefficients locally.  L row p-1 (for this iteration's solve) is its own earlier
+        // output.
         double* s_x = s_small + (M + 1) + (M + 2);  // small_body's s_x slot
         for (int p = 1; p <= m; p++) {
             if (tid == 0) {
                 int go = 0;
                 while (true) {
-                    if (ld_acquire_u32(flags + 5) >= (unsigned)p && ld_acquire_u32(flags + 1) + 1u >= (unsigned)p) { go = 1; break; }
-                    if (ld_acquire_u32(flags + 2) != 0u) {
-                        go = ld_acquire_u32(flags + 5) >= (unsigned)p && ld_acquire_u32(flags + 1) + 1u >= (unsigned)p;
-                        break;
-                    }
+                    if (ld_acquire_u32(flags + 5) >= (unsigned)p) { go = 1; break; }
+                    if (ld_acquire_u32(flags + 2) != 0u) { go = ld_acquire_u32(flags + 5) >= (unsigned)p; break; }
                 }
                 s_go = go;
             }
             __syncthreads();
             if (!s_go) break;
+            small_body(d, SS_CRIT, gs, p, m, s_small, red);
+            __syncthreads();
+            if (tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
             const double* dv = d.dots + (int64_t)p * d.dld;
             for (int i = tid; i < p; i += PC_THREADS) s_x[i] = __ldcg(dv + i);
             trisolve_smem(p, d.L, M, s_x);
@@ -2035,7 +2039,25 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
 
     if (split && b == G - 1) {
         // ---------------- tail CTA ---------------------------------------------------------
+        // Alg. 3 without a forward-substitution CTA: this CTA runs the published copy of the
+        // critical step (see above) as soon as the dots of p are final
+        const bool own_crit = gs == 2 && !tri;
         for (int p = 1; p <= m; p++) {
+            if (own_crit) {
+                if (tid == 0) {
+                    int go = 0;
+                    while (true) {
+                        if (ld_acquire_u32(flags + 5) >= (unsigned)p) { go = 1; break; }
+                        if (ld_acquire_u32(flags + 2) != 0u) { go = ld_acquire_u32(flags + 5) >= (unsigned)p; break; }
+                    }
+                    s_go = go;
+                }
+                __syncthreads();
+                if (!s_go) break;
+                small_body(d, SS_CRIT, gs, p, m, s_small, red);
+                __syncthreads();
+                if (tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
+            }
             if (tid == 0) {
                 int go = 0;
                 while (true) {
@@ -2213,7 +2235,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         }
         grid_barrier(flags, W, epoch);
         if (b == 0) stamp(p, 2);
-        if (tri && b == 0 && tid == 0) { __threadfence(); st_release_u32(flags + 5, (unsigned)p); }  // dots of p final
+        if (gs == 2 && split && b == 0 && tid == 0) { __threadfence(); st_release_u32(flags + 5, (unsigned)p); }  // dots of p final
         // ---- C: critical small step ----------------------------------------------------------
         // Alg. 3 (gs = 2): every worker computes the critical step from the same reduced dots
         // (bitwise the coefficients CTA 0 publishes for the tail), so no barrier separates it
@@ -2239,9 +2261,8 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             }
             __syncthreads();
             if (!s_go) break;
-            small_body(d, SS_CRIT, gs, p, m, s_small, red, /*publish=*/b == 0, /*loc=*/s_coef);
+            small_body(d, SS_CRIT, gs, p, m, s_small, red, /*publish=*/!split, /*loc=*/s_coef);
             __syncthreads();
-            if (b == 0 && tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
             if (b == 0) { stamp(p, 3); stamp(p, 4); }
             local_coef = true;
         } else {
