@@ -676,3 +676,26 @@ def test_c3_full_size_full_k(P, gs):
         assert _loo_close(g["loo"], lo), (g["loo"], lo)
     else:
         assert lo / 100 <= g["loo"] <= 10 * lo, (g["loo"], lo)
+
+
+@pytest.mark.parametrize("alg", ["igs2", "igs1", "igs2_two", "mgs"])
+@pytest.mark.parametrize("pc_max_n", ["0", "100000"])
+def test_default_paths_bitwise_reproducible(P, alg, pc_max_n, monkeypatch):
+    """two runs produce bitwise-identical H.  Every reduction on the path is
+    a fixed-order two-stage sum (no atomics on values), so two solves on two separate
+    contexts (fresh workspaces, fresh graphs) agree bit for bit -- on the graph-replayed
+    per-kernel path (IGS_PC_MAX_N=0) and on the persistent cycle kernel."""
+    import torch
+    monkeypatch.setenv("IGS_PC_MAX_N", pc_max_n)
+    prob = W.config("c3", N=96)
+    b = torch.from_numpy(prob.b).cuda()
+    runs = []
+    for _ in range(2):
+        s = P.Solver(prob.A)
+        runs.append(s.solve(b, k=90, restart=40, tol=1e-12, algorithm=alg))
+        s.close()
+    a, c = runs
+    assert a["iters"] == c["iters"] and a["cycles"] == c["cycles"]
+    assert a["H"].tobytes() == c["H"].tobytes()
+    assert a["x"].cpu().numpy().tobytes() == c["x"].cpu().numpy().tobytes()
+    assert np.asarray(a["res_hist"]).tobytes() == np.asarray(c["res_hist"]).tobytes()
