@@ -144,6 +144,7 @@ struct igs_ctx {
     int64_t n_graph_launches = 0;
     // persistent cycle kernel (small n, single GPU, Alg. 3 / Alg. 2 one sweep)
     bool pc_enabled = true;   // IGS_PERSIST=0 disables
+    bool mgs_fused = true;    // IGS_MGS_FUSED=0: MGS with separate dot and axpy kernels
     int64_t pc_max_n = 160000;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
     int64_t pc_rowsplit_n = 4096;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
@@ -650,6 +651,7 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         if (const char* e = std::getenv("IGS_FUSED")) ctx->fused_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_GRAPHS")) ctx->graphs_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PERSIST")) ctx->pc_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_MGS_FUSED")) ctx->mgs_fused = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PC_GRID")) ctx->pc_grid = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_MAX_N")) ctx->pc_max_n = std::atoll(e);
         if (const char* e = std::getenv("IGS_PC_ROWSPLIT_N")) ctx->pc_rowsplit_n = std::atoll(e);
@@ -1123,11 +1125,35 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
 
 // MGS-GMRES cycle (the sync-count baseline): column j needs j+1
 // separate inner products and one norm, each a device reduction (+ allreduce when G > 1).
+// One fused MGS step (launch_mgs_step): H = *hsrc, w -= *hsrc v (v != NULL), then
+// *out = vn . w (vn != NULL) or w . w -- one reduction, summed across ranks like bdot().
+static igs_status mgs_step(igs_ctx* ctx, const double* v, const double* vn, const double* hsrc,
+                           double* out, double* Hdst) {
+    const int64_t n = ctx->n_local;
+    const int* ist = ctx->dev_state.istate;
+    int grid = mgs_step_grid(n, ctx->num_sms);
+    grid = std::min(grid, 4 * ctx->bdot_grid - 1);
+    const double by = 8.0 * n * ((v ? 3 : 1) + (vn ? 1 : 0));
+    if (ctx->d_xchg && !ctx->capturing) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_tail, 0));
+    TIMED(IGS_K_BLOCK_DOT, by,
+          launch_mgs_step(n, v, ctx->d_z, vn, hsrc, Hdst, ctx->d_part, out, ctx->d_counter, grid,
+                          ctx->d_xchg && ctx->capturing ? nullptr : ist, ctx->d_xchg, ctx->stream));
+    ctx->n_reduce++;
+    if (ctx->d_xchg) {
+        ctx->n_allreduce++;
+        return IGS_OK;
+    }
+    return allreduce(ctx, out, 1);
+}
+
 static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0) {
     Dev& d = ctx->dev_state;
     cudaStream_t st = ctx->stream;
     const int64_t n = ctx->n_local;
     const int* ist = d.istate;
+    // fused projection + next dot (default; IGS_MGS_FUSED=0: separate dot and axpy kernels)
+    const bool fused = ctx->mgs_fused && ((uintptr_t)ctx->d_z % 16) == 0 && ((uintptr_t)ctx->d_V % 16) == 0 &&
+                       (ctx->ldv % 2) == 0;
     CUDA_TRY(cudaMemsetAsync(d.H, 0, sizeof(double) * (size_t)d.ldh * d.m, st));
     TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_PRIME_NORM, 1, 0, m, t0, st));
     TIMED(IGS_K_UPDATE, 16.0 * n,
@@ -1139,12 +1165,20 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0) {
     int* h_status = ctx->h_pinned_int + 16;
     for (int j = 0; j < m; j++) {
         TRY(spmv(ctx, Vcol(ctx, j), ctx->d_z, nullptr, false, ist, IGS_K_SPMV));
-        for (int i = 0; i <= j; i++) {
-            TRY(bdot(ctx, 0, Vcol(ctx, i), ctx->d_z, d.dots, ist, IGS_K_BLOCK_DOT));  // h = v_i . w
-            TIMED(IGS_K_UPDATE, 24.0 * n,
-                  launch_mgs_axpy(n, Vcol(ctx, i), ctx->d_z, d.dots + 1, d.H + i + (int64_t)j * d.ldh, ist, st));
+        if (fused) {
+            // h_0 = v_0 . w; then projection i fused with the next dot (or ||w||^2 after i = j)
+            TRY(mgs_step(ctx, nullptr, Vcol(ctx, 0), nullptr, d.dots + 1, nullptr));
+            for (int i = 0; i <= j; i++)
+                TRY(mgs_step(ctx, Vcol(ctx, i), i < j ? Vcol(ctx, i + 1) : nullptr, d.dots + 1 + (i & 1),
+                             i < j ? d.dots + 1 + ((i + 1) & 1) : d.dots, d.H + i + (int64_t)j * d.ldh));
+        } else {
+            for (int i = 0; i <= j; i++) {
+                TRY(bdot(ctx, 0, Vcol(ctx, i), ctx->d_z, d.dots, ist, IGS_K_BLOCK_DOT));  // h = v_i . w
+                TIMED(IGS_K_UPDATE, 24.0 * n,
+                      launch_mgs_axpy(n, Vcol(ctx, i), ctx->d_z, d.dots + 1, d.H + i + (int64_t)j * d.ldh, ist, st));
+            }
+            TRY(bdot(ctx, 0, ctx->d_z, nullptr, d.dots, ist, IGS_K_BLOCK_DOT));          // ||w||^2
         }
-        TRY(bdot(ctx, 0, ctx->d_z, nullptr, d.dots, ist, IGS_K_BLOCK_DOT));          // ||w||^2
         TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_MGS_NORM, 1, j + 1, m, t0, st));
         TIMED(IGS_K_UPDATE, 16.0 * n,
               launch_update(n, 0, ctx->d_V, ctx->ldv, ctx->d_z, nullptr, nullptr, nullptr,
@@ -1181,7 +1215,8 @@ static igs_status launch_cycle(igs_ctx* ctx, int m, int alg, int t0) {
     const bool use_graph = ctx->graphs_enabled && !ctx->timing && ctx->nranks == 1 && !ctx->force_nccl &&
                            !use_pcycle(ctx, alg) &&
                            ctx->n_local <= ((int64_t)1 << 21) && !ctx->fused_enabled &&
-                           alg != IGS_ALG_MGS && m <= 512;  // MGS: O(m^2) nodes
+                           m <= 512 &&
+                           (alg != IGS_ALG_MGS || (int64_t)m * (m + 7) / 2 <= 50000);  // MGS: O(m^2) nodes
     if (!use_graph) return run_cycle(ctx, m, alg, t0);
     // capture and replay on a private stream (the caller's may be the legacy default stream,
     // which cannot be captured); joined to the caller's stream with events

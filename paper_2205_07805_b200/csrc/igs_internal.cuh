@@ -125,6 +125,13 @@ enum SmallStage : int { SS_PRIME_NORM = 0, SS_PRIME_H = 1, SS_CRIT = 2, SS_TAIL 
 // MGS step: h = dots[1] (v_i . z); H[i,j] = h; z -= h v_i  (one projection of modified GS)
 void launch_mgs_axpy(int64_t n, const double* v, double* z, const double* hsrc, double* Hdst,
                      const int* istate, cudaStream_t s);
+// Fused MGS step (kernels.cu): H[i,j] = *hsrc; z -= *hsrc v (v != NULL); *out = vn . z, or
+// z . z when vn == NULL; deterministic, cross-rank sum fused when xc != NULL.  v, z, vn
+// 16-byte aligned; part: >= grid + 1 doubles.
+int mgs_step_grid(int64_t n, int num_sms);
+void launch_mgs_step(int64_t n, const double* v, double* z, const double* vn, const double* hsrc,
+                     double* Hdst, double* part, double* out, unsigned* counter, int grid,
+                     const int* istate, const XchgDev* xc, cudaStream_t s);
 void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s);
 
 // Algorithm 1 (Gram-Schmidt QR) small steps; q.scal[0] = gamma, q.scal[1] = 1.

@@ -1901,6 +1901,107 @@ void launch_mgs_axpy(int64_t n, const double* v, double* z, const double* hsrc, 
     mgs_axpy_kernel<<<(unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1), 256, 0, s>>>(n, v, z, hsrc, Hdst, istate);
 }
 
+// MGS projection i of column j fused with the inner product that follows it (the
+// modified Gram-Schmidt loop taken in its own order):  with h = v_i . w from the previous
+// reduction,  H[i,j] = h;  w <- w - h v_i;  then  out = v_{i+1} . w  (or w . w after the last
+// projection).  One pass over v_i, w, v_{i+1} instead of a dot pass and an axpy pass; the
+// FMA and every per-element operation are those of the two-kernel sequence.  AXPY = false:
+// the first dot of a column (no projection yet).  Each thread owns 4 rows of a 1024-row
+// chunk (two 16-byte loads per vector), grid-stride; deterministic two-stage sum: per-CTA
+// partials in a fixed tree, the last CTA to arrive sums them in CTA order with a fixed
+// per-thread split (+ across ranks over NVLink when xc != nullptr).
+constexpr int MS_THREADS = 256;
+constexpr int MS_CHUNK = 4 * MS_THREADS;
+
+template <bool AXPY, bool NORM>
+__global__ void __launch_bounds__(MS_THREADS)
+    mgs_step_kernel(int64_t n, const double* __restrict__ v, double* __restrict__ z,
+                    const double* __restrict__ vn, const double* hsrc, double* Hdst,
+                    double* __restrict__ part, double* out, unsigned* counter, const int* istate,
+                    const XchgDev* xc) {
+    if (!running(istate)) return;
+    __shared__ double red[40];
+    __shared__ bool s_last;
+    const double h = AXPY ? __ldcg(hsrc) : 0.0;
+    if (AXPY && blockIdx.x == 0 && threadIdx.x == 0) *Hdst = h;
+    double acc = 0.0;
+    const int64_t nfull = n / MS_CHUNK;
+    for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x) {
+        const int64_t r0 = c * MS_CHUNK + 2 * threadIdx.x, r1 = r0 + 2 * MS_THREADS;
+        double2 w0 = __ldcg(reinterpret_cast<const double2*>(z + r0));
+        double2 w1 = __ldcg(reinterpret_cast<const double2*>(z + r1));
+        double2 q0, q1;
+        if (!NORM) {
+            q0 = __ldg(reinterpret_cast<const double2*>(vn + r0));
+            q1 = __ldg(reinterpret_cast<const double2*>(vn + r1));
+        }
+        if (AXPY) {
+            const double2 a0 = __ldg(reinterpret_cast<const double2*>(v + r0));
+            const double2 a1 = __ldg(reinterpret_cast<const double2*>(v + r1));
+            w0.x = w0.x - h * a0.x;
+            w0.y = w0.y - h * a0.y;
+            w1.x = w1.x - h * a1.x;
+            w1.y = w1.y - h * a1.y;
+            *reinterpret_cast<double2*>(z + r0) = w0;
+            *reinterpret_cast<double2*>(z + r1) = w1;
+        }
+        if (NORM) q0 = w0, q1 = w1;
+        acc = fma(q0.x, w0.x, acc);
+        acc = fma(q0.y, w0.y, acc);
+        acc = fma(q1.x, w1.x, acc);
+        acc = fma(q1.y, w1.y, acc);
+    }
+    // ragged tail (< MS_CHUNK rows): the last CTA of the chunk loop's next round, one row per thread
+    if ((int64_t)blockIdx.x == nfull % gridDim.x) {
+        for (int64_t r = nfull * MS_CHUNK + threadIdx.x; r < n; r += MS_THREADS) {
+            double w = z[r];
+            if (AXPY) {
+                w = w - h * v[r];
+                z[r] = w;
+            }
+            acc = fma(NORM ? w : vn[r], w, acc);
+        }
+    }
+    const double s = block_sum(acc, red);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    double t = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += MS_THREADS) t += __ldcg(part + b);
+    t = block_sum(t, red);
+    if (xc) {
+        if (threadIdx.x == 0) part[gridDim.x] = t;
+        __threadfence();
+        __syncthreads();
+        final_reduce_xchg(part + gridDim.x, 1, 1, out, *xc);
+    } else if (threadIdx.x == 0) {
+        *out = t;
+    }
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
+}
+
+int mgs_step_grid(int64_t n, int num_sms) {
+    const int64_t chunks = (n + MS_CHUNK - 1) / MS_CHUNK;
+    int64_t g = (int64_t)num_sms * 4;
+    if (g > chunks) g = chunks;
+    return (int)(g < 1 ? 1 : g);
+}
+
+void launch_mgs_step(int64_t n, const double* v, double* z, const double* vn, const double* hsrc,
+                     double* Hdst, double* part, double* out, unsigned* counter, int grid,
+                     const int* istate, const XchgDev* xc, cudaStream_t s) {
+    if (v && vn)
+        mgs_step_kernel<true, false><<<grid, MS_THREADS, 0, s>>>(n, v, z, vn, hsrc, Hdst, part, out, counter, istate, xc);
+    else if (v)
+        mgs_step_kernel<true, true><<<grid, MS_THREADS, 0, s>>>(n, v, z, vn, hsrc, Hdst, part, out, counter, istate, xc);
+    else
+        mgs_step_kernel<false, false><<<grid, MS_THREADS, 0, s>>>(n, v, z, vn, hsrc, Hdst, part, out, counter, istate, xc);
+}
+
 __global__ void pack_kernel(int64_t cnt, const int64_t* __restrict__ idx,
                             const double* __restrict__ x, double* __restrict__ buf,
                             const int* istate) {

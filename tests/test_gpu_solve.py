@@ -366,7 +366,8 @@ def test_next_algorithms_restarted(P, alg):
 
 def test_cuda_graph_cycle_matches_stream_path(P, monkeypatch):
     """Small problems replay a captured CUDA graph of the whole cycle; it must give the same
-    bits as the stream-ordered path (same kernels, same order) and the same counters."""
+    bits as the stream-ordered path (same kernels, same order) and the same counters --
+    for all four algorithms (MGS: one node per projection, graphed for m(m+7)/2 <= 50000)."""
     import torch
     prob = W.config("c3", N=48)
     outs = {}
@@ -375,7 +376,8 @@ def test_cuda_graph_cycle_matches_stream_path(P, monkeypatch):
         monkeypatch.setenv("IGS_GRAPHS", graphs)
         s = P.Solver(prob.A)
         b = torch.from_numpy(prob.b).cuda()
-        outs[graphs] = [s.solve(b, k=70, restart=30, tol=1e-10, gs_iters=gs) for gs in (2, 1)]
+        outs[graphs] = [s.solve(b, k=70, restart=30, tol=1e-10, algorithm=alg)
+                        for alg in ("igs2", "igs1", "mgs", "igs2_two")]
         s.close()
     for g, u in zip(outs["1"], outs["0"]):
         assert g["iters"] == u["iters"] and g["reductions"] == u["reductions"]
@@ -699,3 +701,34 @@ def test_default_paths_bitwise_reproducible(P, alg, pc_max_n, monkeypatch):
     assert a["H"].tobytes() == c["H"].tobytes()
     assert a["x"].cpu().numpy().tobytes() == c["x"].cpu().numpy().tobytes()
     assert np.asarray(a["res_hist"]).tobytes() == np.asarray(c["res_hist"]).tobytes()
+
+
+@pytest.mark.parametrize("cfg,N", [("c1", None), ("c3", 100), ("c3", 96), ("c4", 22)])
+def test_mgs_fused_step_matches_two_kernel_mgs(P, cfg, N, monkeypatch):
+    """MGS-GMRES: the default fused step (projection i + the inner
+    product that follows it in one pass) against the two-kernel sequence (IGS_MGS_FUSED=0)
+    and the oracle.  Same per-element FMA; only the dot summation order differs.  Sizes:
+    n = 1000 (< one 1024-row chunk: all in the tail), 10000 (chunks + a 784-row tail),
+    9216 (whole chunks), 10648."""
+    import torch
+    prob = W.config(cfg, N=N) if N else W.config(cfg)
+    k = 60
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("IGS_MGS_FUSED", fused)
+        s = P.Solver(prob.A)
+        outs[fused] = s.solve(b, k=k, restart=25, tol=0.0, algorithm="mgs", want_loo=True)
+        s.close()
+    f, u = outs["1"], outs["0"]
+    assert f["iters"] == u["iters"] and f["cycles"] == u["cycles"] and f["term"] == u["term"]
+    assert f["reductions"] == u["reductions"]
+    d, c = _compare_cols(f["H"], u["H"], u["res_hist"])
+    assert d <= 1e-12, d
+    o = oracle.gmres(prob.A, prob.b, k, restart=25, tol=0.0, variant="mgs", dot_block=4096)
+    d, c = _compare_cols(f["H"], o["H"], o["res_hist"])
+    floor = oracle.column_normwise_diff(
+        oracle.gmres(prob.A, prob.b, k, restart=25, tol=0.0, variant="mgs", dot_block=0)["H"], o["H"], c)
+    assert d <= 1e-10 or d <= 2 * floor, (d, floor)
+    assert f["iters"] == o["iters"]
+    np.testing.assert_allclose(f["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-13)
