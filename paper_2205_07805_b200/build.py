@@ -47,9 +47,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         path = os.path.join(CSRC, src)
         obj = os.path.join(objdir, src + ".o")
         objs.append(obj)
-        if force or _stale(obj, [path] + hdrs):
+        log = obj + ".ptxas.txt"
+        if force or _stale(obj, [path] + hdrs) or (src.endswith(".cu") and not os.path.exists(log)):
             if src.endswith(".cu"):
-                cmd = [NVCC, *ARCH, "-lineinfo", *common, "-c", path, "-o", obj]
+                # -Xptxas -v: per-kernel registers / stack / spills kept next to the object
+                # (tests/test_build_cpu.py checks the hot kernels have no local-memory frame)
+                cmd = [NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v", *common, "-c", path, "-o", obj]
             else:
                 cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-I", INCLUDE, "-c", path, "-o", obj]
             jobs.append(cmd)
@@ -58,6 +61,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("build failed: " + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+        if "-Xptxas" in cmd:
+            with open(cmd[cmd.index("-o") + 1] + ".ptxas.txt", "w") as f:
+                f.write(r.stderr)
+            return
         if verbose and (r.stdout or r.stderr):
             print(r.stdout + r.stderr, file=sys.stderr)
 

@@ -892,8 +892,7 @@ static igs_status spmv(igs_ctx* ctx, const double* x, double* y, const double* b
         CUDA_TRY(cudaEventRecord(ctx->ev_h, ctx->hstream));
         TIMED(kind, by, {
             launch_spmv(ctx->A, x, y, b, resid, istate, ctx->stream);            // interior rows
-            cudaError_t e_ = cudaStreamWaitEvent(ctx->stream, ctx->ev_h, 0);
-            CUDA_TRY(e_);
+            CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_h, 0));
             launch_spmv_rows(ctx->A, x, y, b, resid, istate, ctx->stream);       // boundary rows
         });
         return IGS_OK;
@@ -992,9 +991,9 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         TIMED(IGS_K_PERSIST, by, {
             // row-block dots above pc_rowsplit_n rows (each CTA would otherwise re-read u, z)
             double* part = (n >= ctx->pc_rowsplit_n && grid - 1 <= ctx->bdot_grid) ? ctx->d_part : nullptr;
-            cudaError_t e_ = launch_pcycle(d, ctx->A, ctx->d_V, ctx->ldv, ctx->d_z, n, m, gs,
+            cudaError_t el_ = launch_pcycle(d, ctx->A, ctx->d_V, ctx->ldv, ctx->d_z, n, m, gs,
                                            ctx->d_counter + 4, ctx->d_counter, grid, st, ctx->d_pcprof, part);
-            CUDA_TRY(e_);
+            CUDA_TRY(el_);
         });
         if (ctx->d_pcprof) {  // IGS_PC_PROF=1: mean phase durations of this cycle to stderr
             std::vector<unsigned long long> pr((size_t)(m + 1) * 8);
@@ -1035,12 +1034,12 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
                 TRY(halo(ctx, u, ist));
                 const double by = 8.0 * n * (p + 1) + spmv_bytes(ctx);
                 TIMED(IGS_K_BLOCK_DOT, by, {
-                    cudaError_t e_ = launch_bdot_spmv(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z,
+                    cudaError_t el_ = launch_bdot_spmv(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z,
                                                       static_cast<const int32_t*>(ctx->A.rowptr),
                                                       static_cast<const int32_t*>(ctx->A.col), ctx->A.val,
                                                       ctx->A.ghost, d.dots + (int64_t)p * d.dld, ctx->d_part,
                                                       ctx->d_counter, ctx->num_sms, ist, st);
-                    CUDA_TRY(e_);
+                    CUDA_TRY(el_);
                 });
                 TRY(allreduce(ctx, d.dots + (int64_t)p * d.dld, 2 * (p + 1)));
                 ctx->n_reduce++;
@@ -1074,11 +1073,11 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             const double by = 8.0 * n * p + 32.0 * n + (dr1 ? 0.0 : spmv_bytes(ctx) - 8.0 * n);
             ctx->epoch++;
             TIMED(IGS_K_UPDATE, by, {
-                cudaError_t e_ = launch_fused(n, p, m, ctx->d_V, ctx->ldv, ctx->d_z, gs == 2 ? d.alpha : nullptr,
+                cudaError_t el_ = launch_fused(n, p, m, ctx->d_V, ctx->ldv, ctx->d_z, gs == 2 ? d.alpha : nullptr,
                                               d.beta, d.scal + SC_GAMMA, ctx->A, lag, ctx->d_flags, ctx->epoch,
                                               ctx->d_part, d.dots + (int64_t)(p + 1) * d.dld, ctx->d_counter,
                                               ist, ctx->fused_grid, st);
-                CUDA_TRY(e_);
+                CUDA_TRY(el_);
             });
             ctx->n_fused++;
             dots_ready = true;

@@ -81,7 +81,6 @@ __global__ void __launch_bounds__(256) spmv_kernel(int64_t nrows, const PT* __re
 constexpr int SPS_THREADS = 256;
 constexpr int SPS_ROWS = 256;                // rows per CTA for R = 1 (R rows per thread)
 constexpr int SPS_K = 8;                     // staged nonzeros per thread per row of R
-constexpr int SPS_CAP = SPS_ROWS * SPS_K;    // 2048 products = 16 KB of shared memory (R = 1)
 
 template <int R, typename IT, typename PT, bool GHOST, bool RESID>
 __global__ void __launch_bounds__(SPS_THREADS)
@@ -1342,7 +1341,7 @@ __device__ double block_sum(double v, double* red) {
 // Row i still subtracts L[i,j] x_j for j = 0, 1, 2, ... in natural order; warp 0 solves each
 // 32x32 diagonal block with shuffles, then every thread updates its trailing rows with 32
 // independent loads in flight.
-__device__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, double* x) {
+__device__ __forceinline__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, double* x) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __syncthreads();
     for (int kb = 0; kb < order; kb += 32) {
@@ -1378,7 +1377,7 @@ __device__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, 
 
 // Givens rotation of H column j into R, update g; thread 0 does the
 // sequential part from shared copies.  Returns |g[j+1]| to all threads.
-__device__ double givens_column(const Dev& d, int j, double* col, double* scs, double* ssn,
+__device__ __forceinline__ double givens_column(const Dev& d, int j, double* col, double* scs, double* ssn,
                                 double* red) {
     const double* Hj = d.H + (int64_t)j * d.ldh;
     for (int i = threadIdx.x; i <= j + 1; i += blockDim.x) col[i] = __ldcg(Hj + i);
@@ -1419,7 +1418,7 @@ __device__ double givens_column(const Dev& d, int j, double* col, double* scs, d
 // computed without any global write, and without the live status check, from the same
 // reduced dots -- bitwise the coefficients CTA 0 publishes; loc (shared, >= p + 3 doubles)
 // receives gamma, the update mode and beta (alpha stays in sm[0..p)).
-__device__ void small_body(const Dev& d, int stage, int gs, int p, int m, double* sm, double* red,
+__device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int p, int m, double* sm, double* red,
                            bool publish = true, double* loc = nullptr, bool r3_ready = false) {
     const int t0 = (int)__ldcg(d.scal + SC_T0);  // first global iteration of this cycle (graph-invariant)
     const int M = d.m;
@@ -1743,7 +1742,6 @@ void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStr
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(SS_THREADS) qr_small_kernel(QrDev q, int stage, int k, int m) {
     extern __shared__ double qs[];
-    __shared__ double red[40];
     const int tid = threadIdx.x;
     double* R = q.R;
     if (stage == QR_S0) {

@@ -103,3 +103,27 @@ def test_plan_random_partitions(P, seed):
             inside = (c64 >= r0) & (c64 < r1)
             assert np.array_equal(loc[inside], c64[inside] - r0)
             assert np.array_equal(loc[~inside], (r1 - r0) + np.searchsorted(ghosts, c64[~inside]))
+
+
+def test_kernels_have_no_local_memory_frame(P):
+    """ptxas -v of every .cu (written next to the objects by build.py): no kernel or device
+    function keeps a stack frame or spills.  A stack frame in the persistent cycle kernel
+    (an outlined small step) once cost Alg. 2 one sweep 2.2x in its critical step
+    (c2 22 -> 49 us per iteration), so this guards the compile, not style."""
+    from paper_2205_07805_b200 import build
+    objdir = os.path.join(ROOT, "build", "obj")
+    bad, seen = [], 0
+    for src in build.SOURCES:
+        if not src.endswith(".cu"):
+            continue
+        log = open(os.path.join(objdir, src + ".o.ptxas.txt")).read()
+        assert "warning" not in log, (src, log[:2000])
+        if "Function properties" in log:
+            assert "sm_100a" in log, src
+        for m in re.finditer(r"Function properties for (\S+)\n\s+(\d+) bytes stack frame, (\d+) bytes spill "
+                             r"stores, (\d+) bytes spill loads", log):
+            seen += 1
+            if int(m.group(2)) or int(m.group(3)) or int(m.group(4)):
+                bad.append((src, m.group(1), m.group(2), m.group(3), m.group(4)))
+    assert seen > 50, seen
+    assert not bad, bad
