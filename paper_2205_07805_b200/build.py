@@ -42,6 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "igs.h")]
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", inc]
+    common += os.environ.get("IGS_NVCC_EXTRA", "").split()  # experiment variants (-D...)
     jobs, objs = [], []
     for src in SOURCES:
         path = os.path.join(CSRC, src)

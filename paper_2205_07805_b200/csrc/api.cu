@@ -145,6 +145,8 @@ struct igs_ctx {
     // persistent cycle kernel (small n, single GPU, Alg. 3 / Alg. 2 one sweep)
     bool pc_enabled = true;   // IGS_PERSIST=0 disables
     bool mgs_fused = true;    // IGS_MGS_FUSED=0: MGS with separate dot and axpy kernels
+    bool xs_enabled = true;   // IGS_PC_XSTAGE=0: persistent kernel gathers u from L2 (long rows)
+    int pc_ntri = 0;          // IGS_PC_NTRI: forward-substitution CTAs of the persistent kernel (0 = auto)
     int64_t pc_max_n = 160000;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
     int64_t pc_rowsplit_n = 4096;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
@@ -652,6 +654,8 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         if (const char* e = std::getenv("IGS_GRAPHS")) ctx->graphs_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PERSIST")) ctx->pc_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_MGS_FUSED")) ctx->mgs_fused = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_PC_XSTAGE")) ctx->xs_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_PC_NTRI")) ctx->pc_ntri = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_GRID")) ctx->pc_grid = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_MAX_N")) ctx->pc_max_n = std::atoll(e);
         if (const char* e = std::getenv("IGS_PC_ROWSPLIT_N")) ctx->pc_rowsplit_n = std::atoll(e);
@@ -832,7 +836,7 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(long long) * (ctx->fused_grid + 1), ctx->stream));
     }
     if (!ctx->d_counter) {
-        CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 12));  // [4..8]: persistent-kernel flags
+        CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 12));  // [4..11]: persistent-kernel flags
         CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned) * 12, ctx->stream));
     }
     if (host_vec && !ctx->d_b) {
@@ -981,22 +985,29 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         const double iter_bytes = spmv_bytes(ctx) + 8.0 * n * (m + 1);
         int grid = ctx->pc_grid > 0 ? ctx->pc_grid : (int)std::ceil(iter_bytes / 32768.0) + 1;
         grid = std::max(1, std::min(grid, ctx->num_sms));
-        CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 7 * sizeof(unsigned), st));
+        CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 8 * sizeof(unsigned), st));
         if (std::getenv("IGS_PC_PROF") && !ctx->d_pcprof) {
-            CUDA_TRY(cudaMalloc(&ctx->d_pcprof, sizeof(unsigned long long) * 8 * (size_t)(ctx->dev_state.m + 2)));
+            CUDA_TRY(cudaMalloc(&ctx->d_pcprof, sizeof(unsigned long long) * 16 * (size_t)(ctx->dev_state.m + 2)));
         }
         if (ctx->d_pcprof)
-            CUDA_TRY(cudaMemsetAsync(ctx->d_pcprof, 0, sizeof(unsigned long long) * 8 * (size_t)(ctx->dev_state.m + 2), st));
+            CUDA_TRY(cudaMemsetAsync(ctx->d_pcprof, 0, sizeof(unsigned long long) * 16 * (size_t)(ctx->dev_state.m + 2), st));
         const double by = (double)m * spmv_bytes(ctx) + 16.0 * n * 0.5 * m * (m + 1);
         TIMED(IGS_K_PERSIST, by, {
             // row-block dots above pc_rowsplit_n rows (each CTA would otherwise re-read u, z)
             double* part = (n >= ctx->pc_rowsplit_n && grid - 1 <= ctx->bdot_grid) ? ctx->d_part : nullptr;
+            // long rows on the CSR phase (no SELL copy): stage u in shared memory
+            const int xs = ctx->xs_enabled && !ctx->A.sell_ptr && n <= pcycle_xs_max() &&
+                           ctx->nnz >= 32 * n;
+            // two forward-substitution CTAs on alternate iterations once the order-p solve
+            // outlasts an iteration (long cycles)
+            const int ntri = ctx->pc_ntri > 0 ? ctx->pc_ntri : (m >= 128 && grid >= 8 ? 2 : 1);
             cudaError_t el_ = launch_pcycle(d, ctx->A, ctx->d_V, ctx->ldv, ctx->d_z, n, m, gs,
-                                           ctx->d_counter + 4, ctx->d_counter, grid, st, ctx->d_pcprof, part);
+                                           ctx->d_counter + 4, ctx->d_counter, grid, st, ctx->d_pcprof, part, xs,
+                                           ntri);
             CUDA_TRY(el_);
         });
         if (ctx->d_pcprof) {  // IGS_PC_PROF=1: mean phase durations of this cycle to stderr
-            std::vector<unsigned long long> pr((size_t)(m + 1) * 8);
+            std::vector<unsigned long long> pr((size_t)(m + 2) * 16);
             CUDA_TRY(cudaMemcpyAsync(pr.data(), ctx->d_pcprof, pr.size() * 8, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
             double acc[8] = {0};
@@ -1013,6 +1024,22 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
                 std::fprintf(stderr, "[pcycle grid=%d m=%d] us/iter: A+bar %.2f  B+bar %.2f  C %.2f  bar %.2f  D %.2f  bar %.2f  | tail %.2f | total %.2f\n",
                              grid, m, acc[0] / cnt / 1e3, acc[1] / cnt / 1e3, acc[2] / cnt / 1e3, acc[3] / cnt / 1e3,
                              acc[4] / cnt / 1e3, acc[5] / cnt / 1e3, acc[6] / cnt / 1e3, acc[7] / cnt / 1e3);
+            {  // tail sub-steps (Alg. 3): H column | Givens | status | L row + Step 15 GEMV | hp store
+                double t[6] = {0};
+                int c2 = 0;
+                for (int p = 2; p < m; p++) {
+                    const unsigned long long* q = pr.data() + (size_t)(m + 2) * 8 + (size_t)p * 8;
+                    const unsigned long long* q0 = pr.data() + (size_t)p * 8;
+                    if (!q[0] || !q[5] || !q[6]) continue;
+                    for (int k = 0; k < 5; k++) t[k] += (double)(q[k + 1] - q[k]);
+                    t[5] += (double)(q[6] - q0[2]);
+                    c2++;
+                }
+                if (c2)
+                    std::fprintf(stderr, "[pcycle tail] us/iter: Hcol %.2f  givens %.2f  status %.2f  GEMV %.2f  hp %.2f | C wait %.2f\n",
+                                 t[0] / c2 / 1e3, t[1] / c2 / 1e3, t[2] / c2 / 1e3, t[3] / c2 / 1e3, t[4] / c2 / 1e3,
+                                 t[5] / c2 / 1e3);
+            }
         }
         ctx->n_pcycle++;
         ctx->n_iter += m;

@@ -90,11 +90,15 @@ void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b,
                  const int* istate, cudaStream_t s);
 
 // Persistent cycle kernel (kernels.cu): iterations 1..m of one Alg. 3 (gs = 2) or Alg. 2
-// one-sweep (gs = 1) cycle in one cooperative launch, single GPU.  flags: 7 zeroed unsigned.
+// one-sweep (gs = 1) cycle in one cooperative launch, single GPU.  flags: 8 zeroed unsigned.
+// ntri (Alg. 3): forward-substitution CTAs (1, or 2 taking alternate iterations).
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                          unsigned long long* prof = nullptr, double* part = nullptr);
-// (part != nullptr: row-block dots with grid x 2(m+1) partials, for larger n)
+                          unsigned long long* prof = nullptr, double* part = nullptr, int xs = 0,
+                          int ntri = 1);
+// (part != nullptr: row-block dots with grid x 2(m+1) partials, for larger n;
+//  xs != 0: u staged in shared memory for the CSR phase A -- n <= pcycle_xs_max())
+int64_t pcycle_xs_max();
 
 // Fused block dot: out = [V_p^T u, u.u, V_p^T z, u.z] (z != NULL) or [V_p^T u, u.u].
 // part: [grid * 2(p+1)] scratch, counter: one zeroed unsigned (reset by the kernel).

@@ -1384,11 +1384,25 @@ __device__ __forceinline__ double givens_column(const Dev& d, int j, double* col
     for (int i = threadIdx.x; i < j; i += blockDim.x) { scs[i] = __ldcg(d.cs + i); ssn[i] = __ldcg(d.sn + i); }
     __syncthreads();
     if (threadIdx.x == 0) {
+        // the rotations chain through `carry`; operands are read 8 steps ahead (the stores
+        // to col[] would otherwise order every shared load after the previous step)
         double carry = col[0];
-        for (int i = 0; i < j; i++) {
+        int i = 0;
+        for (; i + 8 <= j; i += 8) {
+            double bb[8], cc[8], ss[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) { bb[k] = col[i + k + 1]; cc[k] = scs[i + k]; ss[k] = ssn[i + k]; }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const double a = carry;
+                col[i + k] = fma(cc[k], a, ss[k] * bb[k]);
+                carry = fma(cc[k], bb[k], -ss[k] * a);
+            }
+        }
+        for (; i < j; i++) {
             const double a = carry, b = col[i + 1];
-            col[i] = scs[i] * a + ssn[i] * b;
-            carry = -ssn[i] * a + scs[i] * b;
+            col[i] = fma(scs[i], a, ssn[i] * b);
+            carry = fma(scs[i], b, -ssn[i] * a);
         }
         const double a = carry, b = col[j + 1];
         const double dd = hypot(a, b);
@@ -1419,7 +1433,16 @@ __device__ __forceinline__ double givens_column(const Dev& d, int j, double* col
 // reduced dots -- bitwise the coefficients CTA 0 publishes; loc (shared, >= p + 3 doubles)
 // receives gamma, the update mode and beta (alpha stays in sm[0..p)).
 __device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int p, int m, double* sm, double* red,
-                           bool publish = true, double* loc = nullptr, bool r3_ready = false) {
+                           bool publish = true, double* loc = nullptr, bool r3_ready = false,
+                           unsigned long long* tp = nullptr) {
+    // tp (IGS_PC_PROF=1, persistent tail): timestamps of the SS_TAIL sub-steps
+    auto tstamp = [&](int k) {
+        if (tp && threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            tp[k] = t;
+        }
+    };
     const int t0 = (int)__ldcg(d.scal + SC_T0);  // first global iteration of this cycle (graph-invariant)
     const int M = d.m;
     double* s_a = sm;               // [M+1]  r2 (Alg. 3) / a (Alg. 2)
@@ -1645,6 +1668,7 @@ __device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int 
     }
 
     // ---------------- SS_TAIL: Hessenberg column p-1, Givens, status, hp ------------------
+    tstamp(0);
     const double tol = __ldcg(d.scal + SC_TOL), nb = __ldcg(d.scal + SC_NB);
     const double gamma = __ldcg(d.gam + p);
     bool bd = __ldcg(d.cbd + p) != 0.0;
@@ -1668,7 +1692,9 @@ __device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int 
         if (tid == 0) d.H[p + (int64_t)(p - 1) * d.ldh] = gamma;
         __syncthreads();
     }
+    tstamp(1);
     const double res = givens_column(d, p - 1, s_col, s_cs, s_sn, red);
+    tstamp(2);
     const bool nonfinite = !isfinite(s) || !isfinite(res) || !isfinite(hn2) || !isfinite(gamma);
     const bool conv = tol > 0.0 && res <= tol * nb;
     if (tid == 0) {
@@ -1684,36 +1710,76 @@ __device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int 
     if (gs == 1 || nonfinite || bd || conv || drain) return;
     // Step 15, derived (reading R1): hp[:p+1, p] = r1 - H[:p+1, :p] (r2 / gamma); H is upper
     // Hessenberg, so row i only meets columns j >= i-1 (the skipped terms are exact zeros)
-    // Each row's columns are split into S contiguous chunks (S threads per row, up to 3:
-    // the thread count exceeds p + 1), partial sums combined in chunk order -- the longest
-    // dependent load chain drops from p/8 to p/(8S) L2 round trips.
+    // Work items = (32-row block, chunk of T consecutive columns): a warp's lanes are the 32
+    // rows (H is column-major: one coalesced 256-byte load per column), 16 columns in flight
+    // per lane; row block rb meets columns j >= 32 rb - 1 only, and inside it the entries
+    // below the subdiagonal are skipped (exact zeros).  T balances the items over the warps;
+    // partials are combined per row in column order.
+    tstamp(3);
     for (int j = tid; j < p; j += blockDim.x) s_t[j] = __ldcg(d.L + p + (int64_t)j * M);
     const int rows = p + 1;
-    const int S = max(1, min(3, (int)blockDim.x / rows));
-    double* s_part = s_col;  // s_col | s_cs | s_sn: 3M + 4 >= S (p + 1) doubles, free after Givens
+    double* s_part = s_col;  // s_col | s_cs | s_sn: 3M + 4 doubles, free after Givens
+    const int nrb = (rows + 31) / 32, nwarps = (int)(blockDim.x >> 5);
+    auto rb_j0 = [&](int rb) { return rb > 0 ? 32 * rb - 1 : 0; };
+    int sumlen = 0;
+    for (int rb = 0; rb < nrb; rb++) sumlen += p - rb_j0(rb);
+    int T = max(16, (sumlen + nwarps - 1) / nwarps);
+    auto items = [&](int tt) {
+        int c = 0;
+        for (int rb = 0; rb < nrb; rb++) c += (p - rb_j0(rb) + tt - 1) / tt;
+        return c;
+    };
+    while (items(T) * 32 > 3 * M + 4 && T < p) T *= 2;
+    if (T > p) T = p;
+    const int nit = items(T);
     __syncthreads();
-    for (int w = tid; w < rows * S; w += blockDim.x) {
-        const int i = w % rows, sidx = w / rows;
-        const int j0 = i > 0 ? i - 1 : 0, len = p - j0;
-        int j = j0 + len * sidx / S;
-        const int e = j0 + len * (sidx + 1) / S;
-        double sacc = 0.0;
-        for (; j + 8 <= e; j += 8) {
-            double hv[8];
-#pragma unroll
-            for (int c = 0; c < 8; c++) hv[c] = __ldcg(d.H + i + (int64_t)(j + c) * d.ldh);
-#pragma unroll
-            for (int c = 0; c < 8; c++) sacc += hv[c] * s_t[j + c];
+    if (nit * 32 > 3 * M + 4) {  // tiny M (< 14): one thread per row, columns in order
+        for (int i = tid; i < rows; i += blockDim.x) {
+            double sacc = 0.0;
+            for (int j = i > 0 ? i - 1 : 0; j < p; j++) sacc += __ldcg(d.H + i + (int64_t)j * d.ldh) * s_t[j];
+            d.HP[i + (int64_t)p * d.ldh] = __ldcg(d.r1h + (int64_t)p * (M + 2) + i) - sacc;
         }
-        for (; j < e; j++) sacc += __ldcg(d.H + i + (int64_t)j * d.ldh) * s_t[j];
-        s_part[sidx * rows + i] = sacc;
+        __syncthreads();
+        tstamp(4);
+        __syncthreads();
+        tstamp(5);
+        return;
+    }
+    for (int it = (int)(threadIdx.x >> 5); it < nit; it += nwarps) {
+        int rb = 0, base = 0;
+        for (;; rb++) {
+            const int c = (p - rb_j0(rb) + T - 1) / T;
+            if (it < base + c) break;
+            base += c;
+        }
+        const int i = 32 * rb + (tid & 31);
+        int j = rb_j0(rb) + (it - base) * T;
+        const int e = min(j + T, p);
+        double sacc = 0.0;
+        for (; j < e; j += 16) {
+            double hv[16];
+#pragma unroll
+            for (int c = 0; c < 16; c++)
+                hv[c] = (j + c < e && i < rows && i <= j + c + 1) ? __ldcg(d.H + i + (int64_t)(j + c) * d.ldh) : 0.0;
+#pragma unroll
+            for (int c = 0; c < 16; c++)
+                if (j + c < e && i <= j + c + 1) sacc += hv[c] * s_t[j + c];
+        }
+        s_part[it * 32 + (tid & 31)] = sacc;
     }
     __syncthreads();
+    tstamp(4);
     for (int i = tid; i < rows; i += blockDim.x) {
-        double sacc = s_part[i];
-        for (int k = 1; k < S; k++) sacc += s_part[k * rows + i];
+        const int rb = i >> 5;
+        int k0 = 0;
+        for (int r = 0; r < rb; r++) k0 += (p - rb_j0(r) + T - 1) / T;
+        const int k1 = k0 + (p - rb_j0(rb) + T - 1) / T;
+        double sacc = 0.0;
+        for (int k = k0; k < k1; k++) sacc += s_part[k * 32 + (i & 31)];
         d.HP[i + (int64_t)p * d.ldh] = __ldcg(d.r1h + (int64_t)p * (M + 2) + i) - sacc;
     }
+    __syncthreads();
+    tstamp(5);
 }
 
 __global__ void __launch_bounds__(SS_THREADS)
@@ -2045,12 +2111,24 @@ void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
 // flags (zeroed before launch): [0] barrier count, [1] last p whose CRIT ran, [2] p at
 // which CTA 0 stopped (0 = running), [3] last p whose TAIL ran, [4] first p whose TAIL
 // left the status not RUNNING, [5] last p whose dots are final, [6] last p whose r3 is
-// computed (forward-substitution CTA, Alg. 3).
+// computed (forward-substitution CTA, Alg. 3; [7]: the second such CTA's, odd p).
 // ------------------------------------------------------------------------------------
 constexpr int PC_THREADS = 512;
 constexpr int PC_WARPS = PC_THREADS / 32;
 constexpr int PC_CB = 8;   // dot columns per register block
-constexpr int PC_LAG = 2;  // iterations the tail CTA may trail the critical step
+#ifndef PC_LAG_ITERS
+#define PC_LAG_ITERS 2
+#endif
+constexpr int PC_LAG = PC_LAG_ITERS;  // iterations the tail CTA may trail the critical step
+#ifndef PC_XS_UNROLL
+#define PC_XS_UNROLL 8       // staged-u CSR phase: loads in flight per lane
+#endif
+#ifndef PC_XS_PRED
+#define PC_XS_PRED 0         // 1: predicated last round instead of a one-by-one remainder
+#endif
+#ifndef PC_ROW_INTERLEAVE
+#define PC_ROW_INTERLEAVE 0  // 1: row groups dealt round-robin over CTAs first
+#endif
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
@@ -2080,7 +2158,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                   const IT* __restrict__ col, const double* __restrict__ val, int lpr, double* V,
                   int64_t ld, double* z, unsigned* flags, unsigned* counter, unsigned long long* prof,
                   double* part, const int64_t* __restrict__ sell_ptr, const uint8_t* __restrict__ sell_len,
-                  const IT* __restrict__ sell_col, const double* __restrict__ sell_val) {
+                  const IT* __restrict__ sell_col, const double* __restrict__ sell_val, int xs, int ntri) {
     extern __shared__ double sm[];
     __shared__ double red[40];
     __shared__ int s_go;
@@ -2101,23 +2179,31 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     // Alg. 3 with >= 3 CTAs: CTA G-2 computes the Step 5 forward substitution r3 of iteration
     // p as soon as its dots and L row p-1 are final, ahead of the tail (which then only does
     // H, Givens and the Step 15 GEMV)
-    const bool tri = gs == 2 && G >= 3;
-    const int W = split ? G - 1 - (tri ? 1 : 0) : 1;  // worker CTAs
+    // ntri = 2: two such CTAs take alternate iterations (a forward substitution of order p
+    // per iteration is the slowest serial chain at large m); the critical-step publishes
+    // stay in iteration order (CTA t publishes CRIT(p) only after CRIT(p-1))
+    const int nt = (gs == 2 && G >= 3) ? max(1, min(ntri, G - 2)) : 0;
+    const bool tri = nt > 0;
+    const int W = split ? G - 1 - nt : 1;  // worker CTAs
     const volatile int* vist = d.istate;
 
-    if (tri && b == G - 2) {
+    if (tri && b >= G - 1 - nt && b <= G - 2) {
+        const int ti = G - 2 - b;  // this CTA takes the iterations p with p % nt == ti
         // ---------------- forward-substitution CTA ---------------------------------------
         // also the published copy of the critical step (L row, r1, gamma, lnorm, mode
         // words), so no worker pays for those global writes; the workers compute the same
         // coefficients locally.  L row p-1 (for this iteration's solve) is its own earlier
         // output.
         double* s_x = s_small + (M + 1) + (M + 2);  // small_body's s_x slot
-        for (int p = 1; p <= m; p++) {
+        for (int p = ti > 0 ? ti : nt; p <= m; p += nt) {
             if (tid == 0) {
                 int go = 0;
-                while (true) {
-                    if (ld_acquire_u32(flags + 5) >= (unsigned)p) { go = 1; break; }
-                    if (ld_acquire_u32(flags + 2) != 0u) { go = ld_acquire_u32(flags + 5) >= (unsigned)p; break; }
+                while (true) {  // dots of p final and CRIT(p-1) published
+                    if (ld_acquire_u32(flags + 5) >= (unsigned)p && ld_acquire_u32(flags + 1) + 1u >= (unsigned)p) { go = 1; break; }
+                    if (ld_acquire_u32(flags + 2) != 0u) {
+                        go = ld_acquire_u32(flags + 5) >= (unsigned)p && ld_acquire_u32(flags + 1) + 1u >= (unsigned)p;
+                        break;
+                    }
                 }
                 s_go = go;
             }
@@ -2131,7 +2217,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             trisolve_smem(p, d.L, M, s_x);
             for (int i = tid; i < p; i += PC_THREADS) d.r3h[(int64_t)p * (M + 2) + i] = s_x[i];
             __syncthreads();
-            if (tid == 0) { __threadfence(); st_release_u32(flags + 6, (unsigned)p); }
+            if (tid == 0) { __threadfence(); st_release_u32(flags + 6 + ti, (unsigned)p); }
         }
         return;
     }
@@ -2158,13 +2244,14 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                 if (tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
             }
             if (tid == 0) {
+                const unsigned* r3f = flags + 6 + (tri ? p % nt : 0);  // r3 of p: its CTA's word
                 int go = 0;
                 while (true) {
-                    if (ld_acquire_u32(flags + 1) >= (unsigned)p && (!tri || ld_acquire_u32(flags + 6) >= (unsigned)p)) { go = 1; break; }
+                    if (ld_acquire_u32(flags + 1) >= (unsigned)p && (!tri || ld_acquire_u32(r3f) >= (unsigned)p)) { go = 1; break; }
                     if (ld_acquire_u32(flags + 2) != 0u) {  // stopped: CRIT(p) may still have run
                         go = ld_acquire_u32(flags + 1) >= (unsigned)p;
                         if (go && tri)  // its r3 follows: the dots of p were final before CRIT(p)
-                            while (ld_acquire_u32(flags + 6) < (unsigned)p) {
+                            while (ld_acquire_u32(r3f) < (unsigned)p) {
                             }
                         break;
                     }
@@ -2175,7 +2262,8 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             __syncthreads();
             if (!s_go) break;
             stamp(p, 6);
-            small_body(d, SS_TAIL, gs, p, m, s_small, red, true, nullptr, /*r3_ready=*/tri);
+            small_body(d, SS_TAIL, gs, p, m, s_small, red, true, nullptr, /*r3_ready=*/tri,
+                       prof ? prof + (int64_t)(m + 2) * 8 + (int64_t)p * 8 : nullptr);
             stamp(p, 7);
             __syncthreads();
             if (tid == 0) {
@@ -2227,10 +2315,52 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         } else if (!drain) {
             const int groups = 32 / lpr, sub = lane / lpr, sl = lane % lpr;
             const int64_t stride = (int64_t)W * PC_WARPS * groups;
+            // xs (long rows, n <= PC_XS_MAX): u staged in shared memory first, so the gathers
+            // leave the per-row dependency chain (same FMA sequence per lane: bitwise equal)
+            double* s_xs = s_red + 2 * PC_WARPS * 32;
+            if (xs && (int64_t)b * groups < n) {
+                for (int64_t i = tid; i < n; i += PC_THREADS) s_xs[i] = __ldcg(u + i);
+                __syncthreads();
+            }
+            // row groups dealt round-robin over the CTAs first (warp w of CTA b takes group
+            // w W + b): consecutive rows -- similar lengths -- land on different SMs
+#if PC_ROW_INTERLEAVE
+            for (int64_t r0 = ((int64_t)warp * W + b) * groups; r0 < n; r0 += stride) {
+#else
             for (int64_t r0 = ((int64_t)b * PC_WARPS + warp) * groups; r0 < n; r0 += stride) {
+#endif
                 const int64_t r = r0 + sub;
                 double sum = 0.0;
-                if (r < n) {
+                if (r < n && xs) {
+                    const int64_t q1 = (int64_t)__ldg(rowptr + r + 1);
+                    int64_t q = (int64_t)__ldg(rowptr + r) + sl;
+#if PC_XS_PRED
+                    // PC_XS_UNROLL independent loads per lane per round trip, the last round predicated
+                    for (; q < q1; q += PC_XS_UNROLL * lpr) {
+                        int cu[PC_XS_UNROLL];
+                        double vu[PC_XS_UNROLL];
+#pragma unroll
+                        for (int k = 0; k < PC_XS_UNROLL; k++) {
+                            const bool in = q + k * lpr < q1;
+                            cu[k] = in ? (int)__ldg(col + q + k * lpr) : 0;
+                            vu[k] = in ? __ldg(val + q + k * lpr) : 0.0;
+                        }
+#pragma unroll
+                        for (int k = 0; k < PC_XS_UNROLL; k++)
+                            if (q + k * lpr < q1) sum = fma(vu[k], s_xs[cu[k]], sum);
+                    }
+#else
+                    for (; q + (PC_XS_UNROLL - 1) * lpr < q1; q += PC_XS_UNROLL * lpr) {
+                        int cu[PC_XS_UNROLL];
+                        double vu[PC_XS_UNROLL];
+#pragma unroll
+                        for (int k = 0; k < PC_XS_UNROLL; k++) { cu[k] = (int)__ldg(col + q + k * lpr); vu[k] = __ldg(val + q + k * lpr); }
+#pragma unroll
+                        for (int k = 0; k < PC_XS_UNROLL; k++) sum = fma(vu[k], s_xs[cu[k]], sum);
+                    }
+                    for (; q < q1; q += lpr) sum = fma(__ldg(val + q), s_xs[(int)__ldg(col + q)], sum);
+#endif
+                } else if (r < n) {
                     const int64_t q1 = (int64_t)__ldg(rowptr + r + 1);
                     int64_t q = (int64_t)__ldg(rowptr + r) + sl;
                     for (; q + 3 * lpr < q1; q += 4 * lpr) {
@@ -2347,6 +2477,11 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                 if (split && p > PC_LAG)
                     while (ld_acquire_u32(flags + 3) < (unsigned)(p - PC_LAG)) {
                     }
+                if (b == 0 && prof) {  // IGS_PC_PROF: end of the wait for TAIL(p - PC_LAG)
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    prof[(int64_t)(m + 2) * 8 + (int64_t)p * 8 + 6] = t;
+                }
                 int go;
                 if (split) {
                     const unsigned sa = ld_acquire_u32(flags + 4);
@@ -2449,7 +2584,8 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             if (tid == 0 && vist[ST_STATUS] == RUNNING) counter[1] += 1u;
             __syncthreads();
             stamp(p, 6);
-            small_body(d, SS_TAIL, gs, p, m, s_small, red, true, nullptr, /*r3_ready=*/tri);
+            small_body(d, SS_TAIL, gs, p, m, s_small, red, true, nullptr, /*r3_ready=*/tri,
+                       prof ? prof + (int64_t)(m + 2) * 8 + (int64_t)p * 8 : nullptr);
             stamp(p, 7);
         }
         grid_barrier(flags, W, epoch);
@@ -2460,12 +2596,14 @@ static size_t pcycle_smem(int M) {
     return small_smem(M) + (size_t)(2 * (M + 1) + 2 * PC_WARPS * 32) * sizeof(double);
 }
 
+int64_t pcycle_xs_max() { return 8192; }  // staged u: <= 64 KB of shared memory
+
 template <typename IT, typename PT>
 static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                              int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                             unsigned long long* prof, double* part) {
+                             unsigned long long* prof, double* part, int xs, int ntri) {
     auto fn = pcycle_kernel<IT, PT>;
-    const size_t smem = pcycle_smem(d.m);
+    const size_t smem = pcycle_smem(d.m) + (xs ? (size_t)n * sizeof(double) : 0);
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -2482,7 +2620,7 @@ static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t
     const IT* sc = static_cast<const IT*>(a.sell_col);
     const double* sv = a.sell_val;
     void* args[] = {&dd, &n, &m, &gs, (void*)&rp, (void*)&ci, (void*)&va, &lpr, &V, &ld, &z, &flags, &counter, &prof,
-                    &part, (void*)&sp, (void*)&sl, (void*)&sc, (void*)&sv};
+                    &part, (void*)&sp, (void*)&sl, (void*)&sc, (void*)&sv, &xs, &ntri};
     return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(PC_THREADS), args, smem, s);
 }
 
@@ -2490,13 +2628,13 @@ int pcycle_max_grid(int num_sms) { return num_sms; }
 
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                          unsigned long long* prof, double* part) {
+                          unsigned long long* prof, double* part, int xs, int ntri) {
     if (a.idx64) {
-        if (a.ptr64) return pcycle_go<int64_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
-        return pcycle_go<int64_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
+        if (a.ptr64) return pcycle_go<int64_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
+        return pcycle_go<int64_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
     }
-    if (a.ptr64) return pcycle_go<int32_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
-    return pcycle_go<int32_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part);
+    if (a.ptr64) return pcycle_go<int32_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
+    return pcycle_go<int32_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
 }
 
 }  // namespace igs

@@ -732,3 +732,61 @@ def test_mgs_fused_step_matches_two_kernel_mgs(P, cfg, N, monkeypatch):
     assert d <= 1e-10 or d <= 2 * floor, (d, floor)
     assert f["iters"] == o["iters"]
     np.testing.assert_allclose(f["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-13)
+
+
+def _ragged_long_rows(n=3000, seed=5):
+    """Seeded CSR with a wide row-length mix (1 .. ~1500 nonzeros; mean > 32), diagonally
+    weighted: exercises the resident-matrix phase of the persistent kernel (rows cut into
+    256-nonzero pieces, pieces spread over warps, CTAs balanced by nonzeros)."""
+    rng = np.random.default_rng(seed)
+    lens = np.where(rng.random(n) < 0.3, 1, rng.integers(2, 1500, n))
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        c = np.unique(np.concatenate([[i], rng.choice(n, lens[i] - 1, replace=False)]))
+        v = rng.standard_normal(c.size) / np.sqrt(lens[i])
+        v[c == i] = 1.0 + 99.0 * i / n  # spread diagonal: ~75 iterations to 1e-8
+        rows.append(c.size); cols.append(c); vals.append(v)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(rows, out=rowptr[1:])
+    A = W.Csr(n, n, 0, rowptr, np.concatenate(cols).astype(np.int32), np.concatenate(vals))
+    return A, W.matvec_ones_host(A)
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+@pytest.mark.parametrize("case", ["c2", "ragged"])
+def test_persistent_long_rows(P, case, gs, monkeypatch):
+    """Persistent kernel on long-row matrices (mean row >= 32 nonzeros, no SELL copy): the CSR
+    phase with u staged in shared memory is bitwise the L2-gather phase (IGS_PC_XSTAGE=0, same
+    FMA sequence per lane), and within the parity bar of the per-kernel path and the oracle."""
+    import torch
+    if case == "c2":
+        prob = W.config("c2"); A, bvec, k = prob.A, prob.b, 300
+    else:
+        A, bvec = _ragged_long_rows(); k = 150
+    b = torch.from_numpy(bvec).cuda()
+    outs = {}
+    for tag, env in (("xs", {"IGS_PC_XSTAGE": "1"}), ("l2", {"IGS_PC_XSTAGE": "0"}), ("pk", {"IGS_PERSIST": "0"})):
+        for key in ("IGS_PC_XSTAGE", "IGS_PERSIST"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        s = P.Solver(A)
+        s.set_timing(1)
+        outs[tag] = s.solve(b, k=k, gs_iters=gs, want_loo=True)
+        assert (s.kernel_stats()["persist"]["launches"] > 0) == (tag != "pk")
+        s.set_timing(0)
+        s.close()
+    r, u, pk = outs["xs"], outs["l2"], outs["pk"]
+    assert r["H"].tobytes() == u["H"].tobytes()
+    assert r["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+    assert r["iters"] == pk["iters"] and r["term"] == pk["term"] and r["reductions"] == pk["reductions"]
+    o = oracle.gmres(A, bvec, k, variant=VARIANT[gs], dot_block=4096, want_V=True)
+    d, c = _compare_cols(r["H"], o["H"], o["res_hist"])
+    floor = oracle.column_normwise_diff(oracle.gmres(A, bvec, k, variant=VARIANT[gs], dot_block=0)["H"], o["H"], c)
+    assert d <= 1e-10 or d <= 2 * floor, (d, floor)
+    np.testing.assert_allclose(r["res_hist"], pk["res_hist"], rtol=1e-6, atol=1e-13)
+    lo = oracle.loss_of_orthogonality(o["V"][:, :o["basis_cols"]])
+    if gs == 2:
+        assert _loo_close(r["loo"], lo), (r["loo"], lo)
+    else:
+        assert _loo_ok(W.Problem("x", A, bvec, k, 0, 0.0, ""), gs, k, r["loo"], lo), (r["loo"], lo)
