@@ -135,7 +135,10 @@ typedef struct {
     int64_t allreduces;    /* out: NCCL allreduces issued by this solve (0 when nranks == 1)  */
     int64_t reductions;    /* out: global reductions (device block dots, each followed by one
                               allreduce when nranks > 1) executed by this solve -- the paper's
-                              synchronization count                            */
+                              synchronization count.  After a convergence stop
+                              the kernel-sequence path has already run the next iteration's
+                              block dot (it overlaps the step that decides the stop): +1 there;
+                              the persistent kernel (single GPU) counts completed iterations */
     double* lnorm_hist;    /* [k+1] host or NULL: ||L||_F of the current cycle's strictly lower
                               Gram factor after iteration t (the paper's loss-of-orthogonality
                               predictor, dep^2(I+L) = ||L||_F^2); lnorm_hist[0]=0;

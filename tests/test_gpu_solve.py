@@ -790,3 +790,41 @@ def test_persistent_long_rows(P, case, gs, monkeypatch):
         assert _loo_close(r["loo"], lo), (r["loo"], lo)
     else:
         assert _loo_ok(W.Problem("x", A, bvec, k, 0, 0.0, ""), gs, k, r["loo"], lo), (r["loo"], lo)
+
+
+@pytest.mark.parametrize("grid", ["0", "4", "5"])
+@pytest.mark.parametrize("case", ["converge", "restart"])
+def test_persistent_two_forward_substitution_ctas(P, grid, case, monkeypatch):
+    """Alg. 3 with two forward-substitution CTAs on alternate iterations (IGS_PC_NTRI=2,
+    automatic for m >= 128): restarts, a convergence stop inside a cycle (the stop protocol
+    with the odd/even r3 progress words) and small grids (grid 4: one worker CTA) give the
+    per-kernel path's iterations, termination and reduction count, H within the parity bar,
+    bitwise reproducible."""
+    import torch
+    prob = W.config("c3", N=64)
+    # converge: stops at iteration 141 of a 150-column cycle; restart: three cycles, tol = 0
+    k, restart, tol = (400, 150, 1e-8) if case == "converge" else (150, 60, 0.0)
+    monkeypatch.setenv("IGS_PC_MAX_N", "100000")
+    monkeypatch.setenv("IGS_PC_GRID", grid)
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for tag, env in (("nt2", {"IGS_PC_NTRI": "2"}), ("nt1", {"IGS_PC_NTRI": "1"}), ("pk", {"IGS_PERSIST": "0"})):
+        for key in ("IGS_PC_NTRI", "IGS_PERSIST"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        s = P.Solver(prob.A)
+        outs[tag] = [s.solve(b, k=k, restart=restart, tol=tol, gs_iters=2) for _ in range(2)]
+        s.close()
+    a, pk = outs["nt2"][0], outs["pk"][0]
+    assert outs["nt2"][1]["H"].tobytes() == a["H"].tobytes()
+    assert a["iters"] == pk["iters"] == outs["nt1"][0]["iters"]
+    assert a["term"] == pk["term"] and a["cycles"] == pk["cycles"]
+    assert a["term"] == ("converged" if case == "converge" else "maxiter"), a["term"]
+    # reductions executed: after a convergence stop the stream path has already run the next
+    # iteration's block dot (it overlaps the tail that decides the stop) -- one extra
+    assert pk["reductions"] - a["reductions"] == (1 if case == "converge" else 0)
+    d, c = _compare_cols(a["H"], pk["H"], pk["res_hist"])
+    assert d <= 1e-10, d
+    np.testing.assert_allclose(a["res_hist"], pk["res_hist"], rtol=1e-6, atol=1e-13)
+    assert a["true_relres"] <= max(10 * pk["true_relres"], 1e-14)
