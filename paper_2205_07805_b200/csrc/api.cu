@@ -146,6 +146,9 @@ struct igs_ctx {
     bool pc_enabled = true;   // IGS_PERSIST=0 disables
     bool mgs_fused = true;    // IGS_MGS_FUSED=0: MGS with separate dot and axpy kernels
     bool xs_enabled = true;   // IGS_PC_XSTAGE=0: persistent kernel gathers u from L2 (long rows)
+    bool two_fused = true;    // IGS_TWO_FUSED=0: Alg. 2 two-reduce with a separate second block dot
+    double two_fused_l2 = 80e6;  // IGS_TWO_FUSED_L2_MB: L2 budget of the fused update + dot
+    bool two_tma = true;         // IGS_TWO_TMA=0: no shared-memory tile variant of the fused update + dot
     int pc_ntri = 0;          // IGS_PC_NTRI: forward-substitution CTAs of the persistent kernel (0 = auto)
     int64_t pc_max_n = 160000;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
@@ -655,6 +658,9 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         if (const char* e = std::getenv("IGS_PERSIST")) ctx->pc_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_MGS_FUSED")) ctx->mgs_fused = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PC_XSTAGE")) ctx->xs_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_TWO_FUSED")) ctx->two_fused = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_TWO_FUSED_L2_MB")) ctx->two_fused_l2 = std::atof(e) * 1e6;
+        if (const char* e = std::getenv("IGS_TWO_TMA")) ctx->two_tma = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PC_NTRI")) ctx->pc_ntri = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_GRID")) ctx->pc_grid = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_MAX_N")) ctx->pc_max_n = std::atoll(e);
@@ -1110,15 +1116,50 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             dots_ready = true;
         } else {
             const double ub = 8.0 * n * ((gs == 2 || !drain) ? p : 0) + 16.0 * n + (drain ? 0.0 : 16.0 * n);
-            TIMED(IGS_K_UPDATE, ub,
-                  launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
-                                d.beta, d.scal + SC_GAMMA, u, drain ? nullptr : Vcol(ctx, p + 1), ist, p, st));
+            // the dots re-read the CTAs' tiles from L2: fused while grid x 512 rows x p
+            // columns stays within ~80 MB (p <= 32 at 4 CTAs per SM; measured slower beyond)
+            // shared-memory tile variant (bulk copies) while two R x (p + 2) tiles fit (p <= ~103)
+            // (the L2 re-read variant is faster while its tiles fit in L2: small p first)
+            const bool fuse2_l2 = two_reduce && !drain && ctx->two_fused &&
+                                  (double)update_dot_grid(n, ctx->num_sms) * 512.0 * p * 8.0 <= ctx->two_fused_l2;
+            const bool fuse2_tma = !fuse2_l2 && two_reduce && !drain && ctx->two_fused && ctx->two_tma && p >= 1 &&
+                                   update_dot_tma_rows(p) > 0 && (ctx->ldv % 2) == 0 &&
+                                   ((uintptr_t)ctx->d_V % 16) == 0 && ((uintptr_t)u % 16) == 0 &&
+                                   ((uintptr_t)ctx->d_z % 16) == 0;
+            const bool fuse2 = fuse2_tma || fuse2_l2;
+            if (fuse2) {
+                // Alg. 2 two-reduce: the update fused with the second sweep's block dot
+                // r2 = V_{p+1}^T u' (one HBM read of V_p; the dots re-read it from L2)
+                if (ctx->d_xchg && !ctx->capturing) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
+                const int64_t ntl = fuse2_tma ? (n + update_dot_tma_rows(p) - 1) / update_dot_tma_rows(p) : 1;
+                int grid = fuse2_tma ? (int)std::min<int64_t>(ntl, ctx->num_sms) : update_dot_grid(n, ctx->num_sms);
+                const int64_t cap = (int64_t)ctx->bdot_grid * (2 * (d.m + 1) + 2) / (p + 2);
+                grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, cap));
+                const int* ist2 = ctx->d_xchg && ctx->capturing ? nullptr : ist;
+                if (fuse2_tma)
+                    TIMED(IGS_K_UPDATE, ub,
+                          launch_update_dot_tma(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
+                                                d.beta, d.scal + SC_GAMMA, u, Vcol(ctx, p + 1), ist2, p, ctx->d_part,
+                                                d.dots2, ctx->d_counter, grid, ctx->d_xchg, st));
+                else
+                    TIMED(IGS_K_UPDATE, ub,
+                          launch_update_dot(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr, d.beta,
+                                            d.scal + SC_GAMMA, u, Vcol(ctx, p + 1), ist2, p, ctx->d_part, d.dots2,
+                                            ctx->d_counter, grid, ctx->d_xchg, st));
+                ctx->n_reduce++;
+                if (ctx->d_xchg) ctx->n_allreduce++;
+                else TRY(allreduce(ctx, d.dots2, p + 2));
+            } else {
+                TIMED(IGS_K_UPDATE, ub,
+                      launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
+                                    d.beta, d.scal + SC_GAMMA, u, drain ? nullptr : Vcol(ctx, p + 1), ist, p, st));
+            }
             dots_ready = false;
             if (two_reduce && !drain) {
                 // Alg. 2 Steps 14-16: r2 = V_{p+1}^T u (second reduction), r3 = (I+L)^{-1} r2,
                 // w = u - V_{p+1} r3 (in place), H[:p+1, p] = r1 + r3
                 double* un = Vcol(ctx, p + 1);
-                TRY(bdot(ctx, p + 1, un, nullptr, d.dots2, ist, IGS_K_BLOCK_DOT));
+                if (!fuse2) TRY(bdot(ctx, p + 1, un, nullptr, d.dots2, ist, IGS_K_BLOCK_DOT));
                 TIMED(IGS_K_SMALL, 0.0, launch_small(d, SS_CRIT2, gs, p, m, t0, st));
                 TIMED(IGS_K_UPDATE, 8.0 * n * (p + 1) + 16.0 * n,
                       launch_update(n, p + 1, ctx->d_V, ctx->ldv, un, nullptr, d.alpha, nullptr,

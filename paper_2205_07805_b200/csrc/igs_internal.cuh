@@ -136,6 +136,19 @@ int mgs_step_grid(int64_t n, int num_sms);
 void launch_mgs_step(int64_t n, const double* v, double* z, const double* vn, const double* hsrc,
                      double* Hdst, double* part, double* out, unsigned* counter, int grid,
                      const int* istate, const XchgDev* xc, cudaStream_t s);
+// Alg. 2 two-reduce: first fused update + the second sweep's block dot in one pass over V_p
+// (HBM) and an L2 re-read: out = [V_p^T u', v.u', u'.u']; part >= grid (p + 2) doubles.
+int update_dot_grid(int64_t n, int num_sms);
+int update_dot_tma_rows(int p);  // tile rows of the shared-memory variant, 0: p too large
+void launch_update_dot_tma(int64_t n, int p, const double* V, int64_t ld, const double* u, const double* z,
+                           const double* alpha, const double* beta, const double* gamma_dev, double* v_out,
+                           double* u_next, const int* istate, int it, double* part, double* out,
+                           unsigned* counter, int grid, const XchgDev* xc, cudaStream_t s);
+size_t update_dot_smem(int p);
+void launch_update_dot(int64_t n, int p, const double* V, int64_t ld, const double* u, const double* z,
+                       const double* alpha, const double* beta, const double* gamma_dev, double* v_out,
+                       double* u_next, const int* istate, int it, double* part, double* out,
+                       unsigned* counter, int grid, const XchgDev* xc, cudaStream_t s);
 void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s);
 
 // Algorithm 1 (Gram-Schmidt QR) small steps; q.scal[0] = gamma, q.scal[1] = 1.

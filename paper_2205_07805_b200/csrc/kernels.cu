@@ -1118,6 +1118,346 @@ __global__ void __launch_bounds__(UP_THREADS)
 }
 
 // ------------------------------------------------------------------------------------
+// Alg. 2 two-reduce: the first fused update (Steps 7-13, as update_kernel, bitwise the same
+// v and u') fused with the second sweep's block dot r2 = V_{p+1}^T u' (Step 14)
+// and u'.u'.  Per 512-row tile each thread (two rows) computes v, u' in one pass over V_p
+// (HBM), writes them, then passes over the same V_p rows again -- an L2 re-read of the tile
+// the CTA just streamed -- for the p + 2 dots; 8 columns per butterfly (bfly8), per-warp
+// accumulators in shared memory in tile order, per-CTA partials summed by the last CTA in CTA
+// order (+ across ranks over NVLink when xc != nullptr).  One HBM read of V_p instead of two.
+// out = [V_p^T u', v.u', u'.u'] (the layout of launch_block_dot(p + 1, u', NULL)).
+// ------------------------------------------------------------------------------------
+constexpr int UD_THREADS = 256, UD_WARPS = UD_THREADS / 32, UD_TILE = 2 * UD_THREADS;
+
+template <bool HAS_ALPHA>
+__global__ void __launch_bounds__(UD_THREADS)
+    update_dot_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
+                      const double* u, const double* __restrict__ z,
+                      const double* __restrict__ alpha, const double* __restrict__ beta,
+                      const double* __restrict__ gamma_dev, double* v_out, double* u_next,
+                      const int* istate, int it, double* __restrict__ part, double* out,
+                      unsigned* counter, const XchgDev* xc) {
+    extern __shared__ double sdyn[];  // alpha[p] | beta[p+1] | acc[UD_WARPS][p+2]
+    __shared__ bool s_last;
+    if (istate) {
+        const volatile int* vs = istate;
+        const int mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
+        if ((mode & 3) != 3) return;  // the second sweep runs only after a full update
+    }
+    const int nd = p + 2;
+    double* sa = sdyn;
+    double* sb = sdyn + p;
+    double* acc = sb + p + 1 + (threadIdx.x >> 5) * nd;
+    const int lane = threadIdx.x & 31;
+    if (HAS_ALPHA)
+        for (int j = threadIdx.x; j < p; j += blockDim.x) sa[j] = alpha[j];
+    for (int j = threadIdx.x; j <= p; j += blockDim.x) sb[j] = beta[j];
+    for (int j = lane; j < nd; j += 32) acc[j] = 0.0;
+    __syncthreads();
+    const double gamma = *gamma_dev;
+    const int64_t ntiles = (n + UD_TILE - 1) / UD_TILE;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r = tile * UD_TILE + 2 * threadIdx.x;
+        const bool in = r < n, pair = r + 1 < n;
+        // ---- pass 1: exactly update_kernel's arithmetic for rows r, r+1
+        double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
+        int j = 0;
+        if (pair) {
+            for (; j + 8 <= p; j += 8) {
+                double2 v[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) v[c] = __ldg(reinterpret_cast<const double2*>(V + (int64_t)(j + c) * ld + r));
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
+                    t2.x = fma(v[c].x, sb[j + c], t2.x); t2.y = fma(v[c].y, sb[j + c], t2.y);
+                }
+            }
+        }
+        if (in) {
+            for (; j < p; j++) {
+                const double2 v = ld2_guard(V + (int64_t)j * ld, r, n);
+                if (HAS_ALPHA) { t1.x = fma(v.x, sa[j], t1.x); t1.y = fma(v.y, sa[j], t1.y); }
+                t2.x = fma(v.x, sb[j], t2.x); t2.y = fma(v.y, sb[j], t2.y);
+            }
+        }
+        double2 vv = make_double2(0.0, 0.0), un = make_double2(0.0, 0.0);
+        if (in) {
+            const double2 uu = ld2_guard(u, r, n);
+            double2 w = uu;
+            if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
+            vv.x = w.x / gamma;
+            vv.y = w.y / gamma;
+            const double2 zz = ld2_guard(z, r, n);
+            const double bp = sb[p];
+            un.x = zz.x / gamma - fma(vv.x, bp, t2.x);
+            un.y = zz.y / gamma - fma(vv.y, bp, t2.y);
+            if (!pair) { vv.y = 0.0; un.y = 0.0; }
+            u_next[r] = un.x;
+            if (pair) u_next[r + 1] = un.y;
+            v_out[r] = vv.x;
+            if (pair) v_out[r + 1] = vv.y;
+        }
+        // ---- pass 2: the p + 2 dots of the tile, 8 columns per butterfly (L2 re-read of V_p)
+        for (int cb = 0; cb < nd; cb += 8) {
+            double a[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int col = cb + c;
+                double2 x = make_double2(0.0, 0.0);
+                if (col < p) x = in ? ld2_guard(V + (int64_t)col * ld, r, n) : x;
+                else if (col == p) x = vv;
+                else if (col == p + 1) x = un;
+                a[c] = fma(x.y, un.y, x.x * un.x);
+            }
+            const double t = bfly8(a, lane);  // lane holds column cb + (lane >> 2)
+            const int col = cb + (lane >> 2);
+            if ((lane & 3) == 0 && col < nd) acc[col] += t;
+        }
+    }
+    __syncthreads();
+    // per-CTA partial: warps summed in warp order
+    for (int j = threadIdx.x; j < nd; j += blockDim.x) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < UD_WARPS; w++) t += sb[p + 1 + w * nd + j];
+        part[(int64_t)blockIdx.x * nd + j] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (xc) final_reduce_xchg(part, nd, (int)gridDim.x, out, *xc);
+    else final_reduce(part, nd, (int)gridDim.x, out);
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
+}
+
+// The same fused update + second-sweep dot with the V_p tile resident in shared memory:
+// 1 producer warp bulk-copies 128-row x p-column tiles (one 1-KB copy per column) into a
+// 2-buffer ring; consumer warps 0-1 compute v, u' for the tile's rows from shared memory
+// (update_kernel's FMA sequence: bitwise the same v, u'), then all 8 consumer warps form the
+// p + 2 dots from the same shared tile (8 columns per butterfly, R / 32 rows per lane).  One HBM
+// read of V_p and no L2 re-read; p <= update_dot_tma_max_p() (two tiles in 227 KB).
+constexpr int UT_CONS = 8, UT_THREADS = (UT_CONS + 1) * 32;
+
+// tile rows R (128 or 256) x (p V columns + u + z), two tiles in flight
+size_t update_dot_tma_smem(int p, int R) {
+    return (size_t)2 * (p + 2) * R * sizeof(double) +
+           (size_t)(2 * p + 1 + 2 * R + UT_CONS * (p + 2)) * sizeof(double) + 4 * sizeof(uint64_t);
+}
+
+int update_dot_tma_rows(int p) {  // 0: does not fit
+    if (update_dot_tma_smem(p, 256) <= 227 * 1024) return 256;
+    if (update_dot_tma_smem(p, 128) <= 227 * 1024) return 128;
+    return 0;
+}
+
+template <bool HAS_ALPHA>
+__global__ void __launch_bounds__(UT_THREADS, 1)
+    update_dot_tma_kernel(int64_t n, int p, int R, const double* __restrict__ V, int64_t ld,
+                          const double* u, const double* __restrict__ z,
+                          const double* __restrict__ alpha, const double* __restrict__ beta,
+                          const double* __restrict__ gamma_dev, double* v_out, double* u_next,
+                          const int* istate, int it, double* __restrict__ part, double* out,
+                          unsigned* counter, const XchgDev* xc) {
+    extern __shared__ __align__(16) double usm[];
+    __shared__ bool s_last;
+    if (istate) {
+        const volatile int* vs = istate;
+        const int mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
+        if ((mode & 3) != 3) return;
+    }
+    const int nd = p + 2, tcols = p + 2;  // tile columns: V_p | u | z
+    double* buf = usm;                                // [2][tcols][R]
+    double* sa = buf + (size_t)2 * tcols * R;         // [p]
+    double* sb = sa + p;                              // [p + 1]
+    double* s_v = sb + p + 1;                         // [R]
+    double* s_un = s_v + R;                           // [R]
+    double* acc = s_un + R;                           // [UT_CONS][nd]
+    uint64_t* full = reinterpret_cast<uint64_t*>(acc + UT_CONS * nd);
+    uint64_t* empty = full + 2;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int b = 0; b < 2; b++) { mbar_init(full + b, 1); mbar_init(empty + b, UT_CONS); }
+        mbar_fence_init();
+    }
+    if (HAS_ALPHA)
+        for (int j = tid; j < p; j += blockDim.x) sa[j] = alpha[j];
+    for (int j = tid; j <= p; j += blockDim.x) sb[j] = beta[j];
+    for (int j = tid; j < UT_CONS * nd; j += blockDim.x) acc[j] = 0.0;
+    __syncthreads();
+    const double gamma = *gamma_dev;
+    const int64_t ntiles = (n + R - 1) / R;
+    const int64_t nk = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    if (warp == UT_CONS) {
+        // ---------------- producer warp: one bulk copy per column (and u, z) and tile ----------
+        for (int64_t k = 0; k < nk; k++) {
+            const int b = (int)(k & 1);
+            const int64_t row0 = (blockIdx.x + k * gridDim.x) * R;
+            const int64_t rows = (n - row0 < R) ? n - row0 : R;
+            const uint32_t bytes = (uint32_t)(((rows + 1) & ~1LL) * sizeof(double));
+            mbar_wait(empty + b, (uint32_t)(((k >> 1) & 1) ^ 1));
+            if (lane == 0) mbar_arrive_expect_tx(full + b, (uint32_t)tcols * bytes);
+            __syncwarp();
+            double* dst = buf + (size_t)b * tcols * R;
+            for (int j = lane; j < tcols; j += 32) {
+                const double* src = j < p ? V + (int64_t)j * ld + row0 : (j == p ? u + row0 : z + row0);
+                bulk_g2s(dst + (size_t)j * R, src, bytes, full + b);
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        for (int64_t k = 0; k < nk; k++) {
+            const int b = (int)(k & 1);
+            const int64_t row0 = (blockIdx.x + k * gridDim.x) * R;
+            const double* tb = buf + (size_t)b * tcols * R;
+            mbar_wait(full + b, (uint32_t)((k >> 1) & 1));
+            if (tid < R / 2) {  // pass 1: rows r, r+1 -- update_kernel's arithmetic
+                const int lr = 2 * tid;
+                const int64_t r = row0 + lr;
+                const bool in = r < n, pair = r + 1 < n;
+                double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
+                if (in) {
+                    int j = 0;
+                    if (pair) {
+                        for (; j + 8 <= p; j += 8) {
+                            double2 v[8];
+#pragma unroll
+                            for (int c = 0; c < 8; c++) v[c] = *reinterpret_cast<const double2*>(tb + (size_t)(j + c) * R + lr);
+#pragma unroll
+                            for (int c = 0; c < 8; c++) {
+                                if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
+                                t2.x = fma(v[c].x, sb[j + c], t2.x); t2.y = fma(v[c].y, sb[j + c], t2.y);
+                            }
+                        }
+                    }
+                    for (; j < p; j++) {
+                        double2 v = *reinterpret_cast<const double2*>(tb + (size_t)j * R + lr);
+                        if (!pair) v.y = 0.0;
+                        if (HAS_ALPHA) { t1.x = fma(v.x, sa[j], t1.x); t1.y = fma(v.y, sa[j], t1.y); }
+                        t2.x = fma(v.x, sb[j], t2.x); t2.y = fma(v.y, sb[j], t2.y);
+                    }
+                }
+                double2 vv = make_double2(0.0, 0.0), un = make_double2(0.0, 0.0);
+                if (in) {
+                    double2 uu = *reinterpret_cast<const double2*>(tb + (size_t)p * R + lr);
+                    double2 zz = *reinterpret_cast<const double2*>(tb + (size_t)(p + 1) * R + lr);
+                    if (!pair) { uu.y = 0.0; zz.y = 0.0; }
+                    double2 w = uu;
+                    if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
+                    vv.x = w.x / gamma;
+                    vv.y = w.y / gamma;
+                    const double bp = sb[p];
+                    un.x = zz.x / gamma - fma(vv.x, bp, t2.x);
+                    un.y = zz.y / gamma - fma(vv.y, bp, t2.y);
+                    u_next[r] = un.x;
+                    v_out[r] = vv.x;
+                    if (pair) { u_next[r + 1] = un.y; v_out[r + 1] = vv.y; }
+                    else { vv.y = 0.0; un.y = 0.0; }
+                }
+                s_v[lr] = vv.x; s_v[lr + 1] = vv.y;
+                s_un[lr] = un.x; s_un[lr + 1] = un.y;
+            }
+            named_barrier(1, UT_CONS * 32);
+            // pass 2: the p + 2 dots of the tile (rows beyond n carry u' = 0 and are skipped)
+            const int64_t nrows = n - row0;
+            const int rpl = R / 32;  // rows lane, lane + 32, ... (conflict-free shared loads)
+            for (int cb = 8 * warp; cb < nd; cb += 8 * UT_CONS) {
+                double a[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) a[c] = 0.0;
+                for (int q = 0; q < rpl; q++) {
+                    const int rr = lane + 32 * q;
+                    if (rr < nrows) {
+                        const double w = s_un[rr];
+#pragma unroll
+                        for (int c = 0; c < 8; c++) {
+                            const int col = cb + c;
+                            if (col < nd) {
+                                const double* src = col < p ? tb + (size_t)col * R : (col == p ? s_v : s_un);
+                                a[c] = fma(src[rr], w, a[c]);
+                            }
+                        }
+                    }
+                }
+                const double t = bfly8(a, lane);
+                const int colx = cb + (lane >> 2);
+                if ((lane & 3) == 0 && colx < nd) acc[warp * nd + colx] += t;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + b);
+            named_barrier(1, UT_CONS * 32);  // s_v / s_un are rewritten by the next tile
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < nd; j += blockDim.x) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < UT_CONS; w++) t += acc[w * nd + j];
+        part[(int64_t)blockIdx.x * nd + j] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (xc) final_reduce_xchg(part, nd, (int)gridDim.x, out, *xc);
+    else final_reduce(part, nd, (int)gridDim.x, out);
+    if (tid == 0) { *counter = 0u; counter[1] += 1u; }
+}
+
+void launch_update_dot_tma(int64_t n, int p, const double* V, int64_t ld, const double* u, const double* z,
+                           const double* alpha, const double* beta, const double* gamma_dev, double* v_out,
+                           double* u_next, const int* istate, int it, double* part, double* out,
+                           unsigned* counter, int grid, const XchgDev* xc, cudaStream_t s) {
+    const int R = update_dot_tma_rows(p);
+    const size_t smem = update_dot_tma_smem(p, R);
+    if (alpha) {
+        cudaFuncSetAttribute(update_dot_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_dot_tma_kernel<true><<<grid, UT_THREADS, smem, s>>>(n, p, R, V, ld, u, z, alpha, beta, gamma_dev, v_out,
+                                                                   u_next, istate, it, part, out, counter, xc);
+    } else {
+        cudaFuncSetAttribute(update_dot_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_dot_tma_kernel<false><<<grid, UT_THREADS, smem, s>>>(n, p, R, V, ld, u, z, alpha, beta, gamma_dev, v_out,
+                                                                    u_next, istate, it, part, out, counter, xc);
+    }
+}
+
+int update_dot_grid(int64_t n, int num_sms) {
+    const int64_t ntiles = (n + UD_TILE - 1) / UD_TILE;
+    static int mult = -1;  // CTAs per SM (IGS_UD_CTAS, default 4)
+    if (mult < 0) {
+        const char* e = getenv("IGS_UD_CTAS");
+        mult = e ? atoi(e) : 4;
+        if (mult < 1) mult = 1;
+    }
+    int64_t g = (int64_t)num_sms * mult;
+    if (g > ntiles) g = ntiles;
+    return (int)(g < 1 ? 1 : g);
+}
+
+size_t update_dot_smem(int p) { return (size_t)(2 * p + 1 + UD_WARPS * (p + 2)) * sizeof(double); }
+
+void launch_update_dot(int64_t n, int p, const double* V, int64_t ld, const double* u, const double* z,
+                       const double* alpha, const double* beta, const double* gamma_dev, double* v_out,
+                       double* u_next, const int* istate, int it, double* part, double* out,
+                       unsigned* counter, int grid, const XchgDev* xc, cudaStream_t s) {
+    const size_t smem = update_dot_smem(p);
+    if (alpha) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(update_dot_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_dot_kernel<true><<<grid, UD_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out,
+                                                               u_next, istate, it, part, out, counter, xc);
+    } else {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(update_dot_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_dot_kernel<false><<<grid, UD_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out,
+                                                                u_next, istate, it, part, out, counter, xc);
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // K5 (sm_100a pipeline): the same fused update with V_p streamed by the bulk-copy engine,
 // as in bdot_tma_kernel: persistent CTA per SM = 8 consumer warps + 1 producer warp, 512-row
 // tiles, 8 columns x 512 rows per stage, 6-stage ring.  Consumer warp w owns rows

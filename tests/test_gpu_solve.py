@@ -828,3 +828,59 @@ def test_persistent_two_forward_substitution_ctas(P, grid, case, monkeypatch):
     assert d <= 1e-10, d
     np.testing.assert_allclose(a["res_hist"], pk["res_hist"], rtol=1e-6, atol=1e-13)
     assert a["true_relres"] <= max(10 * pk["true_relres"], 1e-14)
+
+
+@pytest.mark.parametrize("cfg,N", [("c1", None), ("c3", 100), ("c4", 22)])
+def test_two_reduce_fused_update_dot(P, cfg, N, monkeypatch):
+    """Alg. 2 two-reduce: the first update fused with the second sweep's
+    block dot (default) against the separate update + block dot (IGS_TWO_FUSED=0) and the
+    oracle.  Same v and u' arithmetic; only the r2 summation order differs.  n = 1000 (one
+    partial tile), 10000 and 10648 (ragged last tile)."""
+    import torch
+    prob = W.config(cfg, N=N) if N else W.config(cfg)
+    k = 60
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("IGS_TWO_FUSED", fused)
+        s = P.Solver(prob.A)
+        outs[fused] = s.solve(b, k=k, restart=25, tol=0.0, algorithm="igs2_two", want_loo=True)
+        s.close()
+    f, u = outs["1"], outs["0"]
+    assert f["iters"] == u["iters"] and f["cycles"] == u["cycles"] and f["reductions"] == u["reductions"]
+    d, c = _compare_cols(f["H"], u["H"], u["res_hist"])
+    assert d <= 1e-12, d
+    o = oracle.gmres(prob.A, prob.b, k, restart=25, tol=0.0, variant="igs2_two", dot_block=4096)
+    d, c = _compare_cols(f["H"], o["H"], o["res_hist"])
+    floor = oracle.column_normwise_diff(
+        oracle.gmres(prob.A, prob.b, k, restart=25, tol=0.0, variant="igs2_two", dot_block=0)["H"], o["H"], c)
+    assert d <= 1e-10 or d <= 2 * floor, (d, floor)
+    np.testing.assert_allclose(f["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-13)
+    assert _loo_close(f["loo"], u["loo"]), (f["loo"], u["loo"])
+
+
+@pytest.mark.parametrize("l2mb", ["0", "1000"])
+def test_two_reduce_fused_variants(P, l2mb, monkeypatch):
+    """Both fused update + dot kernels of Alg. 2 two-reduce on every iteration of a
+    100-column cycle: IGS_TWO_FUSED_L2_MB=0 forces the shared-memory tile variant (tile rows
+    256 while p <= 52, then 128; ragged last tile), 1000 the L2 re-read variant; both within
+    the parity bar of the unfused path (IGS_TWO_FUSED=0) and of each other."""
+    import torch
+    prob = W.config("c4", N=22)  # n = 10648
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for tag, env in (("f", {"IGS_TWO_FUSED_L2_MB": l2mb}), ("u", {"IGS_TWO_FUSED": "0"})):
+        for key in ("IGS_TWO_FUSED_L2_MB", "IGS_TWO_FUSED"):
+            monkeypatch.delenv(key, raising=False)
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        monkeypatch.setenv("IGS_GRAPHS", "0")
+        s = P.Solver(prob.A)
+        outs[tag] = s.solve(b, k=100, restart=0, tol=0.0, algorithm="igs2_two", want_loo=True)
+        s.close()
+    f, u = outs["f"], outs["u"]
+    assert f["iters"] == u["iters"] == 100 and f["reductions"] == u["reductions"]
+    d, c = _compare_cols(f["H"], u["H"], u["res_hist"])
+    assert d <= 1e-12, d
+    assert _loo_close(f["loo"], u["loo"]), (f["loo"], u["loo"])
+    np.testing.assert_allclose(f["res_hist"], u["res_hist"], rtol=1e-6, atol=1e-13)
