@@ -1120,9 +1120,12 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             // columns stays within ~80 MB (p <= 32 at 4 CTAs per SM; measured slower beyond)
             // shared-memory tile variant (bulk copies) while two R x (p + 2) tiles fit (p <= ~103)
             // (the L2 re-read variant is faster while its tiles fit in L2: small p first)
-            const bool fuse2_l2 = two_reduce && !drain && ctx->two_fused &&
+            // (small n: the separate block dot spreads the columns over more CTAs -- c2 was
+            // 7.6K vs 9.6K it/s fused -- so fuse only with at least one 512-row tile per SM)
+            const bool fuse2_l2 = two_reduce && !drain && ctx->two_fused && n >= (int64_t)ctx->num_sms * 512 &&
                                   (double)update_dot_grid(n, ctx->num_sms) * 512.0 * p * 8.0 <= ctx->two_fused_l2;
             const bool fuse2_tma = !fuse2_l2 && two_reduce && !drain && ctx->two_fused && ctx->two_tma && p >= 1 &&
+                                   n >= (int64_t)ctx->num_sms * 512 &&
                                    update_dot_tma_rows(p) > 0 && (ctx->ldv % 2) == 0 &&
                                    ((uintptr_t)ctx->d_V % 16) == 0 && ((uintptr_t)u % 16) == 0 &&
                                    ((uintptr_t)ctx->d_z % 16) == 0;

@@ -830,12 +830,12 @@ def test_persistent_two_forward_substitution_ctas(P, grid, case, monkeypatch):
     assert a["true_relres"] <= max(10 * pk["true_relres"], 1e-14)
 
 
-@pytest.mark.parametrize("cfg,N", [("c1", None), ("c3", 100), ("c4", 22)])
+@pytest.mark.parametrize("cfg,N", [("c3", 300), ("c4", 47)])
 def test_two_reduce_fused_update_dot(P, cfg, N, monkeypatch):
     """Alg. 2 two-reduce: the first update fused with the second sweep's
     block dot (default) against the separate update + block dot (IGS_TWO_FUSED=0) and the
-    oracle.  Same v and u' arithmetic; only the r2 summation order differs.  n = 1000 (one
-    partial tile), 10000 and 10648 (ragged last tile)."""
+    oracle.  Same v and u' arithmetic; only the r2 summation order differs.  n = 90000 and
+    103823 (odd: ragged last tile); fused from one 512-row tile per SM up."""
     import torch
     prob = W.config(cfg, N=N) if N else W.config(cfg)
     k = 60
@@ -866,7 +866,7 @@ def test_two_reduce_fused_variants(P, l2mb, monkeypatch):
     256 while p <= 52, then 128; ragged last tile), 1000 the L2 re-read variant; both within
     the parity bar of the unfused path (IGS_TWO_FUSED=0) and of each other."""
     import torch
-    prob = W.config("c4", N=22)  # n = 10648
+    prob = W.config("c4", N=47)  # n = 103823: ragged, above the fusion threshold
     b = torch.from_numpy(prob.b).cuda()
     outs = {}
     for tag, env in (("f", {"IGS_TWO_FUSED_L2_MB": l2mb}), ("u", {"IGS_TWO_FUSED": "0"})):
