@@ -1236,7 +1236,7 @@ __global__ void __launch_bounds__(UD_THREADS)
 
 // The same fused update + second-sweep dot with the V_p tile resident in shared memory:
 // 1 producer warp bulk-copies 128-row x p-column tiles (one 1-KB copy per column) into a
-// 2-buffer ring; consumer warps 0-1 compute v, u' for the tile's rows from shared memory
+// 2-buffer ring; consumer threads (one per tile row) compute v, u' from shared memory
 // (update_kernel's FMA sequence: bitwise the same v, u'), then all 8 consumer warps form the
 // p + 2 dots from the same shared tile (8 columns per butterfly, R / 32 rows per lane).  One HBM
 // read of V_p and no L2 re-read; p <= update_dot_tma_max_p() (two tiles in 227 KB).
@@ -1314,51 +1314,26 @@ __global__ void __launch_bounds__(UT_THREADS, 1)
             const int64_t row0 = (blockIdx.x + k * gridDim.x) * R;
             const double* tb = buf + (size_t)b * tcols * R;
             mbar_wait(full + b, (uint32_t)((k >> 1) & 1));
-            if (tid < R / 2) {  // pass 1: rows r, r+1 -- update_kernel's arithmetic
-                const int lr = 2 * tid;
-                const int64_t r = row0 + lr;
-                const bool in = r < n, pair = r + 1 < n;
-                double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
-                if (in) {
-                    int j = 0;
-                    if (pair) {
-                        for (; j + 8 <= p; j += 8) {
-                            double2 v[8];
-#pragma unroll
-                            for (int c = 0; c < 8; c++) v[c] = *reinterpret_cast<const double2*>(tb + (size_t)(j + c) * R + lr);
-#pragma unroll
-                            for (int c = 0; c < 8; c++) {
-                                if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
-                                t2.x = fma(v[c].x, sb[j + c], t2.x); t2.y = fma(v[c].y, sb[j + c], t2.y);
-                            }
-                        }
+            if (tid < R) {  // pass 1: row r -- update_kernel's per-row FMA sequence (bitwise equal)
+                const int64_t r = row0 + tid;
+                double vv = 0.0, un = 0.0;
+                if (r < n) {
+                    double t1 = 0.0, t2 = 0.0;
+#pragma unroll 8
+                    for (int j = 0; j < p; j++) {
+                        const double v = tb[(size_t)j * R + tid];
+                        if (HAS_ALPHA) t1 = fma(v, sa[j], t1);
+                        t2 = fma(v, sb[j], t2);
                     }
-                    for (; j < p; j++) {
-                        double2 v = *reinterpret_cast<const double2*>(tb + (size_t)j * R + lr);
-                        if (!pair) v.y = 0.0;
-                        if (HAS_ALPHA) { t1.x = fma(v.x, sa[j], t1.x); t1.y = fma(v.y, sa[j], t1.y); }
-                        t2.x = fma(v.x, sb[j], t2.x); t2.y = fma(v.y, sb[j], t2.y);
-                    }
+                    const double uu = tb[(size_t)p * R + tid], zz = tb[(size_t)(p + 1) * R + tid];
+                    const double w = HAS_ALPHA ? uu - t1 : uu;
+                    vv = w / gamma;
+                    un = zz / gamma - fma(vv, sb[p], t2);
+                    u_next[r] = un;
+                    v_out[r] = vv;
                 }
-                double2 vv = make_double2(0.0, 0.0), un = make_double2(0.0, 0.0);
-                if (in) {
-                    double2 uu = *reinterpret_cast<const double2*>(tb + (size_t)p * R + lr);
-                    double2 zz = *reinterpret_cast<const double2*>(tb + (size_t)(p + 1) * R + lr);
-                    if (!pair) { uu.y = 0.0; zz.y = 0.0; }
-                    double2 w = uu;
-                    if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
-                    vv.x = w.x / gamma;
-                    vv.y = w.y / gamma;
-                    const double bp = sb[p];
-                    un.x = zz.x / gamma - fma(vv.x, bp, t2.x);
-                    un.y = zz.y / gamma - fma(vv.y, bp, t2.y);
-                    u_next[r] = un.x;
-                    v_out[r] = vv.x;
-                    if (pair) { u_next[r + 1] = un.y; v_out[r + 1] = vv.y; }
-                    else { vv.y = 0.0; un.y = 0.0; }
-                }
-                s_v[lr] = vv.x; s_v[lr + 1] = vv.y;
-                s_un[lr] = un.x; s_un[lr + 1] = un.y;
+                s_v[tid] = vv;
+                s_un[tid] = un;
             }
             named_barrier(1, UT_CONS * 32);
             // pass 2: the p + 2 dots of the tile (rows beyond n carry u' = 0 and are skipped)
