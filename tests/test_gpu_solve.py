@@ -522,16 +522,21 @@ def test_persistent_cycle_kernel(P, cfg, grid, gs, monkeypatch):
 
 
 @pytest.mark.parametrize("alg", ["igs2", "igs1", "igs2_two", "mgs"])
-@pytest.mark.parametrize("cfg", ["c3s", "c3m"])
+@pytest.mark.parametrize("cfg", ["c3s", "c3m", "c4_47"])
 def test_fused_block_dot_allreduce_one_rank(P, cfg, alg, monkeypatch):
     """IGS_XCHG=1: the block dot's last CTA sums across ranks through an NCCL symmetric window
     and an LSA barrier (device API) instead of a separate ncclAllReduce.  On one GPU the
     communicator has one rank, so the result must be bit-identical to the plain path, with
     one exchange per block dot."""
     import torch
-    prob = W.config("c3", N=48 if cfg == "c3s" else 128)
+    # c4_47 (n = 103823): the fused MGS step and both fused two-reduce update + dot kernels
+    # finish through the exchange as well
+    prob = W.config("c4", N=47) if cfg == "c4_47" else W.config("c3", N=48 if cfg == "c3s" else 128)
     b = torch.from_numpy(prob.b).cuda()
     k, restart = (60, 25) if alg != "mgs" else (30, 15)
+    if cfg == "c4_47" and alg == "igs2_two":
+        k, restart = 80, 80  # the L2 variant to p = 48 (40 MB budget), shared-memory tiles beyond
+        monkeypatch.setenv("IGS_TWO_FUSED_L2_MB", "40")
     outs = {}
     for x in ("1", "0"):
         monkeypatch.setenv("IGS_XCHG", x)
