@@ -993,10 +993,10 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         grid = std::max(1, std::min(grid, ctx->num_sms));
         CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 4, 0, 8 * sizeof(unsigned), st));
         if (std::getenv("IGS_PC_PROF") && !ctx->d_pcprof) {
-            CUDA_TRY(cudaMalloc(&ctx->d_pcprof, sizeof(unsigned long long) * 16 * (size_t)(ctx->dev_state.m + 2)));
+            CUDA_TRY(cudaMalloc(&ctx->d_pcprof, sizeof(unsigned long long) * 24 * (size_t)(ctx->dev_state.m + 2)));
         }
         if (ctx->d_pcprof)
-            CUDA_TRY(cudaMemsetAsync(ctx->d_pcprof, 0, sizeof(unsigned long long) * 16 * (size_t)(ctx->dev_state.m + 2), st));
+            CUDA_TRY(cudaMemsetAsync(ctx->d_pcprof, 0, sizeof(unsigned long long) * 24 * (size_t)(ctx->dev_state.m + 2), st));
         const double by = (double)m * spmv_bytes(ctx) + 16.0 * n * 0.5 * m * (m + 1);
         TIMED(IGS_K_PERSIST, by, {
             // row-block dots above pc_rowsplit_n rows (each CTA would otherwise re-read u, z)
@@ -1013,7 +1013,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             CUDA_TRY(el_);
         });
         if (ctx->d_pcprof) {  // IGS_PC_PROF=1: mean phase durations of this cycle to stderr
-            std::vector<unsigned long long> pr((size_t)(m + 2) * 16);
+            std::vector<unsigned long long> pr((size_t)(m + 2) * 24);
             CUDA_TRY(cudaMemcpyAsync(pr.data(), ctx->d_pcprof, pr.size() * 8, cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
             double acc[8] = {0};
@@ -1041,6 +1041,17 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
                     t[5] += (double)(q[6] - q0[2]);
                     c2++;
                 }
+                double cr[3] = {0};
+                int c3n = 0;
+                for (int p = 2; p < m; p++) {  // Alg. 2 one sweep, CTA 0's critical step
+                    const unsigned long long* q = pr.data() + (size_t)(m + 2) * 16 + (size_t)p * 8;
+                    if (!q[0] || !q[3]) continue;
+                    for (int k = 0; k < 3; k++) cr[k] += (double)(q[k + 1] - q[k]);
+                    c3n++;
+                }
+                if (c3n)
+                    std::fprintf(stderr, "[pcycle crit] us/iter: pre %.2f  trisolve %.2f  post %.2f\n",
+                                 cr[0] / c3n / 1e3, cr[1] / c3n / 1e3, cr[2] / c3n / 1e3);
                 if (c2)
                     std::fprintf(stderr, "[pcycle tail] us/iter: Hcol %.2f  givens %.2f  status %.2f  GEMV %.2f  hp %.2f | C wait %.2f\n",
                                  t[0] / c2 / 1e3, t[1] / c2 / 1e3, t[2] / c2 / 1e3, t[3] / c2 / 1e3, t[4] / c2 / 1e3,

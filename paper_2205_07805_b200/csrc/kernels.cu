@@ -1883,6 +1883,7 @@ __device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int 
 
     if (stage == SS_CRIT) {
         // ---------------- critical path of iteration p (feeds the fused update) ----------
+        tstamp(0);
         for (int i = tid; i < p; i += blockDim.x) s_a[i] = __ldcg(dv + i);
         if (!drain) for (int i = tid; i <= p; i += blockDim.x) s_c[i] = __ldcg(dv + p + 1 + i);
         double gamma, lrow2 = 0.0;
@@ -1973,11 +1974,15 @@ __device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int 
             for (int i = tid; i < p; i += blockDim.x) d.L[p + (int64_t)i * M] = s_a[i] / gamma;
             __threadfence_block();
             // Step 12: r1 = (I + L_{p+1})^{-1} c ; Step 17 (r3 = 0): H[:p+1, p] = r1
+            tstamp(1);
             trisolve_smem(p + 1, d.L, M, s_x);
+            tstamp(2);
             for (int i = tid; i <= p; i += blockDim.x) {
                 d.beta[i] = s_x[i];
                 d.H[i + (int64_t)p * d.ldh] = s_x[i];
             }
+            __syncthreads();
+            tstamp(3);
         }
         return;
     }
@@ -2825,7 +2830,8 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                 }
                 __syncthreads();
                 if (s_go) {
-                    small_body(d, SS_CRIT, gs, p, m, s_small, red);
+                    small_body(d, SS_CRIT, gs, p, m, s_small, red, true, nullptr, false,
+                               prof ? prof + (int64_t)(m + 2) * 16 + (int64_t)p * 8 : nullptr);
                     __syncthreads();
                     if (tid == 0) { __threadfence(); st_release_u32(flags + 1, (unsigned)p); }
                 }
