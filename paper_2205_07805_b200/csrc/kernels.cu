@@ -1656,8 +1656,63 @@ __device__ double block_sum(double v, double* red) {
 // Row i still subtracts L[i,j] x_j for j = 0, 1, 2, ... in natural order; warp 0 solves each
 // 32x32 diagonal block with shuffles, then every thread updates its trailing rows with 32
 // independent loads in flight.
+#ifndef TRISOLVE_LOOKAHEAD
+#define TRISOLVE_LOOKAHEAD 1
+#endif
 __device__ __forceinline__ void trisolve_smem(int order, const double* __restrict__ L, int ldl, double* x) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#if TRISOLVE_LOOKAHEAD
+    // Lookahead schedule (blockDim >= 96): at step k warp 1 applies block k-1 to the rows of
+    // block k only while warp 0 loads block k's diagonal L entries; then warp 0 runs the
+    // 32-step shuffle chain.  Meanwhile warps 2.. apply block k-1 to the rows below block k.
+    // Every row still receives the blocks' contributions in ascending order with the same
+    // FMA sequence as the right-looking loop (#else), so the result is bitwise the same; the
+    // step's critical path loses the second dependent L2 round trip.
+    __syncthreads();
+    for (int kb = 0; kb < order; kb += 32) {
+        const int nb = min(32, order - kb);
+        if (warp <= 1) {
+            const int i = kb + lane;
+            if (warp == 1) {
+                if (kb > 0 && lane < nb) {  // block k-1 (full: only the last block is partial)
+                    double lv[32];
+#pragma unroll
+                    for (int j = 0; j < 32; j++) lv[j] = __ldcg(L + i + (int64_t)(kb - 32 + j) * ldl);
+                    double sacc = x[i];
+#pragma unroll
+                    for (int j = 0; j < 32; j++) sacc = sacc - lv[j] * x[kb - 32 + j];
+                    x[i] = sacc;
+                }
+                named_barrier(2, 64);
+            } else {
+                const bool mine = lane < nb;
+                double lrow[32];
+#pragma unroll
+                for (int j = 0; j < 32; j++)
+                    lrow[j] = (mine && j < lane) ? __ldcg(L + (kb + lane) + (int64_t)(kb + j) * ldl) : 0.0;
+                named_barrier(2, 64);
+                double xi = mine ? x[kb + lane] : 0.0;
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const double xj = __shfl_sync(FULL_MASK, xi, j);
+                    if (j < lane) xi = xi - lrow[j] * xj;
+                }
+                if (mine) x[kb + lane] = xi;
+            }
+        } else if (kb > 0) {
+            for (int i = kb + nb + (int)threadIdx.x - 64; i < order; i += (int)blockDim.x - 64) {
+                double lv[32];
+#pragma unroll
+                for (int j = 0; j < 32; j++) lv[j] = __ldcg(L + i + (int64_t)(kb - 32 + j) * ldl);
+                double sacc = x[i];
+#pragma unroll
+                for (int j = 0; j < 32; j++) sacc = sacc - lv[j] * x[kb - 32 + j];
+                x[i] = sacc;
+            }
+        }
+        __syncthreads();
+    }
+#else
     __syncthreads();
     for (int kb = 0; kb < order; kb += 32) {
         const int nb = min(32, order - kb);
@@ -1688,6 +1743,7 @@ __device__ __forceinline__ void trisolve_smem(int order, const double* __restric
         }
         __syncthreads();
     }
+#endif
 }
 
 // Givens rotation of H column j into R, update g; thread 0 does the
