@@ -2503,7 +2503,7 @@ constexpr int PC_LAG = PC_LAG_ITERS;  // iterations the tail CTA may trail the c
 #define PC_XS_PRED 0         // 1: predicated last round instead of a one-by-one remainder
 #endif
 #ifndef PC_ROW_INTERLEAVE
-#define PC_ROW_INTERLEAVE 0  // 1: row groups dealt round-robin over CTAs first
+#define PC_ROW_INTERLEAVE 1  // row groups dealt round-robin over CTAs first (0: CTA-contiguous)
 #endif
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
