@@ -889,3 +889,34 @@ def test_two_reduce_fused_variants(P, l2mb, monkeypatch):
     assert d <= 1e-12, d
     assert _loo_close(f["loo"], u["loo"]), (f["loo"], u["loo"])
     np.testing.assert_allclose(f["res_hist"], u["res_hist"], rtol=1e-6, atol=1e-13)
+
+
+@pytest.mark.parametrize("persist", ["1", "0"])
+@pytest.mark.parametrize("alg", ["igs2", "igs1", "igs2_two", "mgs"])
+@pytest.mark.parametrize("n", [3, 4, 5, 33])
+def test_tiny_systems(P, n, alg, persist, monkeypatch):
+    """Degenerate sizes: the largest cycle the method allows (k = n - 2) on n = 3, 4,
+    5 and one row past a warp, every algorithm, persistent and kernel paths: same iterations
+    and termination as the oracle, H within the parity bar, the Arnoldi residual history
+    within 1e-6 relative; k >= n - 1 is rejected with a status code."""
+    import torch
+    monkeypatch.setenv("IGS_PERSIST", persist)
+    rng = np.random.default_rng(100 + n)
+    D = np.triu(rng.standard_normal((n, n)), 1) * 0.3 + np.diag(1.0 + np.arange(n))
+    A = W.dense_to_csr(D, keep_zeros_upper=True)
+    b = rng.standard_normal(n)
+    k = n - 2
+    s = P.Solver(A)
+    bt = torch.from_numpy(b).cuda()
+    g = s.solve(bt, k=k, algorithm=alg)
+    with pytest.raises(P.IgsError):
+        s.solve(bt, k=n - 1, algorithm=alg)
+    s.close()
+    o = oracle.gmres(A, b, k, variant=ALG_ORACLE[alg])
+    assert g["iters"] == o["iters"] and g["term"] == o["term"], (g["iters"], o["iters"], g["term"], o["term"])
+    d, c = _compare_cols(g["H"], o["H"], o["res_hist"])
+    # one sweep / MGS: the oracle's own H moves with the reduction order (eps kappa(B_k),
+    # reading R19) -- the bar is 10x that spread (blocks of 8 vs sequential dots)
+    floor = oracle.column_normwise_diff(oracle.gmres(A, b, k, variant=ALG_ORACLE[alg], dot_block=8)["H"], o["H"], c)
+    assert d <= max(1e-10, 10 * floor), (d, floor)
+    np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-14)
