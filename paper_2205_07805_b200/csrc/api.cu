@@ -150,7 +150,7 @@ struct igs_ctx {
     double two_fused_l2 = 80e6;  // IGS_TWO_FUSED_L2_MB: L2 budget of the fused update + dot
     bool two_tma = true;         // IGS_TWO_TMA=0: no shared-memory tile variant of the fused update + dot
     int pc_ntri = 0;          // IGS_PC_NTRI: forward-substitution CTAs of the persistent kernel (0 = auto)
-    int64_t pc_max_n = 160000;  // crossover vs the graph-replayed per-kernel path
+    int64_t pc_max_n = 190000;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
     int64_t pc_rowsplit_n = 4096;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
     int64_t n_pcycle = 0;
