@@ -139,10 +139,16 @@ typedef struct {
                               the kernel-sequence path has already run the next iteration's
                               block dot (it overlaps the step that decides the stop): +1 there;
                               the persistent kernel (single GPU) counts completed iterations */
-    double* lnorm_hist;    /* [k+1] host or NULL: ||L||_F of the current cycle's strictly lower
-                              Gram factor after iteration t (the paper's loss-of-orthogonality
-                              predictor, dep^2(I+L) = ||L||_F^2); lnorm_hist[0]=0;
-                              entries restart at each cycle; NaN for MGS (no L)               */
+    double* lnorm_hist;    /* [k+1] host or NULL: ||L||_F of the algorithm's own correction
+                              matrix L after iteration t (entries restart at each cycle;
+                              lnorm_hist[0] = 0; NaN for MGS, which has no L).  gs_iters = 1
+                              (Alg. 2 one sweep): L rows are a/gamma = the strictly lower part
+                              of the computed basis' Gram V^T V, i.e. the paper's
+                              L_k and dep^2(I+L_k) = ||L_k||_F^2.
+                              gs_iters = 2 (Alg. 3): L rows are Step 9's r2/gamma, the
+                              Gram of each vector BEFORE its second sweep (reading R4) -- not the
+                              basis' Gram; lgram_frob below is the paper's L_k of the final
+                              basis for every algorithm.                                      */
     int want_basis_diag;   /* in: compute s_norm and sigma_min of the final basis (NaN when it
                               has more than IGS_BASIS_DIAG_MAX columns)                       */
     double s_norm;         /* out: ||S||_2, S = (I + U)^{-1} U, U = strictly upper part of
@@ -150,6 +156,9 @@ typedef struct {
                               if !want_basis_diag                                             */
     double sigma_min;      /* out: sigma_min(V) = sqrt(lambda_min(V^T V)) (reading R23); NaN
                               if !want_basis_diag                                             */
+    double lgram_frob;     /* out: ||L_k||_F, L_k = strictly lower part of V^T V of the final
+                              basis (dep^2(I+L_k)), from the same Gram as
+                              loo_frob; NaN unless want_loo or want_basis_diag              */
 } igs_result;
 
 /* Solve A x = b by restarted IGS-GMRES.
@@ -185,6 +194,32 @@ igs_status igs_set_timing(igs_ctx* ctx, int on);
 igs_status igs_kernel_stats(const igs_ctx* ctx, int kind, double* ms, int64_t* launches,
                             double* bytes);
 
+/* Facts about a context (for harnesses and tests): *value for key. */
+typedef enum {
+    IGS_INFO_XCHG = 0,             /* 1: reductions finish through the fused NVLink exchange
+                                      (set up by the first solve), 0: ncclAllReduce / none */
+    IGS_INFO_NRANKS = 1,           /* communicator size G                                   */
+    IGS_INFO_NGHOST = 2,           /* ghost entries received per SpMV (halo, G > 1)         */
+    IGS_INFO_NSEND = 3,            /* entries sent per SpMV                                 */
+    IGS_INFO_NPEERS = 4,           /* halo peers                                            */
+    IGS_INFO_NBND = 5,             /* boundary rows (multiplied after the halo)             */
+    IGS_INFO_GRAPH_LAUNCHES = 6,   /* restart cycles replayed from CUDA graphs              */
+    IGS_INFO_PCYCLE_LAUNCHES = 7,  /* restart cycles run by the persistent kernel           */
+    IGS_INFO_SELL = 8,             /* 1: the SpMV uses the SELL-32 copy of A               */
+    IGS_INFO_CSR_COMPACT = 9       /* 1: the CSR arrays hold only the boundary rows         */
+} igs_info_key;
+igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value);
+
+/* Failure detection.  With a communicator (nranks > 1, or the 1-rank test
+ * communicators), every host wait of igs_create / igs_solve polls ncclCommGetAsyncError and
+ * gives up after `seconds` without progress; the fused exchange's device barrier is bounded
+ * by the same time.  Either failure aborts the communicator (ncclCommAbort) and returns
+ * IGS_ERR_NCCL with the reason in igs_last_error(); later solves on the context return
+ * IGS_ERR_STATE and only igs_destroy is valid.  Default 120 s (env IGS_NCCL_TIMEOUT_S at
+ * create).  Test hook: env IGS_TEST_XCHG_STALL=c makes exchange number c wait for a peer
+ * epoch that never arrives (exercises the device timeout on one GPU). */
+igs_status igs_set_timeout(igs_ctx* ctx, double seconds);
+
 igs_status igs_destroy(igs_ctx* ctx);
 const char* igs_last_error(void);
 
@@ -199,6 +234,13 @@ const char* igs_last_error(void);
  * u, z: n.  Deterministic (fixed two-stage reduction, no FP atomics). */
 igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                             const double* z, double* out, void* cuda_stream);
+
+/* Measurement hook for the block dot above (same arguments and launch path): one warm-up
+ * launch, then `reps` back-to-back launches timed with CUDA events on cuda_stream; *ms (host)
+ * = mean milliseconds per launch.  Scratch is allocated outside the timed region.  Synchronises
+ * cuda_stream.  Errors: IGS_ERR_ARG (bad sizes/alignment), IGS_ERR_CUDA / IGS_ERR_OOM. */
+igs_status igs_bench_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                               const double* z, double* out, int reps, float* ms, void* cuda_stream);
 
 /* y = A x with the context's (local, nranks == 1) matrix: x, y device [n_local]. */
 igs_status igs_op_spmv(igs_ctx* ctx, const double* x, double* y);
@@ -235,6 +277,26 @@ igs_status igs_op_basis_diag(int64_t n, int c, const double* V, int64_t ld, doub
  * order x order, ld = ldl (device); b, x device [order].  One CTA (the small-step solver). */
 igs_status igs_op_trisolve(int order, const double* L, int ldl, const double* b, double* x,
                            void* cuda_stream);
+
+/* ---------------------------------------------------------------------------------
+ * Virtual ranks (test hook for the G > 1 halo path on ONE device).
+ * igs_create_virtual builds out[0..nranks-1]: for each rank r the context igs_create would
+ * build on GPU r for the row block [bounds[r], bounds[r+1]) of one global CSR (host
+ * arrays: rowptr[n_global+1] global offsets, colind global columns, values), all on
+ * cuda_device and stream cuda_stream, with the same halo plan (ghost map, send/receive
+ * lists, boundary-row split) but no NCCL communicator.  igs_virtual_spmv then computes, for
+ * every rank, y[r] = A_r x (b == NULL) or y[r] = b[r] - A_r x with x distributed as x[r]
+ * (device, rank r's rows): it runs every rank's pack kernel into its send buffer, then each
+ * rank's SpMV exactly as igs_solve does at G > 1 (interior rows while the ghosts arrive,
+ * the boundary rows after them), the ghost entries copied from the owners' send buffers by
+ * device copies instead of ncclSend/ncclRecv.  Virtual contexts reject igs_solve; destroy
+ * each with igs_destroy.  Errors: IGS_ERR_ARG (bounds not spanning [0, n_global) in order,
+ * contexts not one complete group in rank order), IGS_ERR_CUDA / IGS_ERR_OOM. */
+igs_status igs_create_virtual(igs_ctx** out, int nranks, int64_t n_global, const int64_t* bounds,
+                              const int64_t* rowptr, const void* colind, int colind_bits,
+                              const double* values, int cuda_device, void* cuda_stream);
+igs_status igs_virtual_spmv(igs_ctx* const* ctxs, int nranks, const double* const* x, double* const* y,
+                            const double* const* b);
 
 /* ---------------------------------------------------------------------------------
  * Host-only halo planning (no device needed; used by igs_create and by CPU tests).

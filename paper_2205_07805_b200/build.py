@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libigs.so")
-SOURCES = ["kernels.cu", "bdot_spmv.cu", "fused.cu", "diag.cu", "api.cu", "plan.cpp"]
+SOURCES = ["kernels.cu", "diag.cu", "api.cu", "plan.cpp"]
 HEADERS = ["igs_internal.cuh", "ptx_util.cuh", "xchg.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

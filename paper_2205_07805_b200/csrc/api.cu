@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <map>
 #include <utility>
@@ -17,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/igs.h"
@@ -84,6 +86,7 @@ struct igs_ctx {
     void* d_col = nullptr;
     double* d_val = nullptr;
     int64_t nnz = 0;
+    bool csr_compact = false;  // CSR arrays hold only the boundary rows (a SELL copy exists)
     // halo
     int64_t n_ghost = 0;
     double* d_ghost = nullptr;
@@ -121,18 +124,6 @@ struct igs_ctx {
     double t_bytes[IGS_K_COUNT] = {0};
     int64_t t_launch[IGS_K_COUNT] = {0};
     int64_t tail_launches = 0;  // side-stream small-step tails (untimed)
-    // fused wavefront path (single GPU): reach = max |col - row|, flags per 128-row tile
-    int64_t reach = 0;
-    bool fused_enabled = false;  // IGS_FUSED=1 enables the wavefront kernel (experimental)
-    double fused_budget = 72e6;  // bytes of V the L2 must hold between phase A and phase B
-    int fused_grid = 0;
-    long long* d_flags = nullptr;  // per-CTA progress words of the fused kernel
-    int epoch = 0;
-    int64_t n_fused = 0;
-    bool bs_ok = false;  // SpMV folded into the bulk-copy block dot (bdot_spmv.cu)
-    bool fused_ok = false;  // int32 CSR, every 128-row tile within the fused kernel's nnz cap
-    CUtensorMap tmV256{};   // V as a 2D tensor, box 256 rows x 8 columns (block dot)
-    bool tm_ok = false;
     // CUDA graphs of whole restart cycles (small problems, single GPU, timing off)
     bool graphs_enabled = true;
     bool capturing = false;
@@ -148,7 +139,6 @@ struct igs_ctx {
     bool xs_enabled = true;   // IGS_PC_XSTAGE=0: persistent kernel gathers u from L2 (long rows)
     bool two_fused = true;    // IGS_TWO_FUSED=0: Alg. 2 two-reduce with a separate second block dot
     double two_fused_l2 = 80e6;  // IGS_TWO_FUSED_L2_MB: L2 budget of the fused update + dot
-    bool two_tma = true;         // IGS_TWO_TMA=0: no shared-memory tile variant of the fused update + dot
     int pc_ntri = 0;          // IGS_PC_NTRI: forward-substitution CTAs of the persistent kernel (0 = auto)
     int64_t pc_max_n = 190000;  // crossover vs the graph-replayed per-kernel path
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
@@ -174,34 +164,20 @@ struct igs_ctx {
     ncclDevComm dcomm{};
     bool dcomm_ok = false;
     XchgDev* d_xchg = nullptr;  // device copy; null = separate ncclAllReduce
+    XchgDev h_xchg{};           // host copy (timeout / test-hook updates are re-uploaded)
+    int* d_misc = nullptr;      // [0]: agreement flag (agree_all), [1]: exchange error word
+    int* d_xerr = nullptr;      // = d_misc + 1: 1 after an exchange barrier timeout
     int xslot = 0;              // slot capacity (doubles) of the registered window
+    // failure handling: host waits poll ncclCommGetAsyncError and give up after
+    // timeout_s (ncclCommAbort); the exchange barrier has the same device-side bound
+    double timeout_s = 120.0;   // IGS_NCCL_TIMEOUT_S / igs_set_timeout
+    bool aborted = false;       // communicator aborted: the context only accepts igs_destroy
+    // virtual ranks (igs_create_virtual, test hook): G contexts of one process on one device;
+    // the halo copies from the owning context's send buffer instead of NCCL send/recv
+    struct VGroup* vgroup = nullptr;
 };
 
 // ------------------------------------------------------------------------------ misc
-typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-bool igs::make_tensor_map(CUtensorMap* tm, const double* base, int64_t n, int64_t ncols, int64_t ld,
-                          int box_rows, int box_cols) {
-    static PFN_encodeTiled encode = nullptr;
-    if (!encode) {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !fn)
-            return false;
-        encode = reinterpret_cast<PFN_encodeTiled>(fn);
-    }
-    if (n < 1 || ncols < 1 || (ld * 8) % 16 != 0 || ((uintptr_t)base % 16) != 0) return false;
-    const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)ncols};
-    const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
-    const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
-    const cuuint32_t estr[2] = {1, 1};
-    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 extern "C" const char* igs_last_error(void) { return g_err.c_str(); }
 
 static inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
@@ -251,6 +227,50 @@ static igs_status timer_flush(igs_ctx* c) {
     } while (0)
 #define TIMED(kind, bytes, launch_stmt) TIMED_ON(ctx->stream, kind, bytes, launch_stmt)
 
+// ------------------------------------------------------------- waits with a deadline
+// Failure detection: with a communicator every host wait polls instead of
+// blocking.  An asynchronous NCCL error (ncclCommGetAsyncError) or no progress for
+// ctx->timeout_s (a peer rank died or never joined a collective) aborts the communicator
+// (ncclCommAbort) and returns IGS_ERR_NCCL; the context then only accepts igs_destroy.
+// The fused exchange's barrier is bounded on the device by the same timeout (xchg.cuh).
+static igs_status abort_comm(igs_ctx* ctx, const std::string& why) {
+    if (ctx->comm && !ctx->aborted) ncclCommAbort(ctx->comm);
+    ctx->aborted = true;
+    ctx->ok = false;
+    set_error(why + " (communicator aborted; destroy the context)");
+    return IGS_ERR_NCCL;
+}
+
+static igs_status wait_for(igs_ctx* ctx, cudaEvent_t ev, cudaStream_t st, const char* what) {
+    if (!ctx->comm) {
+        const cudaError_t e = ev ? cudaEventSynchronize(ev) : cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            set_error(std::string(what) + ": " + cudaGetErrorString(e));
+            return IGS_ERR_CUDA;
+        }
+        return IGS_OK;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spin = 0;; spin++) {
+        const cudaError_t q = ev ? cudaEventQuery(ev) : cudaStreamQuery(st);
+        if (q == cudaSuccess) return IGS_OK;
+        if (q != cudaErrorNotReady) {
+            set_error(std::string(what) + ": " + cudaGetErrorString(q));
+            return IGS_ERR_CUDA;
+        }
+        ncclResult_t ar = ncclSuccess;
+        if (ncclCommGetAsyncError(ctx->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+            return abort_comm(ctx, std::string(what) + ": NCCL asynchronous error: " + ncclGetErrorString(ar));
+        if ((spin & 255u) == 255u) {
+            const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (el > ctx->timeout_s)
+                return abort_comm(ctx, std::string(what) + ": timeout, no progress for " +
+                                           std::to_string(ctx->timeout_s) + " s (a peer rank stopped or hung?)");
+        }
+        if (spin >= 1024) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
 // --------------------------------------------------------------------- create / destroy
 extern "C" igs_status igs_nccl_unique_id(void* out128) {
     ARG_CHECK(out128 != nullptr, "igs_nccl_unique_id: NULL output");
@@ -283,11 +303,25 @@ static igs_status validate_csr(int64_t n_global, int64_t n_local, const int64_t*
     return IGS_OK;
 }
 
+// Virtual ranks (igs_create_virtual): the row bounds and every rank's ghost list are known
+// on the host, so the two all-gathers and the request exchange of setup_halo are computed.
+struct VirtPlan {
+    std::vector<int64_t> bounds;               // [G + 1]
+    std::vector<std::vector<int64_t>> ghosts;  // ghosts[q]: rank q's ghost columns (ascending)
+};
+struct VGroup {
+    int G = 0;
+    std::vector<igs_ctx*> members;
+    int alive = 0;
+};
+
 static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* colind, int bits,
-                             std::vector<int64_t>& local_col) {
+                             std::vector<int64_t>& local_col, const VirtPlan* vp) {
     const int G = ctx->nranks;
     std::vector<int64_t> bounds(G + 1, 0);
-    if (G > 1) {
+    if (vp) {
+        bounds = vp->bounds;
+    } else if (G > 1) {
         // all-gather (row_begin, n_local) through NCCL
         int64_t* d_bl = nullptr;
         CUDA_TRY(cudaMalloc(&d_bl, sizeof(int64_t) * 2 * G));
@@ -296,7 +330,7 @@ static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* co
         NCCL_TRY(ncclAllGather(d_bl + 2 * ctx->rank, d_bl, 2, ncclInt64, ctx->comm, ctx->stream));
         std::vector<int64_t> bl(2 * G);
         CUDA_TRY(cudaMemcpyAsync(bl.data(), d_bl, sizeof(int64_t) * 2 * G, cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        TRY(wait_for(ctx, nullptr, ctx->stream, "igs_create: halo plan"));
         cudaFree(d_bl);
         for (int q = 0; q < G; q++) {
             ARG_CHECK(bl[2 * q] == (q == 0 ? 0 : bl[2 * (q - 1)] + bl[2 * (q - 1) + 1]),
@@ -326,15 +360,23 @@ static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* co
         return IGS_OK;
     }
     // count matrix cnt[q][r] = ghosts rank q needs from rank r (all-gather of owner counts)
-    int64_t* d_cnt = nullptr;
-    CUDA_TRY(cudaMalloc(&d_cnt, sizeof(int64_t) * G * G));
-    CUDA_TRY(cudaMemcpyAsync(d_cnt + (int64_t)G * ctx->rank, owner_cnt.data(), sizeof(int64_t) * G,
-                             cudaMemcpyHostToDevice, ctx->stream));
-    NCCL_TRY(ncclAllGather(d_cnt + (int64_t)G * ctx->rank, d_cnt, G, ncclInt64, ctx->comm, ctx->stream));
-    std::vector<int64_t> cnt((size_t)G * G);
-    CUDA_TRY(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    cudaFree(d_cnt);
+    std::vector<int64_t> cnt((size_t)G * G, 0);
+    if (vp) {
+        for (int q = 0; q < G; q++)
+            for (int64_t c : vp->ghosts[q]) {
+                const int r = (int)(std::upper_bound(bounds.begin(), bounds.end(), c) - bounds.begin()) - 1;
+                cnt[(size_t)q * G + r]++;
+            }
+    } else {
+        int64_t* d_cnt = nullptr;
+        CUDA_TRY(cudaMalloc(&d_cnt, sizeof(int64_t) * G * G));
+        CUDA_TRY(cudaMemcpyAsync(d_cnt + (int64_t)G * ctx->rank, owner_cnt.data(), sizeof(int64_t) * G,
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        NCCL_TRY(ncclAllGather(d_cnt + (int64_t)G * ctx->rank, d_cnt, G, ncclInt64, ctx->comm, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int64_t) * G * G, cudaMemcpyDeviceToHost, ctx->stream));
+        TRY(wait_for(ctx, nullptr, ctx->stream, "igs_create: halo plan"));
+        cudaFree(d_cnt);
+    }
     // receive side: my ghosts, grouped by owner (ghosts are sorted, owners ascending)
     // send side: rows other ranks need from me
     ctx->peers.clear(); ctx->send_off.clear(); ctx->send_cnt.clear(); ctx->recv_off.clear(); ctx->recv_cnt.clear();
@@ -350,6 +392,14 @@ static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* co
     }
     ctx->n_send = soff;
     // exchange the requested global indices
+    std::vector<int64_t> req(soff);
+    if (vp) {  // the peers' requests, in peer order: peer q's ghosts that I own
+        int64_t at = 0;
+        for (size_t i = 0; i < ctx->peers.size(); i++)
+            for (int64_t c : vp->ghosts[ctx->peers[i]])
+                if (c >= ctx->row_begin && c < ctx->row_begin + ctx->n_local) req[(size_t)at++] = c;
+        ARG_CHECK(at == soff, "igs_create_virtual: inconsistent halo plan");
+    } else {
     int64_t *d_req_out = nullptr, *d_req_in = nullptr;
     CUDA_TRY(cudaMalloc(&d_req_out, sizeof(int64_t) * std::max<int64_t>(ng, 1)));
     CUDA_TRY(cudaMalloc(&d_req_in, sizeof(int64_t) * std::max<int64_t>(soff, 1)));
@@ -360,11 +410,11 @@ static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* co
         if (ctx->send_cnt[i]) NCCL_TRY(ncclRecv(d_req_in + ctx->send_off[i], ctx->send_cnt[i], ncclInt64, ctx->peers[i], ctx->comm, ctx->stream));
     }
     NCCL_TRY(ncclGroupEnd());
-    std::vector<int64_t> req(soff);
     CUDA_TRY(cudaMemcpyAsync(req.data(), d_req_in, sizeof(int64_t) * soff, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    TRY(wait_for(ctx, nullptr, ctx->stream, "igs_create: halo plan"));
     cudaFree(d_req_out);
     cudaFree(d_req_in);
+    }
     for (auto& r : req) {
         ARG_CHECK(r >= ctx->row_begin && r < ctx->row_begin + ctx->n_local, "igs_create: bad halo request");
         r -= ctx->row_begin;
@@ -373,9 +423,11 @@ static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* co
     CUDA_TRY(cudaMalloc(&ctx->d_send, sizeof(double) * std::max<int64_t>(soff, 1)));
     CUDA_TRY(cudaMalloc(&ctx->d_ghost, sizeof(double) * std::max<int64_t>(ng, 1)));
     CUDA_TRY(cudaMemcpyAsync(ctx->d_send_idx, req.data(), sizeof(int64_t) * soff, cudaMemcpyHostToDevice, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    TRY(wait_for(ctx, nullptr, ctx->stream, "igs_create: halo plan"));
     return IGS_OK;
 }
+
+static void release_xchg(igs_ctx* ctx);
 
 static void free_ctx(igs_ctx* c) {
     if (!c) return;
@@ -390,7 +442,6 @@ static void free_ctx(igs_ctx* c) {
     if (c->ev_x) cudaEventDestroy(c->ev_x);
     if (c->ev_h) cudaEventDestroy(c->ev_h);
     cudaFree(c->d_gram);
-    cudaFree(c->d_flags);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->h_pinned_int) cudaFreeHost(c->h_pinned_int);
     for (auto e : c->events) cudaEventDestroy(e);
@@ -401,24 +452,24 @@ static void free_ctx(igs_ctx* c) {
     if (c->ev_g0) cudaEventDestroy(c->ev_g0);
     if (c->ev_g1) cudaEventDestroy(c->ev_g1);
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second.exec);
-    if (c->dcomm_ok) ncclDevCommDestroy(c->comm, &c->dcomm);
-    if (c->xwin) ncclCommWindowDeregister(c->comm, c->xwin);
-    if (c->xbuf) ncclMemFree(c->xbuf);
-    cudaFree(c->d_xchg);
-    if (c->comm) ncclCommDestroy(c->comm);
+    // after ncclCommAbort the communicator's resources are gone with it
+    if (c->dcomm_ok && !c->aborted) ncclDevCommDestroy(c->comm, &c->dcomm);
+    release_xchg(c);
+    cudaFree(c->d_misc);
+    if (c->comm && !c->aborted) ncclCommDestroy(c->comm);
     delete c;
 }
 
 // SELL-32 (slices of 32 rows, entries of a slice interleaved by row) from the host CSR.
 static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vector<int64_t>& local_col,
-                             const double* values, bool idx64) {
+                             const double* values, bool idx64, std::vector<int64_t>& bnd) {
     const int64_t n = ctx->n_local, ns = (n + 31) / 32;
     std::vector<int64_t> sp((size_t)ns + 1, 0);
     std::vector<uint8_t> len((size_t)n);
     // G > 1: rows that touch a ghost column are left to the boundary pass (row-list kernel,
     // after the halo); the SELL pass runs while the halo is in flight and skips them
     // (row length SELL_BOUNDARY, no entries stored)
-    std::vector<int64_t> bnd;
+    bnd.clear();
     for (int64_t r = 0; r < n && ctx->n_ghost > 0; r++)
         for (int64_t q = rowptr[r]; q < rowptr[r + 1]; q++)
             if (local_col[(size_t)q] >= n) { bnd.push_back(r); break; }
@@ -433,7 +484,7 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
         for (int64_t r = 32 * s; r < std::min<int64_t>(n, 32 * s + 32); r++) {
             if (bi < bnd.size() && bnd[bi] == r) { len[(size_t)r] = SELL_BOUNDARY; bi++; continue; }
             const int64_t l = rowptr[r + 1] - rowptr[r];
-            if (l >= SELL_BOUNDARY) return IGS_OK;  // long rows: keep the CSR kernels
+            if (l >= SELL_BOUNDARY) { bnd.clear(); return IGS_OK; }  // long rows: keep the CSR kernels
             len[(size_t)r] = (uint8_t)l;
             mx = std::max(mx, l);
         }
@@ -477,6 +528,12 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     return IGS_OK;
 }
 
+static igs_status create_ctx(igs_ctx** out, int64_t n_global, int64_t row_begin,
+                             int64_t n_local, const int64_t* rowptr, const void* colind,
+                             int colind_bits, const double* values, int64_t nnz_local,
+                             igs_mem where, int cuda_device, const void* nccl_unique_id,
+                             int rank, int nranks, void* cuda_stream, const VirtPlan* vp);
+
 extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_begin,
                                  int64_t n_local, const int64_t* rowptr, const void* colind,
                                  int colind_bits, const double* values, int64_t nnz_local,
@@ -484,11 +541,21 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
                                  int rank, int nranks, void* cuda_stream) {
     ARG_CHECK(out != nullptr, "igs_create: NULL out");
     *out = nullptr;
+    ARG_CHECK((nranks == 1) == (nccl_unique_id == nullptr), "igs_create: nccl_unique_id must be given iff nranks > 1");
+    return create_ctx(out, n_global, row_begin, n_local, rowptr, colind, colind_bits, values, nnz_local, where,
+                      cuda_device, nccl_unique_id, rank, nranks, cuda_stream, nullptr);
+}
+
+static igs_status create_ctx(igs_ctx** out, int64_t n_global, int64_t row_begin,
+                             int64_t n_local, const int64_t* rowptr, const void* colind,
+                             int colind_bits, const double* values, int64_t nnz_local,
+                             igs_mem where, int cuda_device, const void* nccl_unique_id,
+                             int rank, int nranks, void* cuda_stream, const VirtPlan* vp) {
+    *out = nullptr;
     ARG_CHECK(n_global > 0, "igs_create: n_global must be > 0");
     ARG_CHECK(row_begin >= 0 && n_local >= 0 && row_begin + n_local <= n_global, "igs_create: bad row block");
     ARG_CHECK(colind_bits == 32 || colind_bits == 64, "igs_create: colind_bits must be 32 or 64");
     ARG_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, "igs_create: bad rank/nranks");
-    ARG_CHECK((nranks == 1) == (nccl_unique_id == nullptr), "igs_create: nccl_unique_id must be given iff nranks > 1");
     ARG_CHECK(nnz_local >= 0, "igs_create: nnz_local < 0");
     ARG_CHECK(n_local == 0 || (rowptr && (nnz_local == 0 || (colind && values))), "igs_create: NULL CSR array");
     ARG_CHECK(where == IGS_MEM_HOST || where == IGS_MEM_DEVICE, "igs_create: bad memory kind");
@@ -538,12 +605,13 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
 
     auto fail = [&](igs_status s) { free_ctx(ctx); return s; };
+    if (const char* e = std::getenv("IGS_NCCL_TIMEOUT_S")) ctx->timeout_s = std::max(1e-6, std::atof(e));
     // the fused block dot + NVLink exchange is the G > 1 default (IGS_XCHG=0: a separate
     // ncclAllReduce after each block dot; IGS_XCHG=1 also on one GPU, via a 1-rank comm)
-    ctx->xchg_req = nranks > 1;
-    if (const char* e = std::getenv("IGS_XCHG")) ctx->xchg_req = std::atoi(e) != 0;
+    ctx->xchg_req = nranks > 1 && !vp;
+    if (const char* e = std::getenv("IGS_XCHG")) ctx->xchg_req = !vp && std::atoi(e) != 0;
     if (const char* e = std::getenv("IGS_FORCE_NCCL")) ctx->force_nccl = nranks == 1 && std::atoi(e) != 0;
-    if (nranks > 1 || ctx->xchg_req || ctx->force_nccl) {
+    if (!vp && (nranks > 1 || ctx->xchg_req || ctx->force_nccl)) {
         // (one rank + IGS_XCHG=1: a 1-rank communicator, so the fused exchange path runs on
         //  a single GPU exactly as it does on G)
         ncclUniqueId id;
@@ -554,118 +622,110 @@ extern "C" igs_status igs_create(igs_ctx** out, int64_t n_global, int64_t row_be
         }
         ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
         if (r != ncclSuccess) {
+            ctx->comm = nullptr;
             set_error(std::string("ncclCommInitRank failed: ") + ncclGetErrorString(r));
             return fail(IGS_ERR_NCCL);
         }
+        if (cudaMalloc(&ctx->d_misc, 2 * sizeof(int)) != cudaSuccess ||
+            cudaMemset(ctx->d_misc, 0, 2 * sizeof(int)) != cudaSuccess) {
+            set_error("igs_create: cudaMalloc (exchange flags) failed");
+            return fail(IGS_ERR_OOM);
+        }
+        ctx->d_xerr = ctx->d_misc + 1;
     }
     std::vector<int64_t> local_col;
     {
-        igs_status s = setup_halo(ctx, rowptr, colind, colind_bits, local_col);
+        igs_status s = setup_halo(ctx, rowptr, colind, colind_bits, local_col, vp);
         if (s != IGS_OK) return fail(s);
     }
     // device CSR: int32 rowptr unless nnz needs 64 bits or the caller chose 64-bit columns
     const bool idx64 = colind_bits == 64 || (n_local + ctx->n_ghost) >= ((int64_t)1 << 31);
     const bool ptr64 = idx64 || nnz_local >= ((int64_t)1 << 31);
-    {
-        std::vector<char> rp((size_t)(n_local + 1) * (ptr64 ? 8 : 4));
-        for (int64_t i = 0; i <= n_local; i++) {
-            if (ptr64) reinterpret_cast<int64_t*>(rp.data())[i] = rowptr[i];
-            else reinterpret_cast<int32_t*>(rp.data())[i] = (int32_t)rowptr[i];
-        }
-        std::vector<char> ci((size_t)std::max<int64_t>(nnz_local, 1) * (idx64 ? 8 : 4));
-        for (int64_t q = 0; q < nnz_local; q++) {
-            if (idx64) reinterpret_cast<int64_t*>(ci.data())[q] = local_col[q];
-            else reinterpret_cast<int32_t*>(ci.data())[q] = (int32_t)local_col[q];
-        }
-        cudaError_t e;
-        // padding: the fused SpMV + block dot bulk-copies 16-B aligned supersets of ranges
-        const size_t pad = 64;
-        if ((e = cudaMalloc(&ctx->d_rowptr, rp.size() + pad)) != cudaSuccess ||
-            (e = cudaMalloc(&ctx->d_col, ci.size() + pad)) != cudaSuccess ||
-            (e = cudaMalloc(&ctx->d_val, sizeof(double) * std::max<int64_t>(nnz_local, 1) + pad)) != cudaSuccess ||
-            (e = cudaMemset(ctx->d_rowptr, 0, rp.size() + pad)) != cudaSuccess ||
-            (e = cudaMemset(ctx->d_col, 0, ci.size() + pad)) != cudaSuccess ||
-            (e = cudaMemset(ctx->d_val, 0, sizeof(double) * std::max<int64_t>(nnz_local, 1) + pad)) != cudaSuccess) {
-            set_error(std::string("igs_create: cudaMalloc: ") + cudaGetErrorString(e));
-            return fail(IGS_ERR_OOM);
-        }
-        if ((e = cudaMemcpy(ctx->d_rowptr, rp.data(), rp.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
-            (e = cudaMemcpy(ctx->d_col, ci.data(), (size_t)nnz_local * (idx64 ? 8 : 4), cudaMemcpyHostToDevice)) != cudaSuccess ||
-            (e = cudaMemcpy(ctx->d_val, values, sizeof(double) * nnz_local, cudaMemcpyHostToDevice)) != cudaSuccess) {
-            set_error(std::string("igs_create: cudaMemcpy: ") + cudaGetErrorString(e));
-            return fail(IGS_ERR_CUDA);
-        }
-    }
     ctx->A.nrows = n_local;
-    ctx->A.rowptr = ctx->d_rowptr;
-    ctx->A.col = ctx->d_col;
-    ctx->A.val = ctx->d_val;
     ctx->A.ptr64 = ptr64;
     ctx->A.idx64 = idx64;
     ctx->A.nloc = n_local;
     ctx->A.ghost = ctx->n_ghost > 0 ? ctx->d_ghost : nullptr;
+    // short rows (<= 8 nnz on average): CSR-stream kernel (lpr = 0); otherwise vector CSR with
+    // lanes per row = next power of two of the mean row length, in [1, 32]
     {
-        // short rows (<= 8 nnz on average): CSR-stream kernel (lpr = 0); otherwise vector
-        // CSR with lanes per row = next power of two of the mean row length, in [1, 32]
         const double avg = n_local > 0 ? (double)nnz_local / (double)n_local : 1.0;
         int lpr = 1;
         while (lpr < 32 && lpr < avg) lpr *= 2;
         ctx->A.lpr = avg <= 8.0 ? 0 : lpr;
-        // SELL-32 copy for short rows (coalesced per-thread rows)
-        const char* es = std::getenv("IGS_SELL");
+    }
+    // SELL-32 copy for short rows (coalesced per-thread rows).  When it exists
+    // it is the only full copy of A on the device: the CSR arrays keep just the boundary rows
+    // (G > 1: rows with a ghost column, multiplied after the halo by launch_spmv_rows).
+    std::vector<int64_t> bnd;
+    {
+        const char* es = std::getenv("IGS_SELL");  // test hook: IGS_SELL=0 keeps the CSR kernels
         if (ctx->A.lpr == 0 && n_local > 0 && !(es && std::atoi(es) == 0)) {
-            igs_status ss = build_sell(ctx, rowptr, local_col, values, idx64);
+            igs_status ss = build_sell(ctx, rowptr, local_col, values, idx64, bnd);
             if (ss != IGS_OK) return fail(ss);
         }
-        // every 256-row tile within the staged-nonzero cap, 32-bit CSR -> fused SpMV + dot
-        if (!idx64 && !ptr64) {
-            bool ok = true;
-            const int T = fused_tile_rows();
-            for (int64_t r0 = 0; r0 < n_local && ok; r0 += T) {
-                const int64_t r1 = std::min<int64_t>(r0 + T, n_local);
-                ok = rowptr[r1] - rowptr[r0] <= fused_nnz_cap();
-            }
-            ctx->fused_ok = ok;
-        }
-        if (!idx64 && !ptr64 && n_local >= bdot_spmv_tile_rows()) {
-            bool ok = true;
-            const int T = bdot_spmv_tile_rows();
-            for (int64_t r0 = 0; r0 < n_local && ok; r0 += T) {
-                const int64_t r1 = std::min<int64_t>(r0 + T, n_local);
-                ok = rowptr[r1] - rowptr[r0] <= bdot_spmv_nnz_cap();
-            }
-            // opt-in (IGS_BDOT_SPMV=1): measured 2x slower than SpMV kernel + block dot on c4
-            // (the per-tile gather latency serialises with the V stream)
-            const char* e = std::getenv("IGS_BDOT_SPMV");
-            ctx->bs_ok = ok && e && std::atoi(e) != 0;
-        }
     }
+    {
+        const bool compact = ctx->A.sell_ptr != nullptr;  // boundary rows only
+        const int64_t nr = compact ? (int64_t)bnd.size() : n_local;
+        std::vector<int64_t> rpc((size_t)nr + 1, 0);
+        for (int64_t i = 0; i < nr; i++) {
+            const int64_t r = compact ? bnd[(size_t)i] : i;
+            rpc[(size_t)i + 1] = rpc[(size_t)i] + (rowptr[r + 1] - rowptr[r]);
+        }
+        const int64_t nzc = rpc[(size_t)nr];
+        std::vector<char> rp((size_t)(nr + 1) * (ptr64 ? 8 : 4));
+        for (int64_t i = 0; i <= nr; i++) {
+            if (ptr64) reinterpret_cast<int64_t*>(rp.data())[i] = rpc[(size_t)i];
+            else reinterpret_cast<int32_t*>(rp.data())[i] = (int32_t)rpc[(size_t)i];
+        }
+        std::vector<char> ci((size_t)std::max<int64_t>(nzc, 1) * (idx64 ? 8 : 4));
+        std::vector<double> vc;
+        const double* vsrc = values;
+        if (compact) vc.resize((size_t)std::max<int64_t>(nzc, 1));
+        for (int64_t i = 0, at = 0; i < nr; i++) {
+            const int64_t r = compact ? bnd[(size_t)i] : i;
+            for (int64_t q = rowptr[r]; q < rowptr[r + 1]; q++, at++) {
+                if (idx64) reinterpret_cast<int64_t*>(ci.data())[at] = local_col[(size_t)q];
+                else reinterpret_cast<int32_t*>(ci.data())[at] = (int32_t)local_col[(size_t)q];
+                if (compact) vc[(size_t)at] = values[q];
+            }
+        }
+        if (compact) vsrc = vc.data();
+        cudaError_t e;
+        const size_t pad = 64;
+        if ((e = cudaMalloc(&ctx->d_rowptr, rp.size() + pad)) != cudaSuccess ||
+            (e = cudaMalloc(&ctx->d_col, ci.size() + pad)) != cudaSuccess ||
+            (e = cudaMalloc(&ctx->d_val, sizeof(double) * std::max<int64_t>(nzc, 1) + pad)) != cudaSuccess ||
+            (e = cudaMemset(ctx->d_rowptr, 0, rp.size() + pad)) != cudaSuccess ||
+            (e = cudaMemset(ctx->d_col, 0, ci.size() + pad)) != cudaSuccess ||
+            (e = cudaMemset(ctx->d_val, 0, sizeof(double) * std::max<int64_t>(nzc, 1) + pad)) != cudaSuccess) {
+            set_error(std::string("igs_create: cudaMalloc: ") + cudaGetErrorString(e));
+            return fail(IGS_ERR_OOM);
+        }
+        if ((e = cudaMemcpy(ctx->d_rowptr, rp.data(), rp.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy(ctx->d_col, ci.data(), (size_t)nzc * (idx64 ? 8 : 4), cudaMemcpyHostToDevice)) != cudaSuccess ||
+            (e = cudaMemcpy(ctx->d_val, vsrc, sizeof(double) * nzc, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            set_error(std::string("igs_create: cudaMemcpy: ") + cudaGetErrorString(e));
+            return fail(IGS_ERR_CUDA);
+        }
+        ctx->csr_compact = compact;
+    }
+    ctx->A.rowptr = ctx->d_rowptr;
+    ctx->A.col = ctx->d_col;
+    ctx->A.val = ctx->d_val;
     ctx->bdot_grid = bdot_grid_size(n_local, ctx->num_sms);
     {
-        int64_t reach = 0;
-        for (int64_t i = 0; i < n_local; i++)
-            for (int64_t q = rowptr[i]; q < rowptr[i + 1]; q++) {
-                const int64_t cc = colind_bits == 64 ? static_cast<const int64_t*>(colind)[q]
-                                                     : (int64_t) static_cast<const int32_t*>(colind)[q];
-                const int64_t d = cc - (row_begin + i);
-                reach = std::max(reach, d < 0 ? -d : d);
-            }
-        ctx->reach = reach;
-        ctx->fused_grid = fused_grid(ctx->num_sms);
-        if (ctx->fused_grid > ctx->bdot_grid) ctx->bdot_grid = ctx->fused_grid;
-        if (const char* e = std::getenv("IGS_FUSED")) ctx->fused_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_GRAPHS")) ctx->graphs_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PERSIST")) ctx->pc_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_MGS_FUSED")) ctx->mgs_fused = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PC_XSTAGE")) ctx->xs_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_TWO_FUSED")) ctx->two_fused = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_TWO_FUSED_L2_MB")) ctx->two_fused_l2 = std::atof(e) * 1e6;
-        if (const char* e = std::getenv("IGS_TWO_TMA")) ctx->two_tma = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PC_NTRI")) ctx->pc_ntri = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_GRID")) ctx->pc_grid = std::atoi(e);
         if (const char* e = std::getenv("IGS_PC_MAX_N")) ctx->pc_max_n = std::atoll(e);
         if (const char* e = std::getenv("IGS_PC_ROWSPLIT_N")) ctx->pc_rowsplit_n = std::atoll(e);
-        if (const char* e = std::getenv("IGS_FUSED_L2_MB")) ctx->fused_budget = std::atof(e) * 1e6;
     }
     cudaError_t e;
     if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -688,6 +748,11 @@ extern "C" igs_status igs_destroy(igs_ctx* ctx) {
     if (!ctx) return IGS_OK;
     cudaSetDevice(ctx->dev);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (VGroup* g = ctx->vgroup) {  // the last member frees the group
+        g->members[(size_t)ctx->rank] = nullptr;
+        if (--g->alive == 0) delete g;
+        ctx->vgroup = nullptr;
+    }
     free_ctx(ctx);
     return IGS_OK;
 }
@@ -723,39 +788,85 @@ extern "C" igs_status igs_bind_workspace(igs_ctx* ctx, void* dev_ptr, size_t byt
     return IGS_OK;
 }
 
-// Symmetric window of 2 slots x `slot` doubles + the device communicator with one LSA
-// barrier (collective over the ranks; ensure_workspace runs on every rank in step).
-static igs_status setup_xchg(igs_ctx* ctx, int slot) {
+// min over ranks of a success flag (every rank takes the same branch afterwards)
+static igs_status agree_all(igs_ctx* ctx, bool mine, bool* all) {
+    ctx->h_pinned_int[30] = mine ? 1 : 0;
+    CUDA_TRY(cudaMemcpyAsync(ctx->d_misc, ctx->h_pinned_int + 30, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    NCCL_TRY(ncclAllReduce(ctx->d_misc, ctx->d_misc, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned_int + 31, ctx->d_misc, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TRY(wait_for(ctx, nullptr, ctx->stream, "fused exchange setup"));
+    *all = ctx->h_pinned_int[31] == 1;
+    return IGS_OK;
+}
+
+static void release_xchg(igs_ctx* ctx) {
+    if (ctx->xwin && !ctx->aborted) ncclCommWindowDeregister(ctx->comm, ctx->xwin);
+    ctx->xwin = nullptr;
+    if (ctx->xbuf && !ctx->aborted) ncclMemFree(ctx->xbuf);
+    ctx->xbuf = nullptr;
+    cudaFree(ctx->d_xchg);
+    ctx->d_xchg = nullptr;
+    ctx->xslot = 0;
+}
+
+// Symmetric window (2 slots x `slot` doubles + one inbox word per rank, xchg.cuh) and the
+// device communicator.  Collective: ensure_workspace runs on every rank in step.  Every
+// step that can fail on one rank only (allocation, registration) is followed by an
+// agreement allreduce, so either all ranks use the fused exchange or all fall back to
+// ncclAllReduce -- a rank that fell back alone would strand its peers at the barrier.
+static igs_status setup_xchg(igs_ctx* ctx, int slot, bool* ok_out) {
+    *ok_out = true;
     if (ctx->d_xchg && slot <= ctx->xslot) return IGS_OK;
-    if (ctx->xwin) { NCCL_TRY(ncclCommWindowDeregister(ctx->comm, ctx->xwin)); ctx->xwin = nullptr; }
-    if (ctx->xbuf) { NCCL_TRY(ncclMemFree(ctx->xbuf)); ctx->xbuf = nullptr; }
-    size_t bytes = (size_t)2 * slot * sizeof(double);
+    release_xchg(ctx);
+    const size_t inbox_off = (size_t)round_up((int64_t)2 * slot * sizeof(double), 16);
+    size_t bytes = inbox_off + sizeof(unsigned) * (size_t)ctx->nranks;
     bytes = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
-    NCCL_TRY(ncclMemAlloc(&ctx->xbuf, bytes));
-    NCCL_TRY(ncclCommWindowRegister(ctx->comm, ctx->xbuf, bytes, &ctx->xwin, NCCL_WIN_COLL_SYMMETRIC));
-    if (!ctx->dcomm_ok) {
+    bool ok = ncclMemAlloc(&ctx->xbuf, bytes) == ncclSuccess;
+    if (!ok) ctx->xbuf = nullptr;
+    // zero the inboxes before any peer can write into them (the agreement below orders it)
+    if (ok) ok = cudaMemsetAsync(ctx->xbuf, 0, bytes, ctx->stream) == cudaSuccess &&
+                 cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+    bool all = false;
+    TRY(agree_all(ctx, ok, &all));
+    if (all) {
+        ok = ncclCommWindowRegister(ctx->comm, ctx->xbuf, bytes, &ctx->xwin, NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess;
+        if (!ok) ctx->xwin = nullptr;
+        TRY(agree_all(ctx, ok, &all));
+    }
+    if (all && !ctx->dcomm_ok) {
         ncclDevCommRequirements reqs;
         std::memset(&reqs, 0, sizeof(reqs));
         reqs.lsaBarrierCount = 1;
-        NCCL_TRY(ncclDevCommCreate(ctx->comm, &reqs, &ctx->dcomm));
-        ctx->dcomm_ok = true;
+        ok = ncclDevCommCreate(ctx->comm, &reqs, &ctx->dcomm) == ncclSuccess;
+        ctx->dcomm_ok = ok;
+        TRY(agree_all(ctx, ok, &all));
     }
-    if (ctx->dcomm.lsaSize != ctx->nranks) {  // not one NVLink domain: keep ncclAllReduce
-        cudaFree(ctx->d_xchg);
-        ctx->d_xchg = nullptr;
+    // one NVLink (LSA) domain spanning the communicator: the same on every rank
+    if (all) all = ctx->dcomm.lsaSize == ctx->nranks;
+    if (all && !ctx->d_xchg) {
+        ok = cudaMalloc(&ctx->d_xchg, sizeof(XchgDev) + 16) == cudaSuccess &&
+             cudaMemset(ctx->d_xchg, 0, sizeof(XchgDev) + 16) == cudaSuccess;
+        if (!ok) ctx->d_xchg = nullptr;
+        TRY(agree_all(ctx, ok, &all));
+    }
+    if (!all) {
+        release_xchg(ctx);
+        *ok_out = false;
         return IGS_OK;
     }
-    if (!ctx->d_xchg) {
-        CUDA_TRY(cudaMalloc(&ctx->d_xchg, sizeof(XchgDev) + 16));
-        CUDA_TRY(cudaMemset(ctx->d_xchg, 0, sizeof(XchgDev) + 16));
-    }
-    XchgDev h;
+    XchgDev& h = ctx->h_xchg;
     std::memset(&h, 0, sizeof(h));
     h.comm = ctx->dcomm;
     h.win = ctx->xwin;
     h.calls = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->d_xchg) + sizeof(XchgDev));
+    h.err = ctx->d_xerr;
+    h.timeout_ns = (unsigned long long)(ctx->timeout_s * 1e9);
+    h.stall_call = 0xffffffffu;
+    if (const char* e = std::getenv("IGS_TEST_XCHG_STALL")) h.stall_call = (unsigned)std::atoi(e);  // test hook
     h.slot_doubles = slot;
     h.nranks = ctx->nranks;
+    h.me = ctx->dcomm.lsaRank;
+    h.inbox_off = inbox_off;
     CUDA_TRY(cudaMemcpy(ctx->d_xchg, &h, sizeof(h), cudaMemcpyHostToDevice));
     ctx->xslot = slot;
     return IGS_OK;
@@ -780,10 +891,6 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         }
         for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
         ctx->graphs.clear();
-        // 2D-tensor-copy block dot: opt-in (IGS_TMAP=1); measured 4.7 TB/s vs 6.3 TB/s for the
-        // 1D bulk-copy pipeline on c4
-        const char* etm = std::getenv("IGS_TMAP");
-        ctx->tm_ok = etm && std::atoi(etm) != 0 && make_tensor_map(&ctx->tmV256, ctx->d_V, ctx->n_local, mm + 1, ldv, 256, 8);
         // zero once: padding rows of every column must stay 0 (kernels read them as 0)
         CUDA_TRY(cudaMemsetAsync(ctx->d_V, 0, vbytes, ctx->stream));
         cudaFree(ctx->d_small);
@@ -823,23 +930,18 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         d.istate = ctx->d_int;
         ctx->m_cap = mm;
         ctx->k_cap = kk;
-        if (ctx->xchg_req && setup_xchg(ctx, d.dld) != IGS_OK) {
-            // symmetric memory / device communicator unavailable: keep ncclAllReduce (the
-            // window registration is collective, so every rank takes the same branch)
-            std::fprintf(stderr, "[igs] fused NVLink exchange unavailable (%s); using ncclAllReduce\n",
-                         igs_last_error());
-            cudaFree(ctx->d_xchg);
-            ctx->d_xchg = nullptr;
-            ctx->xchg_req = false;
+        if (ctx->xchg_req) {
+            bool ok = true;
+            TRY(setup_xchg(ctx, d.dld, &ok));
+            if (!ok) {  // on every rank (agreed): keep ncclAllReduce
+                std::fprintf(stderr, "[igs] fused NVLink exchange unavailable on some rank; using ncclAllReduce\n");
+                ctx->xchg_req = false;
+            }
         }
     }
     if (!ctx->d_z) {
         CUDA_TRY(cudaMalloc(&ctx->d_z, sizeof(double) * ldv));
         CUDA_TRY(cudaMemsetAsync(ctx->d_z, 0, sizeof(double) * ldv, ctx->stream));
-    }
-    if (!ctx->d_flags && ctx->nranks == 1) {
-        CUDA_TRY(cudaMalloc(&ctx->d_flags, sizeof(long long) * (ctx->fused_grid + 1)));
-        CUDA_TRY(cudaMemsetAsync(ctx->d_flags, 0, sizeof(long long) * (ctx->fused_grid + 1), ctx->stream));
     }
     if (!ctx->d_counter) {
         CUDA_TRY(cudaMalloc(&ctx->d_counter, sizeof(unsigned) * 12));  // [4..11]: persistent-kernel flags
@@ -872,6 +974,20 @@ static igs_status allreduce(igs_ctx* ctx, double* buf, int64_t count) {
 }
 
 static igs_status halo_on(igs_ctx* ctx, const double* x, const int* istate, cudaStream_t st) {
+    if (ctx->vgroup) {
+        // virtual ranks (test hook): the ghosts come from the owners' send buffers, which
+        // igs_virtual_spmv packed (pack kernel) before any rank's SpMV was enqueued
+        for (size_t i = 0; i < ctx->peers.size(); i++) {
+            if (!ctx->recv_cnt[i]) continue;
+            const igs_ctx* q = ctx->vgroup->members[(size_t)ctx->peers[i]];
+            const size_t j = (size_t)(std::find(q->peers.begin(), q->peers.end(), ctx->rank) - q->peers.begin());
+            ARG_CHECK(j < q->peers.size() && q->send_cnt[j] == ctx->recv_cnt[i], "virtual halo: inconsistent plan");
+            CUDA_TRY(cudaMemcpyAsync(ctx->d_ghost + ctx->recv_off[i], q->d_send + q->send_off[j],
+                                     sizeof(double) * ctx->recv_cnt[i], cudaMemcpyDeviceToDevice, st));
+        }
+        ctx->n_halo += (int64_t)ctx->peers.size();
+        return IGS_OK;
+    }
     launch_pack(ctx->n_send, ctx->d_send_idx, x, ctx->d_send, istate, st);
     NCCL_TRY(ncclGroupStart());
     for (size_t i = 0; i < ctx->peers.size(); i++) {
@@ -916,24 +1032,20 @@ static igs_status bdot(igs_ctx* ctx, int p, const double* u, const double* z, do
                        const int* istate, int kind) {
     const double by = 8.0 * ctx->n_local * (p + 1 + (z ? 1 : 0));
     if (ctx->d_xchg) {
-        // block dot with the cross-rank sum fused in.  Every rank must take the same skip
-        // decision (a rank that skipped would leave its peers at the LSA barrier), so the
-        // status word it reads must be final: join the side-stream tail of the previous
-        // iteration first (it had the update and the SpMV to finish).  Outside graphs only;
-        // graphs are single-rank.
-        if (istate && !ctx->capturing) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_tail, 0));
+        // block dot with the cross-rank sum fused in.  The kernel joins the exchange on every
+        // rank even when this rank's status word says the cycle has stopped (it then skips the
+        // work only): the status word is written by the side-stream tail and can differ
+        // between ranks for an iteration or two, so no wait on the tail is needed here.
         TIMED(kind, by,
               launch_block_dot(ctx->n_local, p, ctx->d_V, ctx->ldv, u, z, out, ctx->d_part,
-                               ctx->d_counter, ctx->bdot_grid, ctx->capturing ? nullptr : istate, ctx->stream,
-                               nullptr, ctx->d_xchg));
+                               ctx->d_counter, ctx->bdot_grid, istate, ctx->stream, ctx->d_xchg));
         ctx->n_allreduce++;
         ctx->n_reduce++;
         return IGS_OK;
     }
     TIMED(kind, by,
           launch_block_dot(ctx->n_local, p, ctx->d_V, ctx->ldv, u, z, out, ctx->d_part,
-                           ctx->d_counter, ctx->bdot_grid, istate, ctx->stream,
-                           ctx->tm_ok ? &ctx->tmV256 : nullptr));
+                           ctx->d_counter, ctx->bdot_grid, istate, ctx->stream));
     TRY(allreduce(ctx, out, z ? 2 * (p + 1) : p + 1));
     ctx->n_reduce++;
     return IGS_OK;
@@ -944,7 +1056,7 @@ static igs_status fetch(igs_ctx* ctx, const double* dsrc, int nd, double* hd, co
                         int ni, int* hi) {
     if (nd) CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned, dsrc, sizeof(double) * nd, cudaMemcpyDeviceToHost, ctx->stream));
     if (ni) CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned_int, isrc, sizeof(int) * ni, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    TRY(wait_for(ctx, nullptr, ctx->stream, "igs_solve"));
     if (nd) std::memcpy(hd, ctx->h_pinned, sizeof(double) * nd);
     if (ni) std::memcpy(hi, ctx->h_pinned_int, sizeof(int) * ni);
     return IGS_OK;
@@ -958,7 +1070,8 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0);
 // alg: IGS_ALG_IGS1 (1), IGS_ALG_IGS2 (2, Alg. 3), IGS_ALG_IGS2_TWO (3, Alg. 2 literal),
 // IGS_ALG_MGS (4).  Algorithms 1 and 3 share the gs = 1 small-step stages.
 static bool use_pcycle(const igs_ctx* ctx, int alg) {
-    return ctx->pc_enabled && ctx->nranks == 1 && !ctx->xchg_req && !ctx->force_nccl && ctx->n_local <= ctx->pc_max_n && !ctx->fused_enabled &&
+    return ctx->pc_enabled && ctx->nranks == 1 && !ctx->xchg_req && !ctx->force_nccl && ctx->A.n_bnd == 0 &&
+           ctx->n_local <= ctx->pc_max_n &&
            (alg == IGS_ALG_IGS1 || alg == IGS_ALG_IGS2) && ctx->dev_state.m <= 1024;
 }
 
@@ -1061,37 +1174,18 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         ctx->n_pcycle++;
         ctx->n_iter += m;
         ctx->n_reduce += m;
-        if (!ctx->capturing) CUDA_TRY(cudaStreamSynchronize(st));
+        if (!ctx->capturing) TRY(wait_for(ctx, nullptr, st, "igs_solve: cycle"));
         return IGS_OK;
     }
     const int poll_every = 16;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int ev_slot = 0, ev_pending = -1;
     int* h_status = ctx->h_pinned_int + 16;  // 2 slots
-    bool dots_ready = false;  // dots of iteration p already produced by the fused kernel
     for (int p = 1; p <= m; p++) {
         const bool drain = (p == m);
         double* u = Vcol(ctx, p);
-        if (!dots_ready) {
-            if (!drain && ctx->bs_ok && !ctx->xchg_req && bdot_spmv_fits(p)) {
-                // Step 4: z = A u and the fused block dot in one bulk-copy pipeline
-                TRY(halo(ctx, u, ist));
-                const double by = 8.0 * n * (p + 1) + spmv_bytes(ctx);
-                TIMED(IGS_K_BLOCK_DOT, by, {
-                    cudaError_t el_ = launch_bdot_spmv(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z,
-                                                      static_cast<const int32_t*>(ctx->A.rowptr),
-                                                      static_cast<const int32_t*>(ctx->A.col), ctx->A.val,
-                                                      ctx->A.ghost, d.dots + (int64_t)p * d.dld, ctx->d_part,
-                                                      ctx->d_counter, ctx->num_sms, ist, st);
-                    CUDA_TRY(el_);
-                });
-                TRY(allreduce(ctx, d.dots + (int64_t)p * d.dld, 2 * (p + 1)));
-                ctx->n_reduce++;
-            } else {
-                if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
-                TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
-            }
-        }
+        if (!drain) TRY(spmv(ctx, u, ctx->d_z, nullptr, false, ist, IGS_K_SPMV));  // Step 4
+        TRY(bdot(ctx, p, u, drain ? nullptr : ctx->d_z, d.dots + (int64_t)p * d.dld, ist, IGS_K_BLOCK_DOT));
         // (no wait on tail(p-1): the critical step reads nothing the tail writes; a stop the
         //  tail decides is seen one iteration later at worst, and the tails stay ordered on
         //  the side stream; the cycle end joins the side stream)
@@ -1104,28 +1198,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         CUDA_TRY(cudaGetLastError());
         if (ctx->timing) ctx->tail_launches++;
         CUDA_TRY(cudaEventRecord(ctx->ev_tail, ctx->side));
-        const int T = fused_tile_rows();
-        // L2 window of the fused kernel: phase A may lead phase B by `ahead` own tiles of every
-        // CTA, ahead = ceil(L / G) + 2 with L = ceil(reach / T) (fused.cu)
-        const int64_t Lt = (ctx->reach + T - 1) / T, Gf = ctx->fused_grid;
-        const double window = (double)(((Lt + Gf - 1) / Gf + 2) * Gf + 2) * T * (p + 3) * 8.0;
-        if (!drain && !two_reduce && ctx->nranks == 1 && !ctx->xchg_req && ctx->fused_enabled && ctx->fused_ok && ctx->d_flags && p + 2 <= fused_max_cols() &&
-            window <= ctx->fused_budget && n >= 4 * T) {
-            // update(p) + SpMV(p+1) + block dot(p+1), V_p read from HBM once
-            const int lag = (int)((ctx->reach + T - 1) / T);
-            const bool dr1 = (p + 1 == m);
-            const double by = 8.0 * n * p + 32.0 * n + (dr1 ? 0.0 : spmv_bytes(ctx) - 8.0 * n);
-            ctx->epoch++;
-            TIMED(IGS_K_UPDATE, by, {
-                cudaError_t el_ = launch_fused(n, p, m, ctx->d_V, ctx->ldv, ctx->d_z, gs == 2 ? d.alpha : nullptr,
-                                              d.beta, d.scal + SC_GAMMA, ctx->A, lag, ctx->d_flags, ctx->epoch,
-                                              ctx->d_part, d.dots + (int64_t)(p + 1) * d.dld, ctx->d_counter,
-                                              ist, ctx->fused_grid, st);
-                CUDA_TRY(el_);
-            });
-            ctx->n_fused++;
-            dots_ready = true;
-        } else {
+        {
             const double ub = 8.0 * n * ((gs == 2 || !drain) ? p : 0) + 16.0 * n + (drain ? 0.0 : 16.0 * n);
             // the dots re-read the CTAs' tiles from L2: fused while grid x 512 rows x p
             // columns stays within ~80 MB (p <= 32 at 4 CTAs per SM; measured slower beyond)
@@ -1135,7 +1208,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             // 7.6K vs 9.6K it/s fused -- so fuse only with at least one 512-row tile per SM)
             const bool fuse2_l2 = two_reduce && !drain && ctx->two_fused && n >= (int64_t)ctx->num_sms * 512 &&
                                   (double)update_dot_grid(n, ctx->num_sms) * 512.0 * p * 8.0 <= ctx->two_fused_l2;
-            const bool fuse2_tma = !fuse2_l2 && two_reduce && !drain && ctx->two_fused && ctx->two_tma && p >= 1 &&
+            const bool fuse2_tma = !fuse2_l2 && two_reduce && !drain && ctx->two_fused && p >= 1 &&
                                    n >= (int64_t)ctx->num_sms * 512 &&
                                    update_dot_tma_rows(p) > 0 && (ctx->ldv % 2) == 0 &&
                                    ((uintptr_t)ctx->d_V % 16) == 0 && ((uintptr_t)u % 16) == 0 &&
@@ -1144,12 +1217,11 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             if (fuse2) {
                 // Alg. 2 two-reduce: the update fused with the second sweep's block dot
                 // r2 = V_{p+1}^T u' (one HBM read of V_p; the dots re-read it from L2)
-                if (ctx->d_xchg && !ctx->capturing) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
                 const int64_t ntl = fuse2_tma ? (n + update_dot_tma_rows(p) - 1) / update_dot_tma_rows(p) : 1;
                 int grid = fuse2_tma ? (int)std::min<int64_t>(ntl, ctx->num_sms) : update_dot_grid(n, ctx->num_sms);
                 const int64_t cap = (int64_t)ctx->bdot_grid * (2 * (d.m + 1) + 2) / (p + 2);
                 grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, cap));
-                const int* ist2 = ctx->d_xchg && ctx->capturing ? nullptr : ist;
+                const int* ist2 = ist;  // with the exchange the kernel joins it even when stopped
                 if (fuse2_tma)
                     TIMED(IGS_K_UPDATE, ub,
                           launch_update_dot_tma(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
@@ -1168,7 +1240,6 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
                       launch_update(n, p, ctx->d_V, ctx->ldv, u, ctx->d_z, gs == 2 ? d.alpha : nullptr,
                                     d.beta, d.scal + SC_GAMMA, u, drain ? nullptr : Vcol(ctx, p + 1), ist, p, st));
             }
-            dots_ready = false;
             if (two_reduce && !drain) {
                 // Alg. 2 Steps 14-16: r2 = V_{p+1}^T u (second reduction), r3 = (I+L)^{-1} r2,
                 // w = u - V_{p+1} r3 (in place), H[:p+1, p] = r1 + r3
@@ -1188,10 +1259,14 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
                 CUDA_TRY(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
                 CUDA_TRY(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
             }
+            // with collectives in the loop the copied status must be the same on every rank:
+            // read it after tail(p) (the status through iteration p is then final), so all
+            // ranks leave the loop at the same checkpoint and issue the same collectives
+            if (ctx->comm) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
             CUDA_TRY(cudaMemcpyAsync(h_status + ev_slot, ist + ST_STATUS, sizeof(int), cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaEventRecord(ev[ev_slot], st));
             if (ev_pending >= 0) {
-                CUDA_TRY(cudaEventSynchronize(ev[ev_pending]));
+                TRY(wait_for(ctx, ev[ev_pending], nullptr, "igs_solve: checkpoint"));
                 if (h_status[ev_pending] != RUNNING) { ev_pending = -1; break; }
             }
             ev_pending = ev_slot;
@@ -1199,7 +1274,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         }
     }
     CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
-    if (!ctx->capturing) CUDA_TRY(cudaStreamSynchronize(st));
+    if (!ctx->capturing) TRY(wait_for(ctx, nullptr, st, "igs_solve: cycle"));
     if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
     return IGS_OK;
 }
@@ -1215,10 +1290,10 @@ static igs_status mgs_step(igs_ctx* ctx, const double* v, const double* vn, cons
     int grid = mgs_step_grid(n, ctx->num_sms);
     grid = std::min(grid, 4 * ctx->bdot_grid - 1);
     const double by = 8.0 * n * ((v ? 3 : 1) + (vn ? 1 : 0));
-    if (ctx->d_xchg && !ctx->capturing) CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_tail, 0));
+    // (with the exchange the kernel joins it even when stopped; see bdot())
     TIMED(IGS_K_BLOCK_DOT, by,
-          launch_mgs_step(n, v, ctx->d_z, vn, hsrc, Hdst, ctx->d_part, out, ctx->d_counter, grid,
-                          ctx->d_xchg && ctx->capturing ? nullptr : ist, ctx->d_xchg, ctx->stream));
+          launch_mgs_step(n, v, ctx->d_z, vn, hsrc, Hdst, ctx->d_part, out, ctx->d_counter, grid, ist,
+                          ctx->d_xchg, ctx->stream));
     ctx->n_reduce++;
     if (ctx->d_xchg) {
         ctx->n_allreduce++;
@@ -1273,14 +1348,14 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0) {
             CUDA_TRY(cudaMemcpyAsync(h_status + ev_slot, ist + ST_STATUS, sizeof(int), cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaEventRecord(ev[ev_slot], st));
             if (ev_pending >= 0) {
-                CUDA_TRY(cudaEventSynchronize(ev[ev_pending]));
+                TRY(wait_for(ctx, ev[ev_pending], nullptr, "igs_solve: checkpoint"));
                 if (h_status[ev_pending] != RUNNING) break;
             }
             ev_pending = ev_slot;
             ev_slot ^= 1;
         }
     }
-    if (!ctx->capturing) CUDA_TRY(cudaStreamSynchronize(st));
+    if (!ctx->capturing) TRY(wait_for(ctx, nullptr, st, "igs_solve: cycle"));
     if (ev[0]) { cudaEventDestroy(ev[0]); cudaEventDestroy(ev[1]); }
     return IGS_OK;
 }
@@ -1293,10 +1368,11 @@ static igs_status launch_cycle(igs_ctx* ctx, int m, int alg, int t0) {
     ctx->h_pinned[40] = (double)t0;
     CUDA_TRY(cudaMemcpyAsync(ctx->dev_state.scal + SC_T0, ctx->h_pinned + 40, sizeof(double),
                              cudaMemcpyHostToDevice, st));
-    const bool use_graph = ctx->graphs_enabled && !ctx->timing && ctx->nranks == 1 && !ctx->force_nccl &&
-                           !use_pcycle(ctx, alg) &&
-                           ctx->n_local <= ((int64_t)1 << 21) && !ctx->fused_enabled &&
-                           m <= 512 &&
+    // (G > 1 too: the halo send/recv, ncclAllReduce and the exchange kernels are captured;
+    //  every rank captures the same sequence, and a stop inside the cycle turns the remaining
+    //  work into no-ops while the collectives still run on every rank)
+    const bool use_graph = ctx->graphs_enabled && !ctx->timing && !use_pcycle(ctx, alg) &&
+                           ctx->n_local <= ((int64_t)1 << 21) && m <= 512 &&
                            (alg != IGS_ALG_MGS || (int64_t)m * (m + 7) / 2 <= 50000);  // MGS: O(m^2) nodes
     if (!use_graph) return run_cycle(ctx, m, alg, t0);
     // capture and replay on a private stream (the caller's may be the legacy default stream,
@@ -1353,7 +1429,12 @@ extern "C" igs_status igs_solve(igs_ctx* ctx, igs_mem vec_mem, const double* b, 
 extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double* b, const double* x0,
                                     int k, int restart, double tol, int algorithm, igs_result* res) {
     const int gs_iters = algorithm;
+    if (ctx && ctx->aborted) {
+        set_error("igs_solve: the communicator was aborted after an earlier failure; destroy the context");
+        return IGS_ERR_STATE;
+    }
     ARG_CHECK(ctx && ctx->ok, "igs_solve: bad context");
+    ARG_CHECK(!ctx->vgroup, "igs_solve: virtual-rank contexts (igs_create_virtual) only run igs_virtual_spmv");
     ARG_CHECK(res && res->x && b, "igs_solve: NULL b / res / res->x");
     ARG_CHECK(algorithm >= IGS_ALG_IGS1 && algorithm <= IGS_ALG_MGS, "igs_solve_alg: unknown algorithm");
     ARG_CHECK(k >= 1 && (int64_t)k < ctx->n_global - 1, "igs_solve: need 1 <= k < n_global - 1 (P:873)");
@@ -1391,7 +1472,7 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     const int64_t ar0 = ctx->n_allreduce;
     unsigned red0 = 0;  // reductions executed on the device (block dots that ran to completion)
     CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned_int + 24, ctx->d_counter + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    TRY(wait_for(ctx, nullptr, st, "igs_solve"));
     std::memcpy(&red0, ctx->h_pinned_int + 24, sizeof(unsigned));
 
     // ||b|| (one reduction; also the non-finite check of b)
@@ -1415,7 +1496,7 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     if (nb == 0.0) {
         CUDA_TRY(cudaMemsetAsync(dx, 0, sizeof(double) * n, st));
         if (hostv) CUDA_TRY(cudaMemcpyAsync(res->x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
+        TRY(wait_for(ctx, nullptr, st, "igs_solve"));
         res->term = IGS_TERM_CONVERGED;
         res->true_relres = 0.0;
         if (res->res_hist) res->res_hist[0] = 0.0;
@@ -1452,6 +1533,13 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         TRY(launch_cycle(ctx, m, gs_iters, total));
         int istate[ST_COUNT];
         TRY(fetch(ctx, nullptr, 0, nullptr, d.istate, ST_COUNT, istate));
+        if (ctx->d_xchg) {  // the exchange barrier gave up on a peer (xchg.cuh): fail, do not hang
+            int xerr = 0;
+            TRY(fetch(ctx, nullptr, 0, nullptr, ctx->d_xerr, 1, &xerr));
+            if (xerr)
+                return abort_comm(ctx, "igs_solve: fused exchange barrier timeout after " +
+                                           std::to_string(ctx->timeout_s) + " s (a peer rank did not arrive)");
+        }
         const int status = istate[ST_STATUS], p = istate[ST_PDONE];
         if (status == STOP_NONFINITE) {
             set_error("igs_solve: non-finite value during the Arnoldi iteration");
@@ -1481,11 +1569,12 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         CUDA_TRY(cudaMemcpyAsync(hl.data(), d.lnorm, sizeof(double) * (total + 1), cudaMemcpyDeviceToHost, st));
     res->s_norm = std::nan("");
     res->sigma_min = std::nan("");
+    res->lgram_frob = std::nan("");
     // LOO of the final basis, ||S||_2 and sigma_min: diagnostics from G = V^T V
     if ((res->want_loo || res->want_basis_diag) && last_basis > 0) {
         const int c = last_basis;
         const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 4096));
-        const size_t need = (size_t)splits * c * c + (size_t)c * c + 1;
+        const size_t need = (size_t)splits * c * c + (size_t)c * c + 2;
         if (need > ctx->gram_cap) {
             cudaFree(ctx->d_gram);
             ctx->d_gram = nullptr;
@@ -1496,9 +1585,10 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         TIMED(IGS_K_CYCLE, 8.0 * n * c, launch_gram(n, c, ctx->d_V, ctx->ldv, ctx->d_gram, splits, G, st));
         TRY(allreduce(ctx, G, (int64_t)c * c));
         TIMED(IGS_K_CYCLE, 0.0, launch_loo_norm(c, G, G + (size_t)c * c, st));
-        double loo = 0.0;
-        TRY(fetch(ctx, G + (size_t)c * c, 1, &loo, nullptr, 0, nullptr));
-        if (res->want_loo) res->loo_frob = loo;
+        double loo[2] = {0.0, 0.0};
+        TRY(fetch(ctx, G + (size_t)c * c, 2, loo, nullptr, 0, nullptr));
+        if (res->want_loo) res->loo_frob = loo[0];
+        res->lgram_frob = loo[1];
         if (res->want_basis_diag && c <= IGS_BASIS_DIAG_MAX) {  // larger bases: NaN (one-CTA Jacobi)
             double* ws = nullptr;
             CUDA_TRY(cudaMalloc(&ws, sizeof(double) * (basis_diag_doubles(c) + 2)));
@@ -1512,7 +1602,7 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         }
     }
     if (hostv) CUDA_TRY(cudaMemcpyAsync(res->x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    TRY(wait_for(ctx, nullptr, st, "igs_solve"));
     CUDA_TRY(cudaGetLastError());
     if (res->res_hist) std::memcpy(res->res_hist, hres.data(), sizeof(double) * (total + 1));
     if (res->lnorm_hist) {
@@ -1524,10 +1614,80 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
     res->allreduces = ctx->n_allreduce - ar0;
     {
         unsigned red1 = 0;
-        CUDA_TRY(cudaMemcpy(&red1, ctx->d_counter + 1, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_pinned_int + 24, ctx->d_counter + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        TRY(wait_for(ctx, nullptr, st, "igs_solve"));
+        std::memcpy(&red1, ctx->h_pinned_int + 24, sizeof(unsigned));
         res->reductions = (int64_t)(red1 - red0);
     }
     TRY(timer_flush(ctx));
+    return IGS_OK;
+}
+
+// ------------------------------------------------------------ virtual ranks (test hook)
+extern "C" igs_status igs_create_virtual(igs_ctx** out, int nranks, int64_t n_global, const int64_t* bounds,
+                                         const int64_t* rowptr, const void* colind, int colind_bits,
+                                         const double* values, int cuda_device, void* cuda_stream) {
+    ARG_CHECK(out && nranks >= 1 && n_global > 0 && bounds && rowptr && (colind_bits == 32 || colind_bits == 64),
+              "igs_create_virtual: bad argument");
+    ARG_CHECK(bounds[0] == 0 && bounds[nranks] == n_global, "igs_create_virtual: bounds must span [0, n_global)");
+    for (int r = 0; r < nranks; r++) {
+        out[r] = nullptr;
+        ARG_CHECK(bounds[r + 1] >= bounds[r], "igs_create_virtual: bounds not monotone");
+    }
+    const size_t cb = colind_bits / 8;
+    VirtPlan vp;
+    vp.bounds.assign(bounds, bounds + nranks + 1);
+    vp.ghosts.resize(nranks);
+    std::vector<std::vector<int64_t>> rp(nranks);
+    for (int r = 0; r < nranks; r++) {  // rank r's CSR block with local row offsets
+        const int64_t r0 = bounds[r], nl = bounds[r + 1] - r0;
+        rp[r].resize(nl + 1);
+        for (int64_t i = 0; i <= nl; i++) rp[r][i] = rowptr[r0 + i] - rowptr[r0];
+        const char* cr = static_cast<const char*>(colind) + cb * rowptr[r0];
+        int64_t ng = 0;
+        std::vector<int64_t> oc(nranks);
+        TRY(igs_plan_ghosts(r0, nl, rp[r].data(), cr, colind_bits, nranks, bounds, &ng, nullptr, oc.data()));
+        vp.ghosts[r].resize(ng);
+        TRY(igs_plan_ghosts(r0, nl, rp[r].data(), cr, colind_bits, nranks, bounds, &ng, vp.ghosts[r].data(), oc.data()));
+    }
+    VGroup* g = new VGroup();
+    g->G = nranks;
+    g->members.assign(nranks, nullptr);
+    for (int r = 0; r < nranks; r++) {
+        const int64_t r0 = bounds[r], nl = bounds[r + 1] - r0;
+        const char* cr = static_cast<const char*>(colind) + cb * rowptr[r0];
+        igs_status st = create_ctx(&out[r], n_global, r0, nl, rp[r].data(), cr, colind_bits, values + rowptr[r0],
+                                   rp[r][nl], IGS_MEM_HOST, cuda_device, nullptr, r, nranks, cuda_stream, &vp);
+        if (st != IGS_OK) {
+            const std::string msg = igs_last_error();
+            for (int q = 0; q < r; q++) { out[q]->vgroup = nullptr; free_ctx(out[q]); out[q] = nullptr; }
+            delete g;
+            set_error(msg);
+            return st;
+        }
+        out[r]->vgroup = g;
+        g->members[r] = out[r];
+        g->alive++;
+    }
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_virtual_spmv(igs_ctx* const* ctxs, int nranks, const double* const* x, double* const* y,
+                                       const double* const* b) {
+    ARG_CHECK(ctxs && x && y && nranks >= 1, "igs_virtual_spmv: bad argument");
+    VGroup* g = ctxs[0] ? ctxs[0]->vgroup : nullptr;
+    ARG_CHECK(g && g->G == nranks, "igs_virtual_spmv: not one complete virtual group");
+    for (int r = 0; r < nranks; r++)
+        ARG_CHECK(ctxs[r] == g->members[r] && ((x[r] && y[r]) || ctxs[r]->n_local == 0),
+                  "igs_virtual_spmv: contexts not in rank order / NULL vector");
+    igs_ctx* c0 = ctxs[0];
+    CUDA_TRY(cudaSetDevice(c0->dev));
+    for (int r = 0; r < nranks; r++)  // every rank's send buffer first (the copies read them)
+        launch_pack(ctxs[r]->n_send, ctxs[r]->d_send_idx, x[r], ctxs[r]->d_send, nullptr, ctxs[r]->stream);
+    CUDA_TRY(cudaGetLastError());
+    for (int r = 0; r < nranks; r++)
+        TRY(spmv(ctxs[r], x[r], y[r], b ? b[r] : nullptr, b != nullptr, nullptr, IGS_K_SPMV));
+    for (int r = 0; r < nranks; r++) TRY(wait_for(ctxs[r], nullptr, ctxs[r]->stream, "igs_virtual_spmv"));
     return IGS_OK;
 }
 
@@ -1537,6 +1697,36 @@ extern "C" igs_status igs_stats(const igs_ctx* ctx, int64_t* allreduces, int64_t
     if (allreduces) *allreduces = ctx->n_allreduce;
     if (halo_msgs) *halo_msgs = ctx->n_halo;
     if (iterations) *iterations = ctx->n_iter;
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value) {
+    ARG_CHECK(ctx != nullptr && value != nullptr, "igs_info: NULL argument");
+    switch (key) {
+        case IGS_INFO_XCHG: *value = ctx->d_xchg != nullptr; break;
+        case IGS_INFO_NRANKS: *value = ctx->nranks; break;
+        case IGS_INFO_NGHOST: *value = ctx->n_ghost; break;
+        case IGS_INFO_NSEND: *value = ctx->n_send; break;
+        case IGS_INFO_NPEERS: *value = (int64_t)ctx->peers.size(); break;
+        case IGS_INFO_NBND: *value = ctx->A.n_bnd; break;
+        case IGS_INFO_GRAPH_LAUNCHES: *value = ctx->n_graph_launches; break;
+        case IGS_INFO_PCYCLE_LAUNCHES: *value = ctx->n_pcycle; break;
+        case IGS_INFO_SELL: *value = ctx->A.sell_ptr != nullptr; break;
+        case IGS_INFO_CSR_COMPACT: *value = ctx->csr_compact; break;
+        default: ARG_CHECK(false, "igs_info: unknown key");
+    }
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_set_timeout(igs_ctx* ctx, double seconds) {
+    ARG_CHECK(ctx != nullptr && seconds > 0.0 && std::isfinite(seconds), "igs_set_timeout: bad argument");
+    ctx->timeout_s = seconds;
+    if (ctx->d_xchg && !ctx->aborted) {
+        CUDA_TRY(cudaSetDevice(ctx->dev));
+        ctx->h_xchg.timeout_ns = (unsigned long long)(seconds * 1e9);
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_xchg, &ctx->h_xchg, sizeof(XchgDev), cudaMemcpyHostToDevice, ctx->stream));
+        TRY(wait_for(ctx, nullptr, ctx->stream, "igs_set_timeout"));
+    }
     return IGS_OK;
 }
 
@@ -1585,15 +1775,49 @@ extern "C" igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_
     CUDA_TRY(cudaMalloc(&part, sizeof(double) * (size_t)grid * 2 * (p + 1)));
     CUDA_TRY(cudaMalloc(&counter, 4 * sizeof(unsigned)));
     CUDA_TRY(cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned), st));
-    CUtensorMap tm;
-    const char* etm = std::getenv("IGS_TMAP");
-    const bool tmok = etm && std::atoi(etm) != 0 && p > 0 && make_tensor_map(&tm, V, n, p, ld, 256, 8);
-    launch_block_dot(n, p, V, ld, u, z, out, part, counter, grid, nullptr, st, tmok ? &tm : nullptr);
+    launch_block_dot(n, p, V, ld, u, z, out, part, counter, grid, nullptr, st);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(part);
     cudaFree(counter);
     CUDA_TRY(e);
+    return IGS_OK;
+}
+
+// Measurement hook: `reps` back-to-back block dots (the solver's launch path) timed with
+// CUDA events on cuda_stream; scratch allocated outside the timed region.
+extern "C" igs_status igs_bench_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                                          const double* z, double* out, int reps, float* ms,
+                                          void* cuda_stream) {
+    ARG_CHECK(n >= 1 && p >= 0 && u && out && ms && reps >= 1 && (p == 0 || V), "igs_bench_block_dot: bad argument");
+    ARG_CHECK(p == 0 || (ld >= n && ld % 2 == 0 && ((uintptr_t)V % 16) == 0), "igs_bench_block_dot: V needs even ld >= n and 16-byte alignment");
+    TRY(have_device());
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    int dev = 0, sms = 148;
+    CUDA_TRY(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = bdot_grid_size(n, sms);
+    double* part = nullptr;
+    unsigned* counter = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    CUDA_TRY(cudaMalloc(&part, sizeof(double) * (size_t)grid * 2 * (p + 1)));
+    CUDA_TRY(cudaMalloc(&counter, 4 * sizeof(unsigned)));
+    struct Free { double* p; unsigned* c; cudaEvent_t a, b;
+                  ~Free() { cudaFree(p); cudaFree(c); if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); } }
+        guard{part, counter, nullptr, nullptr};
+    CUDA_TRY(cudaEventCreate(&e0));
+    guard.a = e0;
+    CUDA_TRY(cudaEventCreate(&e1));
+    guard.b = e1;
+    CUDA_TRY(cudaMemsetAsync(counter, 0, 4 * sizeof(unsigned), st));
+    launch_block_dot(n, p, V, ld, u, z, out, part, counter, grid, nullptr, st);  // warm-up
+    CUDA_TRY(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; r++) launch_block_dot(n, p, V, ld, u, z, out, part, counter, grid, nullptr, st);
+    CUDA_TRY(cudaEventRecord(e1, st));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventSynchronize(e1));
+    CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
+    *ms /= (float)reps;
     return IGS_OK;
 }
 
@@ -1690,13 +1914,13 @@ extern "C" igs_status igs_op_basis_diag(int64_t n, int c, const double* V, int64
     TRY(have_device());
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
     const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / 4096));
-    const size_t nd = (size_t)splits * c * c + (size_t)c * c + 1 + basis_diag_doubles(c) + 2;
+    const size_t nd = (size_t)splits * c * c + (size_t)c * c + 2 + basis_diag_doubles(c) + 2;
     double* ws = nullptr;
     CUDA_TRY(cudaMalloc(&ws, nd * sizeof(double)));
     struct Free { double* w; ~Free() { cudaFree(w); } } guard{ws};
     double* G = ws + (size_t)splits * c * c;
-    double* loo = G + (size_t)c * c;
-    double* dws = loo + 1;
+    double* loo = G + (size_t)c * c;  // [||I - G||_F, ||tril(G, -1)||_F]
+    double* dws = loo + 2;
     double* sd = dws + basis_diag_doubles(c);
     launch_gram(n, c, V, ld, ws, splits, G, st);
     launch_loo_norm(c, G, loo, st);

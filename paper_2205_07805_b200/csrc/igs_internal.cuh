@@ -54,12 +54,6 @@ struct Dev {
     double* lnorm;     // [kmax+1] ||L||_F of the current cycle after iteration t
 };
 
-// 2D TMA descriptors of a column-major n x ncols FP64 block with leading dimension ld
-// (api.cu builds them with cuTensorMapEncodeTiled through cudaGetDriverEntryPoint).
-// box8: (box_rows x 8 columns); box1: (box_rows x 1 column).
-bool make_tensor_map(CUtensorMap* tm, const double* base, int64_t n, int64_t ncols, int64_t ld,
-                     int box_rows, int box_cols);
-
 // ---- launchers (kernels.cu) -----------------------------------------------------------
 struct SpmvArgs {
     int64_t nrows;
@@ -77,7 +71,8 @@ struct SpmvArgs {
     const double* sell_val = nullptr;
     const void* sell_col = nullptr;     // int32 or int64 (idx64), local column space
     // G > 1: rows with a ghost column (sell_len == SELL_BOUNDARY, not in the SELL arrays),
-    // multiplied from the CSR arrays by launch_spmv_rows once the halo has arrived
+    // multiplied by launch_spmv_rows once the halo has arrived.  With a SELL copy the CSR
+    // arrays above hold only these rows (row t of the compact CSR is row bnd_rows[t])
     const int64_t* bnd_rows = nullptr;
     int64_t n_bnd = 0;
 };
@@ -106,8 +101,7 @@ int bdot_grid_size(int64_t n, int num_sms);
 struct XchgDev;  // xchg.cuh: fused cross-rank sum over NVLink (NCCL device API)
 void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                       const double* z, double* out, double* part, unsigned* counter, int grid,
-                      const int* istate, cudaStream_t s, const CUtensorMap* tmV = nullptr,
-                      const XchgDev* xc = nullptr);
+                      const int* istate, cudaStream_t s, const XchgDev* xc = nullptr);
 
 // Fused update (see igs.h igs_op_update).  gamma read from *gamma_dev.
 // istate/it: when istate != NULL the mode bits istate[ST_MODE] (valid iff
@@ -184,26 +178,5 @@ void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, 
 
 // small helpers
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
-
-// bdot_spmv.cu: SpMV + block dot of one iteration in one bulk-copy pipeline (int32 CSR whose
-// arrays are padded by >= 8 entries; every 256-row tile has <= bdot_spmv_nnz_cap() nonzeros)
-int bdot_spmv_tile_rows();
-int bdot_spmv_nnz_cap();
-bool bdot_spmv_fits(int p);
-cudaError_t launch_bdot_spmv(int64_t n, int p, const double* V, int64_t ld, const double* u, double* z,
-                             const int32_t* rowptr, const int32_t* col, const double* val,
-                             const double* ghost, double* out, double* part, unsigned* counter,
-                             int grid, const int* istate, cudaStream_t s);
-
-// fused.cu: update(p) + SpMV(p+1) + block dot(p+1) in one persistent wavefront kernel
-int fused_max_cols();
-int fused_tile_rows();
-int fused_nnz_cap();
-int fused_grid(int num_sms);
-cudaError_t launch_fused(int64_t n, int p, int m, const double* V, int64_t ld, double* z,
-                         const double* alpha, const double* beta, const double* gamma_dev,
-                         const SpmvArgs& A, int lag, long long* progress, int epoch, double* part,
-                         double* out, unsigned* counter, const int* istate, int grid,
-                         cudaStream_t s);
 
 }  // namespace igs

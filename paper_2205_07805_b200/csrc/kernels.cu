@@ -215,16 +215,15 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
                       const int* istate, cudaStream_t s) {
     const unsigned blocks = (unsigned)((a.nrows + SELL_THREADS - 1) / SELL_THREADS);
     if (blocks == 0) return;
-    // L2 prefetch distance in CTAs: about one resident wave (4 CTAs per SM of 256 threads);
-    // IGS_SELL_PF overrides (0 = off).  c4: 5.5 -> 6.4 TB/s (the latency of the dependent
-    // value/column -> gather phases now hits L2 instead of DRAM)
+    // L2 prefetch distance in CTAs: about one resident wave (4 CTAs per SM of 256 threads).
+    // c4: 5.5 -> 6.4 TB/s (the latency of the dependent value/column -> gather phases now
+    // hits L2 instead of DRAM)
     static int ahead = -1;
     if (ahead < 0) {
-        const char* e = getenv("IGS_SELL_PF");
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        ahead = e ? atoi(e) : 4 * sms;
+        ahead = 4 * sms;
     }
     const IT* ci = static_cast<const IT*>(a.sell_col);
     if (a.ghost) {
@@ -236,8 +235,10 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
     }
 }
 
-// Boundary rows (G > 1): one thread per listed row, CSR arrays, ghosts for columns >= nloc,
-// separate multiply and add left to right (the same rounding as the SELL / CSR kernels).
+// Boundary rows (G > 1): one thread per listed row rows[t], whose entries are entries
+// rowptr[t]..rowptr[t+1] of the compact boundary-row CSR (igs_create keeps only these rows
+// next to the SELL copy), ghosts for columns >= nloc, separate multiply and add left to
+// right (the same rounding as the SELL / CSR kernels).
 template <typename IT, typename PT, bool RESID>
 __global__ void __launch_bounds__(256)
     spmv_rows_kernel(int64_t nb, const int64_t* __restrict__ rows, const PT* __restrict__ rowptr,
@@ -249,8 +250,8 @@ __global__ void __launch_bounds__(256)
     if (t >= nb) return;
     const int64_t r = __ldg(rows + t);
     double sum = 0.0;
-    const int64_t q1 = (int64_t)__ldg(rowptr + r + 1);
-    for (int64_t q = (int64_t)__ldg(rowptr + r); q < q1; q++) {
+    const int64_t q1 = (int64_t)__ldg(rowptr + t + 1);
+    for (int64_t q = (int64_t)__ldg(rowptr + t); q < q1; q++) {
         const int64_t c = (int64_t)__ldg(col + q);
         const double xv = c >= nloc ? __ldg(ghost + (c - nloc)) : __ldg(x + c);
         sum = __dadd_rn(sum, __dmul_rn(__ldg(val + q), xv));
@@ -280,9 +281,10 @@ void launch_spmv_rows(const SpmvArgs& a, const double* x, double* y, const doubl
     }
 }
 
-template <int R, typename IT, typename PT>
-static void spmv_stream_r(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
-                          const int* istate, cudaStream_t s) {
+template <typename IT, typename PT>
+static void spmv_stream(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                        const int* istate, cudaStream_t s) {
+    constexpr int R = 1;  // rows per thread
     const unsigned blocks = (unsigned)((a.nrows + SPS_ROWS * R - 1) / (SPS_ROWS * R));
     if (blocks == 0) return;
     const PT* rp = static_cast<const PT*>(a.rowptr);
@@ -294,18 +296,6 @@ static void spmv_stream_r(const SpmvArgs& a, const double* x, double* y, const d
         if (resid) spmv_stream_kernel<R, IT, PT, false, true><<<blocks, SPS_THREADS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
         else spmv_stream_kernel<R, IT, PT, false, false><<<blocks, SPS_THREADS, 0, s>>>(a.nrows, rp, ci, a.val, x, nullptr, a.nloc, y, b, istate);
     }
-}
-
-template <typename IT, typename PT>
-static void spmv_stream(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
-                        const int* istate, cudaStream_t s) {
-    static int R = 0;  // rows per thread (IGS_SPMV_R = 1 | 2, default 1)
-    if (R == 0) {
-        const char* e = getenv("IGS_SPMV_R");
-        R = (e && atoi(e) == 2) ? 2 : 1;
-    }
-    if (R == 2) spmv_stream_r<2, IT, PT>(a, x, y, b, resid, istate, s);
-    else spmv_stream_r<1, IT, PT>(a, x, y, b, resid, istate, s);
 }
 
 template <int LPR, typename IT, typename PT>
@@ -450,7 +440,10 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
                 const double* __restrict__ u, const double* __restrict__ z,
                 double* __restrict__ part, double* __restrict__ out, unsigned* counter,
                 const int* istate, const XchgDev* xc) {
-    if (!running(istate)) return;
+    // a stopped cycle skips the work; with the cross-rank exchange every rank still joins
+    // the exchange (uniform across ranks: the status word can differ between ranks)
+    const bool live = running(istate);
+    if (!live && !xc) return;
     extern __shared__ double sacc[];  // [BD_WARPS][NV * ncols]
     __shared__ bool s_last;
     const int ncols = p + 1;  // columns 0..p-1 of V, then u itself
@@ -460,7 +453,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
     for (int i = lane; i < stride; i += 32) acc[i] = 0.0;
     __syncwarp();
 
-    const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
+    const int64_t ntiles = live ? (n + BD_TILE - 1) / BD_TILE : 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t r0 = tile * BD_TILE + warp * BD_ROWS_W + 2 * lane;
         const int64_t r1 = r0 + 64;
@@ -484,7 +477,7 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
     // stage 2b: last CTA sums the partials in CTA order (+ across ranks over NVLink)
     if (xc) final_reduce_xchg(part, stride, (int)gridDim.x, out, *xc);
     else final_reduce(part, stride, (int)gridDim.x, out);
-    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += live ? 1u : 0u; }  // [1]: reductions executed
 }
 
 // ------------------------------------------------------------------------------------
@@ -511,7 +504,8 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                     const double* __restrict__ u, const double* __restrict__ z,
                     double* __restrict__ part, double* __restrict__ out, unsigned* counter,
                     const int* istate, const XchgDev* xc) {
-    if (!running(istate)) return;
+    const bool live = running(istate);  // see bdot_kernel
+    if (!live && !xc) return;
     extern __shared__ __align__(128) double smem_bt[];
     double* ring = smem_bt;                                        // [STAGES][8][512]
     double* uzslot = ring + BT_STAGES * BT_STAGE_DOUBLES;          // [2 tiles][u | z][512]
@@ -532,7 +526,7 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     __syncthreads();
     const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
     const int ngroups = (ncols + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
-    const int64_t nk = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t nk = (live && ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (warp == BT_CONS_WARPS) {
         // ---------------- producer: one elected lane issues the bulk copies ----------------
         if (lane == 0) {
@@ -653,10 +647,13 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     __syncthreads();
     // stage 2 on the last K CTAs to finish (the grid is co-resident: one CTA per SM), each
     // summing a contiguous slice of the 2(p+1) outputs in CTA order -- the same order as one
-    // finisher, K times the parallelism (c3, p = 300: 602 outputs x 148 partials)
+    // finisher, K times the parallelism (c3, p = 300: 602 outputs x 148 partials).  With the
+    // cross-rank exchange the slices go to this rank's window slot and the last finisher runs
+    // the barrier and the sum over ranks (xchg.cuh).
     const int G = (int)gridDim.x;
-    const int K = xc ? 1 : min(G, max(1, min(16, stride / 32)));
+    const int K = min(G, max(1, min(16, stride / 32)));
     __shared__ unsigned s_ticket;
+    __shared__ bool s_lastf;
     if (threadIdx.x == 0) s_ticket = atomicAdd(counter, 1u);
     __syncthreads();
     const int t = (int)s_ticket;
@@ -671,277 +668,35 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         __syncthreads();
     }
     __threadfence();
-    // [V_p^T u, u.u, V_p^T z, u.z] (+ across ranks over NVLink)
-    if (xc) final_reduce_xchg(part, stride, G, out, *xc);
-    else {
+    const unsigned call = xc ? *(volatile unsigned*)xc->calls : 0u;
+    double* dst = xc ? xchg_slot(*xc, call) : out;  // [V_p^T u, u.u, V_p^T z, u.z]
+    {
         const int f = t - (G - K), per = (stride + K - 1) / K;
         const int i0 = min(stride, f * per), i1 = min(stride, i0 + per);
-        final_reduce_range(part, stride, G, out, i0, i1);
+        final_reduce_range(part, stride, G, dst, i0, i1);
     }
-    if (K == 1) {
+    if (K == 1 && !xc) {
         if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }  // [1]: reductions executed
         return;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // [2]: finishers done; the last one resets the tickets
-        __threadfence();
-        if (atomicAdd(counter + 2, 1u) == (unsigned)(K - 1)) { counter[0] = 0u; counter[2] = 0u; counter[1] += 1u; }
+    if (threadIdx.x == 0) {  // [2]: finishers done; the last one finishes and resets the tickets
+        __threadfence_system();
+        s_lastf = atomicAdd(counter + 2, 1u) == (unsigned)(K - 1);
     }
+    __syncthreads();
+    if (!s_lastf) return;
+    __threadfence();
+    if (xc) xchg_finish(stride, out, *xc, call);
+    if (threadIdx.x == 0) { counter[0] = 0u; counter[2] = 0u; counter[1] += live ? 1u : 0u; }
 }
 
-// ------------------------------------------------------------------------------------
-// K2 (TMA tensor variant, the default): same structure as bdot_tma_kernel, but V is
-// streamed with 2D tensor copies -- one cp.async.bulk.tensor instruction per 8-column x
-// 256-row box (16 KB) -- because a single producer thread issuing 1D bulk copies tops out at
-// a few copies per microsecond (1-4 KB copies measured at 1.7-7 TB/s).  Rows past n and
-// columns past the map come back zero-filled.  12-stage ring (192 KB) per SM.
-// ------------------------------------------------------------------------------------
-constexpr int TM_ROWS = 256;
-constexpr int TM_RPL = TM_ROWS / 32;
-constexpr int TM_STAGES = 12;
-constexpr int TM_STAGE_D = BT_CONS_WARPS * TM_ROWS;  // 8 columns x 256 rows = 16 KB
-
-template <int NV>
-__global__ void __launch_bounds__(BT_THREADS, 1)
-    bdot_tmap_kernel(const __grid_constant__ CUtensorMap tmV, int64_t n, int p,
-                     const double* __restrict__ u, const double* __restrict__ z,
-                     double* __restrict__ part, double* __restrict__ out, unsigned* counter,
-                     const int* istate) {
-    if (!running(istate)) return;
-    extern __shared__ __align__(128) double smem_tm[];
-    double* ring = smem_tm;                                        // [STAGES][8][256]
-    double* uzslot = ring + TM_STAGES * TM_STAGE_D;                // [2 tiles][u | z][256]
-    double* acc = uzslot + 4 * TM_ROWS;                            // [NV*(p+1)]
-    const int ncols = p + 1;
-    const int stride = NV * ncols;
-    uint64_t* full = reinterpret_cast<uint64_t*>(acc + ((stride + 1) & ~1));
-    uint64_t* empty = full + TM_STAGES;
-    uint64_t* uzfull = empty + TM_STAGES;
-    uint64_t* uzempty = uzfull + 2;
-    __shared__ bool s_last;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] = 0.0;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < TM_STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, BT_CONS_WARPS); }
-        for (int s = 0; s < 2; s++) { mbar_init(uzfull + s, 1); mbar_init(uzempty + s, BT_CONS_WARPS); }
-        mbar_fence_init();
-    }
-    __syncthreads();
-    const int64_t ntiles = (n + TM_ROWS - 1) / TM_ROWS;
-    const int ngroups = (ncols + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
-    const int nstream = (p + BT_CONS_WARPS - 1) / BT_CONS_WARPS;  // groups holding V columns
-    const int64_t nk = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    if (warp == BT_CONS_WARPS) {
-        if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
-            auto issue_uz = [&](int64_t k) {
-                const int tb = (int)(k & 1);
-                const int64_t row0 = (blockIdx.x + k * gridDim.x) * TM_ROWS;
-                mbar_wait(uzempty + tb, (uint32_t)(((k >> 1) & 1) ^ 1));
-                if (row0 + TM_ROWS <= n) {
-                    const uint32_t b = TM_ROWS * sizeof(double);
-                    mbar_arrive_expect_tx(uzfull + tb, (NV == 2 ? 2 : 1) * b);
-                    bulk_g2s(uzslot + (2 * tb) * TM_ROWS, u + row0, b, uzfull + tb);
-                    if (NV == 2) bulk_g2s(uzslot + (2 * tb + 1) * TM_ROWS, z + row0, b, uzfull + tb);
-                } else {
-                    mbar_arrive(uzfull + tb);
-                }
-            };
-            if (nk > 0) issue_uz(0);
-            uint32_t it = 0;
-            for (int64_t k = 0; k < nk; k++) {
-                if (k + 1 < nk) issue_uz(k + 1);
-                const int row0 = (int)((blockIdx.x + k * gridDim.x) * TM_ROWS);
-                for (int g = 0; g < nstream; g++, it++) {
-                    const int st = it % TM_STAGES;
-                    mbar_wait(empty + st, ((it / TM_STAGES) & 1) ^ 1);
-                    mbar_arrive_expect_tx(full + st, TM_STAGE_D * sizeof(double));
-                    tma_load_2d(ring + (size_t)st * TM_STAGE_D, &tmV, row0, g * BT_CONS_WARPS, full + st, pol);
-                }
-            }
-        }
-    } else {
-        uint32_t it = 0;
-        for (int64_t kt = 0; kt < nk; kt++) {
-            const int64_t row0 = (blockIdx.x + kt * gridDim.x) * TM_ROWS;
-            const bool full_tile = row0 + TM_ROWS <= n;
-            const int tb = (int)(kt & 1);
-            double ur[TM_RPL], zr[TM_RPL];
-            mbar_wait(uzfull + tb, (uint32_t)((kt >> 1) & 1));
-            if (full_tile) {
-                const double* us = uzslot + (2 * tb) * TM_ROWS;
-                const double* zs = uzslot + (2 * tb + 1) * TM_ROWS;
-#pragma unroll
-                for (int k = 0; k < TM_RPL; k++) {
-                    ur[k] = us[lane + 32 * k];
-                    zr[k] = NV == 2 ? zs[lane + 32 * k] : 0.0;
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < TM_RPL; k++) {
-                    const int64_t r = row0 + lane + 32 * k;
-                    const bool ok = r < n;
-                    ur[k] = ok ? __ldg(u + r) : 0.0;
-                    zr[k] = (NV == 2 && ok) ? __ldg(z + r) : 0.0;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(uzempty + tb);
-            for (int g = 0; g < ngroups; g++) {
-                const int c = g * BT_CONS_WARPS + warp;
-                const bool streamed = g < nstream;
-                const int st = it % TM_STAGES;
-                if (streamed) mbar_wait(full + st, (it / TM_STAGES) & 1);
-                if (c < ncols) {
-                    double su = 0.0, sz = 0.0;
-                    if (c < p) {
-                        const double* col = ring + (size_t)st * TM_STAGE_D + warp * TM_ROWS;
-#pragma unroll
-                        for (int k = 0; k < TM_RPL; k++) {
-                            const double v = col[lane + 32 * k];   // rows >= n are zero-filled
-                            su = fma(v, ur[k], su);
-                            if (NV == 2) sz = fma(v, zr[k], sz);
-                        }
-                    } else {  // column p is u itself
-#pragma unroll
-                        for (int k = 0; k < TM_RPL; k++) {
-                            su = fma(ur[k], ur[k], su);
-                            if (NV == 2) sz = fma(ur[k], zr[k], sz);
-                        }
-                    }
-#pragma unroll
-                    for (int off = 16; off > 0; off >>= 1) {
-                        su += __shfl_xor_sync(FULL_MASK, su, off);
-                        if (NV == 2) sz += __shfl_xor_sync(FULL_MASK, sz, off);
-                    }
-                    if (lane == 0) {
-                        acc[c] += su;
-                        if (NV == 2) acc[ncols + c] += sz;
-                    }
-                }
-                if (streamed) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(empty + st);
-                    it++;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < stride; i += blockDim.x) part[(int64_t)blockIdx.x * stride + i] = acc[i];
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    final_reduce(part, stride, (int)gridDim.x, out);  // [V_p^T u, u.u, V_p^T z, u.z]
-    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
-}
-
-static size_t bdot_tmap_smem(int p, int nv) {
-    const size_t stride = (size_t)nv * (p + 1);
-    return (size_t)(TM_STAGES * TM_STAGE_D + 4 * TM_ROWS) * sizeof(double) +
-           ((stride + 1) & ~(size_t)1) * sizeof(double) + (2 * TM_STAGES + 4) * sizeof(uint64_t);
-}
-
-// ------------------------------------------------------------------------------------
-// K2 (streaming variant): each warp owns a 512-row sub-range (8 chunks of 64 rows; a lane
-// owns rows 2l, 2l+1 of every chunk) and walks ALL column groups over it, accumulating 8
-// column partials per vector in registers across the 8 chunks; the butterfly reduction runs
-// once per (512 rows x 8 columns) instead of once per 128 rows.  Loads of the next chunk are
-// in flight while the current one is multiplied (16 x 16 B per lane).  u, z of the warp's
-// rows are read from shared memory.  Per-warp shared accumulators, fixed-order stage 2.
-// ------------------------------------------------------------------------------------
-constexpr int BS2_WARPS = 8;
-constexpr int BS2_CHUNKS = 8;                      // 64-row chunks per warp
-constexpr int BS2_ROWS_W = 64 * BS2_CHUNKS;        // 512 rows per warp
-constexpr int BS2_TILE = BS2_WARPS * BS2_ROWS_W;   // 4096 rows per CTA tile
-
-template <int NV>
-__global__ void __launch_bounds__(BS2_WARPS * 32, 2)
-    bdot_stream_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
-                       const double* __restrict__ u, const double* __restrict__ z,
-                       double* __restrict__ part, double* __restrict__ out, unsigned* counter,
-                       const int* istate) {
-    if (!running(istate)) return;
-    extern __shared__ __align__(16) double sst[];
-    const int ncols = p + 1;
-    const int stride = NV * ncols;
-    double* suz = sst;                                   // [NV][4096]
-    double* sacc = sst + NV * BS2_TILE;                  // [8 warps][stride]
-    __shared__ bool s_last;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* acc = sacc + warp * stride;
-    for (int i = lane; i < stride; i += 32) acc[i] = 0.0;
-    const int64_t ntiles = (n + BS2_TILE - 1) / BS2_TILE;
-    const int ngroups = (ncols + 7) / 8;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t t0 = tile * BS2_TILE;
-        __syncthreads();
-        for (int i = threadIdx.x; i < BS2_TILE; i += blockDim.x) {
-            const int64_t r = t0 + i;
-            suz[i] = r < n ? __ldg(u + r) : 0.0;
-            if (NV == 2) suz[BS2_TILE + i] = r < n ? __ldg(z + r) : 0.0;
-        }
-        __syncthreads();
-        const int64_t w0 = t0 + warp * BS2_ROWS_W;     // this warp's 512 rows
-        const bool fullw = w0 + BS2_ROWS_W <= n;
-        const double* us = suz + warp * BS2_ROWS_W;
-        const double* zs = suz + BS2_TILE + warp * BS2_ROWS_W;
-        for (int g = 0; g < ngroups; g++) {
-            const double* cp[8];
-#pragma unroll
-            for (int c = 0; c < 8; c++) {
-                const int j = min(g * 8 + c, ncols - 1);
-                cp[c] = (j < p) ? V + (int64_t)j * ld : u;
-            }
-            double au[8], az[8];
-#pragma unroll
-            for (int c = 0; c < 8; c++) { au[c] = 0.0; az[c] = 0.0; }
-#pragma unroll 2
-            for (int ch = 0; ch < BS2_CHUNKS; ch++) {
-                const int64_t r = w0 + ch * 64 + 2 * lane;
-                double2 v[8];
-#pragma unroll
-                for (int c = 0; c < 8; c++) v[c] = fullw ? __ldg(reinterpret_cast<const double2*>(cp[c] + r)) : ld2_guard(cp[c], r, n);
-                const double2 uu = *reinterpret_cast<const double2*>(us + ch * 64 + 2 * lane);
-                double2 zz = make_double2(0.0, 0.0);
-                if (NV == 2) zz = *reinterpret_cast<const double2*>(zs + ch * 64 + 2 * lane);
-#pragma unroll
-                for (int c = 0; c < 8; c++) {
-                    au[c] = fma(v[c].y, uu.y, fma(v[c].x, uu.x, au[c]));
-                    if (NV == 2) az[c] = fma(v[c].y, zz.y, fma(v[c].x, zz.x, az[c]));
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 8; c++)
-                if (g * 8 + c >= ncols) { au[c] = 0.0; az[c] = 0.0; }
-            const double su = bfly8(au, lane);
-            double sz = 0.0;
-            if (NV == 2) sz = bfly8(az, lane);
-            const int j = g * 8 + (lane >> 2);
-            if ((lane & 3) == 0 && j < ncols) {
-                acc[j] += su;
-                if (NV == 2) acc[ncols + j] += sz;
-            }
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < stride; i += blockDim.x) {
-        double sacc2 = 0.0;
-#pragma unroll
-        for (int w = 0; w < BS2_WARPS; w++) sacc2 += sacc[w * stride + i];
-        part[(int64_t)blockIdx.x * stride + i] = sacc2;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    final_reduce(part, stride, (int)gridDim.x, out);  // [V_p^T u, u.u, V_p^T z, u.z]
-    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
+int bdot_grid_size(int64_t n, int num_sms) {
+    const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
+    int64_t g = (int64_t)num_sms * 2;  // also >= the bulk-copy kernel's grid (num_sms)
+    if (g > ntiles) g = ntiles;
+    if (g < 1) g = 1;
+    return (int)g;
 }
 
 static size_t bdot_tma_smem(int p, int nv) {
@@ -952,65 +707,13 @@ static size_t bdot_tma_smem(int p, int nv) {
 
 static size_t bdot_smem(int p, int nv) { return (size_t)BD_WARPS * nv * (p + 1) * sizeof(double); }
 
-int bdot_grid_size(int64_t n, int num_sms) {
-    const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
-    int64_t g = (int64_t)num_sms * 2;  // also >= the TMA kernel's grid (num_sms)
-    if (g > ntiles) g = ntiles;
-    if (g < 1) g = 1;
-    return (int)g;
-}
-
 void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                       const double* z, double* out, double* part, unsigned* counter, int grid,
-                      const int* istate, cudaStream_t s, const CUtensorMap* tmV, const XchgDev* xc) {
+                      const int* istate, cudaStream_t s, const XchgDev* xc) {
     const int nv = z ? 2 : 1;
-    if (xc) tmV = nullptr;  // the exchange is fused into the bulk-copy and register kernels only
-    // default: 2D TMA tensor copies of V (tmV: box 256 rows x 8 columns over V's columns)
-    const size_t msmem = bdot_tmap_smem(p, nv);
-    if (tmV && p > 0 && msmem <= 227 * 1024 && ((uintptr_t)u % 16) == 0 && (!z || ((uintptr_t)z % 16) == 0) &&
-        n >= TM_ROWS) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t ntiles = (n + TM_ROWS - 1) / TM_ROWS;
-        const int tg = (int)(ntiles < sms ? ntiles : sms);
-        if (tg <= grid) {
-            if (nv == 2) {
-                cudaFuncSetAttribute(bdot_tmap_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
-                bdot_tmap_kernel<2><<<tg, BT_THREADS, msmem, s>>>(*tmV, n, p, u, z, part, out, counter, istate);
-            } else {
-                cudaFuncSetAttribute(bdot_tmap_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
-                bdot_tmap_kernel<1><<<tg, BT_THREADS, msmem, s>>>(*tmV, n, p, u, z, part, out, counter, istate);
-            }
-            return;
-        }
-    }
     // sm_100a bulk-copy pipeline when V columns are 16-B aligned with an even ld and the
     // accumulators fit next to the 192 KB ring; the register kernel otherwise
     const size_t tsmem = bdot_tma_smem(p, nv);
-    static int variant = -1;  // IGS_BDOT=stream selects the register-streaming variant
-    if (variant < 0) {
-        const char* e = getenv("IGS_BDOT");
-        variant = (e && e[0] == 's') ? 1 : 0;
-    }
-    const size_t ssmem = (size_t)(nv * BS2_TILE + BS2_WARPS * nv * (p + 1)) * sizeof(double);
-    if (!xc && variant == 1 && p > 0 && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 && ((uintptr_t)u % 16) == 0 &&
-        ssmem <= 113 * 1024) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t ntiles = (n + BS2_TILE - 1) / BS2_TILE;
-        int g = (int)(ntiles < 2 * sms ? ntiles : 2 * sms);
-        if (g > grid) g = grid;
-        if (nv == 2) {
-            cudaFuncSetAttribute(bdot_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
-            bdot_stream_kernel<2><<<g, BS2_WARPS * 32, ssmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
-        } else {
-            cudaFuncSetAttribute(bdot_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
-            bdot_stream_kernel<1><<<g, BS2_WARPS * 32, ssmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate);
-        }
-        return;
-    }
     if (p > 0 && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 && tsmem <= 227 * 1024 && n >= BT_ROWS) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -1139,11 +842,13 @@ __global__ void __launch_bounds__(UD_THREADS)
                       unsigned* counter, const XchgDev* xc) {
     extern __shared__ double sdyn[];  // alpha[p] | beta[p+1] | acc[UD_WARPS][p+2]
     __shared__ bool s_last;
+    bool live = true;
     if (istate) {
         const volatile int* vs = istate;
         const int mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
-        if ((mode & 3) != 3) return;  // the second sweep runs only after a full update
+        live = (mode & 3) == 3;  // the second sweep runs only after a full update
     }
+    if (!live && !xc) return;  // with the exchange every rank joins it (bdot_kernel)
     const int nd = p + 2;
     double* sa = sdyn;
     double* sb = sdyn + p;
@@ -1155,7 +860,7 @@ __global__ void __launch_bounds__(UD_THREADS)
     for (int j = lane; j < nd; j += 32) acc[j] = 0.0;
     __syncthreads();
     const double gamma = *gamma_dev;
-    const int64_t ntiles = (n + UD_TILE - 1) / UD_TILE;
+    const int64_t ntiles = live ? (n + UD_TILE - 1) / UD_TILE : 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t r = tile * UD_TILE + 2 * threadIdx.x;
         const bool in = r < n, pair = r + 1 < n;
@@ -1231,7 +936,7 @@ __global__ void __launch_bounds__(UD_THREADS)
     __threadfence();
     if (xc) final_reduce_xchg(part, nd, (int)gridDim.x, out, *xc);
     else final_reduce(part, nd, (int)gridDim.x, out);
-    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += live ? 1u : 0u; }
 }
 
 // The same fused update + second-sweep dot with the V_p tile resident in shared memory:
@@ -1264,11 +969,13 @@ __global__ void __launch_bounds__(UT_THREADS, 1)
                           unsigned* counter, const XchgDev* xc) {
     extern __shared__ __align__(16) double usm[];
     __shared__ bool s_last;
+    bool live = true;
     if (istate) {
         const volatile int* vs = istate;
         const int mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
-        if ((mode & 3) != 3) return;
+        live = (mode & 3) == 3;
     }
+    if (!live && !xc) return;  // with the exchange every rank joins it (bdot_kernel)
     const int nd = p + 2, tcols = p + 2;  // tile columns: V_p | u | z
     double* buf = usm;                                // [2][tcols][R]
     double* sa = buf + (size_t)2 * tcols * R;         // [p]
@@ -1290,7 +997,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1)
     __syncthreads();
     const double gamma = *gamma_dev;
     const int64_t ntiles = (n + R - 1) / R;
-    const int64_t nk = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const int64_t nk = (live && blockIdx.x < ntiles) ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     if (warp == UT_CONS) {
         // ---------------- producer warp: one bulk copy per column (and u, z) and tile ----------
         for (int64_t k = 0; k < nk; k++) {
@@ -1381,7 +1088,7 @@ __global__ void __launch_bounds__(UT_THREADS, 1)
     __threadfence();
     if (xc) final_reduce_xchg(part, nd, (int)gridDim.x, out, *xc);
     else final_reduce(part, nd, (int)gridDim.x, out);
-    if (tid == 0) { *counter = 0u; counter[1] += 1u; }
+    if (tid == 0) { *counter = 0u; counter[1] += live ? 1u : 0u; }
 }
 
 void launch_update_dot_tma(int64_t n, int p, const double* V, int64_t ld, const double* u, const double* z,
@@ -1403,12 +1110,7 @@ void launch_update_dot_tma(int64_t n, int p, const double* V, int64_t ld, const 
 
 int update_dot_grid(int64_t n, int num_sms) {
     const int64_t ntiles = (n + UD_TILE - 1) / UD_TILE;
-    static int mult = -1;  // CTAs per SM (IGS_UD_CTAS, default 4)
-    if (mult < 0) {
-        const char* e = getenv("IGS_UD_CTAS");
-        mult = e ? atoi(e) : 4;
-        if (mult < 1) mult = 1;
-    }
+    const int mult = 4;  // CTAs per SM
     int64_t g = (int64_t)num_sms * mult;
     if (g > ntiles) g = ntiles;
     return (int)(g < 1 ? 1 : g);
@@ -1432,152 +1134,10 @@ void launch_update_dot(int64_t n, int p, const double* V, int64_t ld, const doub
     }
 }
 
-// ------------------------------------------------------------------------------------
-// K5 (sm_100a pipeline): the same fused update with V_p streamed by the bulk-copy engine,
-// as in bdot_tma_kernel: persistent CTA per SM = 8 consumer warps + 1 producer warp, 512-row
-// tiles, 8 columns x 512 rows per stage, 6-stage ring.  Consumer warp w owns rows
-// 64w + 2l, 64w + 2l + 1 of the tile (one 16-B shared load per column) and accumulates
-// t1 = V alpha, t2 = V beta over the columns in ascending order -- the same FMA sequence as
-// update_kernel, so the results are bitwise identical; no cross-lane reduction exists.  u
-// and z of the tile are fetched into registers when the tile starts and used in the
-// epilogue.  Opt-in (IGS_UPDATE_TMA=1): in the c4 bench it streams 6.5 TB/s against the
-// register kernel's 6.9 TB/s.
-// ------------------------------------------------------------------------------------
-template <bool HAS_ALPHA>
-__global__ void __launch_bounds__(BT_THREADS, 1)
-    update_tma_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
-                      const double* u, const double* __restrict__ z,
-                      const double* __restrict__ alpha, const double* __restrict__ beta,
-                      const double* __restrict__ gamma_dev, double* v_out, double* u_next,
-                      const int* istate, int it, int default_mode, const double* __restrict__ zdiv_dev) {
-    int mode = default_mode;
-    if (istate) {
-        const volatile int* vs = istate;
-        mode = (vs[ST_MODE_IT] == it) ? vs[ST_MODE] : 0;
-        mode &= default_mode;
-    }
-    if (mode == 0) return;
-    const bool want_next = (mode & 2) != 0;
-    extern __shared__ __align__(128) double smem_ut[];
-    double* ring = smem_ut;                                  // [STAGES][8][512]
-    double* sa = ring + BT_STAGES * BT_STAGE_DOUBLES;        // alpha [p]
-    double* sb = sa + ((p + 1) & ~1);                        // beta [p+1]
-    uint64_t* full = reinterpret_cast<uint64_t*>(sb + ((p + 2) & ~1));
-    uint64_t* empty = full + BT_STAGES;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (HAS_ALPHA)
-        for (int j = threadIdx.x; j < p; j += blockDim.x) sa[j] = alpha[j];
-    if (want_next)
-        for (int j = threadIdx.x; j <= p; j += blockDim.x) sb[j] = beta[j];
-    if (threadIdx.x == 0) {
-        for (int st = 0; st < BT_STAGES; st++) { mbar_init(full + st, 1); mbar_init(empty + st, BT_CONS_WARPS); }
-        mbar_fence_init();
-    }
-    __syncthreads();
-    const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
-    const int ngroups = (p + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
-    const int64_t nk = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    if (warp == BT_CONS_WARPS) {
-        if (lane == 0) {
-            uint32_t itg = 0;
-            for (int64_t k = 0; k < nk; k++) {
-                const int64_t row0 = (blockIdx.x + k * gridDim.x) * BT_ROWS;
-                const int64_t rows = (n - row0 < BT_ROWS) ? n - row0 : BT_ROWS;
-                const uint32_t bytes = (uint32_t)(((rows + 1) & ~1LL) * sizeof(double));
-                for (int g = 0; g < ngroups; g++, itg++) {
-                    const int st = itg % BT_STAGES;
-                    mbar_wait(empty + st, ((itg / BT_STAGES) & 1) ^ 1);
-                    const int c0 = g * BT_CONS_WARPS;
-                    const int nc = min(BT_CONS_WARPS, p - c0);
-                    mbar_arrive_expect_tx(full + st, (uint32_t)nc * bytes);
-                    for (int c = 0; c < nc; c++)
-                        bulk_g2s(ring + (size_t)st * BT_STAGE_DOUBLES + c * BT_ROWS,
-                                 V + (int64_t)(c0 + c) * ld + row0, bytes, full + st);
-                }
-            }
-        }
-        return;
-    }
-    const double gamma = *gamma_dev;
-    const double zdiv = zdiv_dev ? *zdiv_dev : gamma;
-    const int rl = 64 * warp + 2 * lane;  // this lane's two rows within the tile
-    uint32_t itg = 0;
-    for (int64_t kt = 0; kt < nk; kt++) {
-        const int64_t row0 = (blockIdx.x + kt * gridDim.x) * BT_ROWS;
-        const int64_t r = row0 + rl;
-        const bool pair = r + 1 < n;
-        // epilogue operands, in flight while the tile streams
-        const double2 uu = ld2_guard(u, r, n);
-        const double2 zz = want_next ? ld2_guard(z, r, n) : make_double2(0.0, 0.0);
-        double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
-        for (int g = 0; g < ngroups; g++, itg++) {
-            const int st = itg % BT_STAGES;
-            mbar_wait(full + st, (itg / BT_STAGES) & 1);
-            const int c0 = g * BT_CONS_WARPS;
-            const int nc = min(BT_CONS_WARPS, p - c0);
-            const double* stg = ring + (size_t)st * BT_STAGE_DOUBLES + rl;
-#pragma unroll
-            for (int c = 0; c < BT_CONS_WARPS; c++) {
-                if (c < nc) {
-                    const double2 v = *reinterpret_cast<const double2*>(stg + c * BT_ROWS);
-                    if (HAS_ALPHA) { t1.x = fma(v.x, sa[c0 + c], t1.x); t1.y = fma(v.y, sa[c0 + c], t1.y); }
-                    if (want_next) { t2.x = fma(v.x, sb[c0 + c], t2.x); t2.y = fma(v.y, sb[c0 + c], t2.y); }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + st);
-        }
-        if (r < n) {
-            double2 w = uu;
-            if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
-            double2 v;
-            v.x = w.x / gamma;
-            v.y = w.y / gamma;
-            if (want_next) {
-                const double bp = sb[p];
-                u_next[r] = zz.x / zdiv - fma(v.x, bp, t2.x);
-                if (pair) u_next[r + 1] = zz.y / zdiv - fma(v.y, bp, t2.y);
-            }
-            if (mode & 1) {
-                v_out[r] = v.x;
-                if (pair) v_out[r + 1] = v.y;
-            }
-        }
-    }
-}
-
-static size_t update_tma_smem(int p) {
-    return (size_t)(BT_STAGES * BT_STAGE_DOUBLES + ((p + 1) & ~1) + ((p + 2) & ~1)) * sizeof(double) +
-           2 * BT_STAGES * sizeof(uint64_t);
-}
-
 void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
                    const double* z, const double* alpha, const double* beta,
                    const double* gamma_dev, double* v_out, double* u_next, const int* istate,
                    int it, cudaStream_t s, const double* zdiv_dev) {
-    static int tma = -1;  // IGS_UPDATE_TMA=1: bulk-copy variant (measured slower in the bench:
-    if (tma < 0) {        // 113 vs 106 ms per c4 step)
-        const char* e = getenv("IGS_UPDATE_TMA");
-        tma = (e && atoi(e) == 1) ? 1 : 0;
-    }
-    const size_t usmem = update_tma_smem(p);
-    if (tma && p >= BT_CONS_WARPS && n >= BT_ROWS && (ld % 2) == 0 && ((uintptr_t)V % 16) == 0 &&
-        ((uintptr_t)u % 16) == 0 && (!z || ((uintptr_t)z % 16) == 0) && usmem <= 227 * 1024) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
-        const int tg = (int)(ntiles < sms ? ntiles : sms);
-        const int dmode = 1 | (u_next ? 2 : 0);
-        if (alpha) {
-            cudaFuncSetAttribute(update_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
-            update_tma_kernel<true><<<tg, BT_THREADS, usmem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
-        } else {
-            cudaFuncSetAttribute(update_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
-            update_tma_kernel<false><<<tg, BT_THREADS, usmem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
-        }
-        return;
-    }
     const int64_t nthreads = (n + 1) / 2;
     const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
     if (blocks == 0) return;
@@ -2310,16 +1870,23 @@ void launch_gram(int64_t n, int c, const double* V, int64_t ld, double* part, in
     gram_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c, splits, part, G);
 }
 
+// out[0] = ||I - G||_F; out[1] = ||tril(G, -1)||_F, the paper's L_k of the
+// computed basis (strictly lower part of V^T V; dep^2(I + L_k) = ||L_k||_F^2,
+// P:1216-1223).  gram_reduce_kernel mirrors one computed triangle, so G is exactly
+// symmetric and either triangle gives the same norm.
 __global__ void loo_norm_kernel(int c, const double* __restrict__ G, double* out) {
     __shared__ double red[40];
-    double part = 0.0;
+    double part = 0.0, low = 0.0;
     for (int64_t e = threadIdx.x; e < (int64_t)c * c; e += blockDim.x) {
         const int i = (int)(e / c), j = (int)(e % c);
         const double d = (i == j ? 1.0 : 0.0) - G[e];
         part += d * d;
+        if (j > i) low += G[e] * G[e];
     }
     const double s = block_sum(part, red);
-    if (threadIdx.x == 0) *out = sqrt(s);
+    __syncthreads();
+    const double l = block_sum(low, red);
+    if (threadIdx.x == 0) { out[0] = sqrt(s); out[1] = sqrt(l); }
 }
 
 void launch_loo_norm(int c, const double* G, double* out, cudaStream_t s) {
@@ -2359,13 +1926,14 @@ __global__ void __launch_bounds__(MS_THREADS)
                     const double* __restrict__ vn, const double* hsrc, double* Hdst,
                     double* __restrict__ part, double* out, unsigned* counter, const int* istate,
                     const XchgDev* xc) {
-    if (!running(istate)) return;
+    const bool live = running(istate);  // stopped: with the exchange, join it without work
+    if (!live && !xc) return;
     __shared__ double red[40];
     __shared__ bool s_last;
-    const double h = AXPY ? __ldcg(hsrc) : 0.0;
-    if (AXPY && blockIdx.x == 0 && threadIdx.x == 0) *Hdst = h;
+    const double h = AXPY && live ? __ldcg(hsrc) : 0.0;
+    if (AXPY && live && blockIdx.x == 0 && threadIdx.x == 0) *Hdst = h;
     double acc = 0.0;
-    const int64_t nfull = n / MS_CHUNK;
+    const int64_t nfull = live ? n / MS_CHUNK : 0;
     for (int64_t c = blockIdx.x; c < nfull; c += gridDim.x) {
         const int64_t r0 = c * MS_CHUNK + 2 * threadIdx.x, r1 = r0 + 2 * MS_THREADS;
         double2 w0 = __ldcg(reinterpret_cast<const double2*>(z + r0));
@@ -2392,7 +1960,7 @@ __global__ void __launch_bounds__(MS_THREADS)
         acc = fma(q1.y, w1.y, acc);
     }
     // ragged tail (< MS_CHUNK rows): the last CTA of the chunk loop's next round, one row per thread
-    if ((int64_t)blockIdx.x == nfull % gridDim.x) {
+    if (live && (int64_t)blockIdx.x == nfull % gridDim.x) {
         for (int64_t r = nfull * MS_CHUNK + threadIdx.x; r < n; r += MS_THREADS) {
             double w = z[r];
             if (AXPY) {
@@ -2421,7 +1989,7 @@ __global__ void __launch_bounds__(MS_THREADS)
     } else if (threadIdx.x == 0) {
         *out = t;
     }
-    if (threadIdx.x == 0) { *counter = 0u; counter[1] += 1u; }
+    if (threadIdx.x == 0) { *counter = 0u; counter[1] += live ? 1u : 0u; }
 }
 
 int mgs_step_grid(int64_t n, int num_sms) {

@@ -28,7 +28,8 @@ EXPORTS = ["igs_create", "igs_nccl_unique_id", "igs_workspace_bytes", "igs_bind_
            "igs_solve", "igs_solve_alg", "igs_stats", "igs_set_timing", "igs_kernel_stats", "igs_destroy",
            "igs_last_error", "igs_op_block_dot", "igs_op_spmv", "igs_op_update",
            "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap", "igs_qr",
-           "igs_op_basis_diag"]
+           "igs_op_basis_diag", "igs_bench_block_dot", "igs_set_timeout", "igs_create_virtual",
+           "igs_virtual_spmv", "igs_info"]
 
 
 class IgsError(RuntimeError):
@@ -44,7 +45,7 @@ class igs_result(ctypes.Structure):
                 ("h_cols", ctypes.c_int), ("basis_cols", ctypes.c_int), ("allreduces", ctypes.c_int64),
                 ("reductions", ctypes.c_int64), ("lnorm_hist", ctypes.c_void_p),
                 ("want_basis_diag", ctypes.c_int), ("s_norm", ctypes.c_double),
-                ("sigma_min", ctypes.c_double)]
+                ("sigma_min", ctypes.c_double), ("lgram_frob", ctypes.c_double)]
 
 
 _lib = None
@@ -67,11 +68,16 @@ def lib() -> ctypes.CDLL:
             "igs_solve_alg": [P, I, P, P, I, I, D, I, ctypes.POINTER(igs_result)],
             "igs_stats": [P, P, P, P],
             "igs_set_timing": [P, I],
+            "igs_set_timeout": [P, D],
+            "igs_info": [P, I, P],
+            "igs_create_virtual": [P, I, I64, P, P, P, I, P, I, P],
+            "igs_virtual_spmv": [P, I, P, P, P],
             "igs_kernel_stats": [P, I, P, P, P],
             "igs_destroy": [P],
             "igs_last_error": [],
             "igs_op_block_dot": [I64, I, P, I64, P, P, P, P],
             "igs_op_spmv": [P, P, P],
+            "igs_bench_block_dot": [I64, I, P, I64, P, P, P, I, P, P],
             "igs_op_update": [I64, I, P, I64, P, P, P, P, D, P, P, P],
             "igs_op_trisolve": [I, P, I, P, P, P],
             "igs_qr": [I64, I, P, I64, P, I64, P, I, P, P],
@@ -183,6 +189,14 @@ def igs_op_block_dot(n, p, V, ld, u, z, out, stream=None):
                                   _stream_ptr(stream)), "igs_op_block_dot")
 
 
+def igs_bench_block_dot(n, p, V, ld, u, z, out, reps=10, stream=None) -> float:
+    """Mean milliseconds per block-dot launch over `reps` back-to-back launches (CUDA events)."""
+    ms = ctypes.c_float(0.0)
+    _check(lib().igs_bench_block_dot(int(n), int(p), _ptr(V), int(ld), _ptr(u), _ptr(z), _ptr(out), int(reps),
+                                     ctypes.byref(ms), _stream_ptr(stream)), "igs_bench_block_dot")
+    return ms.value
+
+
 def igs_op_spmv(ctx: int, x, y):
     _check(lib().igs_op_spmv(ctx, _ptr(x), _ptr(y)), "igs_op_spmv")
 
@@ -243,6 +257,68 @@ def igs_plan_remap(row_begin, n_local, rowptr, colind, ghosts):
 
 
 # ------------------------------------------------------------------------- convenience
+INFO_KEYS = ["xchg", "nranks", "n_ghost", "n_send", "n_peers", "n_bnd", "graph_launches", "pcycle_launches",
+             "sell", "csr_compact"]
+
+
+def igs_info(ctx: int) -> dict:
+    out = {}
+    for i, k in enumerate(INFO_KEYS):
+        v = ctypes.c_int64(0)
+        _check(lib().igs_info(ctx, i, ctypes.byref(v)), "igs_info")
+        out[k] = v.value
+    return out
+
+
+def igs_set_timeout(ctx: int, seconds: float):
+    _check(lib().igs_set_timeout(ctx, float(seconds)), "igs_set_timeout")
+
+
+class VirtualGroup:
+    """G virtual-rank contexts of one global CSR on one device (igs_create_virtual): the
+    G > 1 halo path of the SpMV (pack kernel, ghost copies, interior/boundary split) on a
+    single GPU.  Test hook; `spmv(xs, ys[, bs])` takes per-rank device tensors."""
+
+    def __init__(self, csr, bounds, *, device: int = 0, stream=None):
+        import torch
+        torch.cuda.set_device(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        self.bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+        self.G = len(self.bounds) - 1
+        rowptr = np.ascontiguousarray(csr.rowptr, dtype=np.int64)
+        colind = np.ascontiguousarray(csr.colind)
+        values = np.ascontiguousarray(csr.values, dtype=np.float64)
+        bits = 64 if colind.dtype.itemsize == 8 else 32
+        arr = (ctypes.c_void_p * self.G)()
+        _check(lib().igs_create_virtual(arr, self.G, int(csr.n_cols), self.bounds.ctypes.data, rowptr.ctypes.data,
+                                        colind.ctypes.data, bits, values.ctypes.data, int(device),
+                                        _stream_ptr(self.stream)), "igs_create_virtual")
+        self.ctxs = [arr[i] for i in range(self.G)]
+        self._arr = arr
+
+    def spmv(self, xs, ys, bs=None):
+        G = self.G
+        px = (ctypes.c_void_p * G)(*[_ptr(t) for t in xs])
+        py = (ctypes.c_void_p * G)(*[_ptr(t) for t in ys])
+        pb = (ctypes.c_void_p * G)(*[_ptr(t) for t in bs]) if bs is not None else None
+        _check(lib().igs_virtual_spmv(self._arr, G, px, py, pb), "igs_virtual_spmv")
+
+    def stats(self) -> list:
+        return [igs_stats(c) for c in self.ctxs]
+
+    def close(self):
+        for c in getattr(self, "ctxs", []) or []:
+            if c:
+                igs_destroy(c)
+        self.ctxs = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Solver:
     """One rank's IGS-GMRES solver: `Solver(csr, ...)` then `.solve(b, k=..., ...)`.
 
@@ -311,7 +387,7 @@ class Solver:
                    true_relres=res.true_relres, loo=res.loo_frob, h_cols=res.h_cols,
                    basis_cols=res.basis_cols, allreduces=res.allreduces, reductions=res.reductions,
                    res_hist=rh[:res.iters + 1], lnorm_hist=lh[:res.iters + 1], m=m1,
-                   s_norm=res.s_norm, sigma_min=res.sigma_min)
+                   s_norm=res.s_norm, sigma_min=res.sigma_min, lgram=res.lgram_frob)
         if want_H:
             out["H"] = H.reshape(m1, m1 + 1).T
         return out
@@ -321,6 +397,12 @@ class Solver:
 
     def set_timing(self, on: int):
         igs_set_timing(self.ctx, on)
+
+    def set_timeout(self, seconds: float):
+        igs_set_timeout(self.ctx, seconds)
+
+    def info(self) -> dict:
+        return igs_info(self.ctx)
 
     def kernel_stats(self) -> dict:
         return igs_kernel_stats(self.ctx)

@@ -262,19 +262,3 @@ def test_basis_diag_vs_oracle(torch_cuda, case):
     if case == "repeated":
         assert abs(s2 - 1.0) <= 1e-10 and smin <= 1e-7
 
-
-def test_update_bulk_copy_kernel_bitwise_equals_register_kernel(torch_cuda):
-    """update_tma_kernel (V_p streamed by the bulk-copy engine) keeps update_kernel's FMA
-    order, so both must give the same bits (incl. ragged tails and p not a multiple of 8)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    outs = {}
-    for v in ("0", "1"):
-        env = dict(os.environ, IGS_UPDATE_TMA=v)
-        r = subprocess.run([sys.executable, os.path.join(root, "tools", "update_variants.py")], env=env,
-                           capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-2000:]
-        outs[v] = r.stdout.strip().splitlines()[-1]
-    assert outs["0"] == outs["1"]
