@@ -46,7 +46,7 @@ UNIT = "Arnoldi iterations/s"
 N_GRID = 256
 M = 100                     # GMRES(100)
 CPU_SAMPLE_ITERS = 50       # oracle sample: iterations 1..50 of the cycle (~12 s on 16 cores)
-CPU_SAMPLE_ITERS_1T = 4     # the same at one thread: iterations 1..4 (~15 s)
+CPU_SAMPLE_ITERS_1T = 12    # the same at one thread: iterations 1..12 (~8 s)
 NOMINAL_HBM_GBS = 8000.0    # north-star denominator (B200 HBM3e, nominal)
 
 

@@ -242,6 +242,12 @@ igs_status igs_op_block_dot(int64_t n, int p, const double* V, int64_t ld, const
 igs_status igs_bench_block_dot(int64_t n, int p, const double* V, int64_t ld, const double* u,
                                const double* z, double* out, int reps, float* ms, void* cuda_stream);
 
+/* Measurement hook for the fused update below (same arguments, gamma by value): one warm-up,
+ * then `reps` timed launches; *ms = mean milliseconds per launch.  Synchronises cuda_stream. */
+igs_status igs_bench_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                            const double* z, const double* alpha, const double* beta, double gamma,
+                            double* v_out, double* u_next, int reps, float* ms, void* cuda_stream);
+
 /* y = A x with the context's (local, nranks == 1) matrix: x, y device [n_local]. */
 igs_status igs_op_spmv(igs_ctx* ctx, const double* x, double* y);
 

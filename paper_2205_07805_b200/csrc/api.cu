@@ -1821,6 +1821,35 @@ extern "C" igs_status igs_bench_block_dot(int64_t n, int p, const double* V, int
     return IGS_OK;
 }
 
+// Measurement hook: `reps` back-to-back fused updates (Alg. 3 form when alpha != NULL).
+extern "C" igs_status igs_bench_update(int64_t n, int p, const double* V, int64_t ld, const double* u,
+                                       const double* z, const double* alpha, const double* beta, double gamma,
+                                       double* v_out, double* u_next, int reps, float* ms, void* cuda_stream) {
+    ARG_CHECK(n >= 1 && p >= 0 && u && v_out && ms && reps >= 1 && (p == 0 || V), "igs_bench_update: bad argument");
+    ARG_CHECK(!u_next || (z && beta), "igs_bench_update: u_next needs z and beta");
+    TRY(have_device());
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    double* dg = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    CUDA_TRY(cudaMalloc(&dg, sizeof(double)));
+    struct Free { double* g; cudaEvent_t a, b;
+                  ~Free() { cudaFree(g); if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); } } guard{dg, nullptr, nullptr};
+    CUDA_TRY(cudaEventCreate(&e0));
+    guard.a = e0;
+    CUDA_TRY(cudaEventCreate(&e1));
+    guard.b = e1;
+    CUDA_TRY(cudaMemcpyAsync(dg, &gamma, sizeof(double), cudaMemcpyHostToDevice, st));
+    launch_update(n, p, V, ld, u, z, alpha, beta, dg, v_out, u_next, nullptr, 0, st);
+    CUDA_TRY(cudaEventRecord(e0, st));
+    for (int r = 0; r < reps; r++) launch_update(n, p, V, ld, u, z, alpha, beta, dg, v_out, u_next, nullptr, 0, st);
+    CUDA_TRY(cudaEventRecord(e1, st));
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventSynchronize(e1));
+    CUDA_TRY(cudaEventElapsedTime(ms, e0, e1));
+    *ms /= (float)reps;
+    return IGS_OK;
+}
+
 // Algorithm 1: Q R = A with one or two Gauss-Seidel sweeps, on the solver's own
 // kernels (block dot, small step, fused update).  Reductions per column: 1 (+1 for sweeps=2).
 extern "C" igs_status igs_qr(int64_t n, int m, const double* A, int64_t lda, double* Q, int64_t ldq,

@@ -29,7 +29,7 @@ EXPORTS = ["igs_create", "igs_nccl_unique_id", "igs_workspace_bytes", "igs_bind_
            "igs_last_error", "igs_op_block_dot", "igs_op_spmv", "igs_op_update",
            "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap", "igs_qr",
            "igs_op_basis_diag", "igs_bench_block_dot", "igs_set_timeout", "igs_create_virtual",
-           "igs_virtual_spmv", "igs_info"]
+           "igs_virtual_spmv", "igs_info", "igs_bench_update"]
 
 
 class IgsError(RuntimeError):
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
             "igs_op_block_dot": [I64, I, P, I64, P, P, P, P],
             "igs_op_spmv": [P, P, P],
             "igs_bench_block_dot": [I64, I, P, I64, P, P, P, I, P, P],
+            "igs_bench_update": [I64, I, P, I64, P, P, P, P, D, P, P, I, P, P],
             "igs_op_update": [I64, I, P, I64, P, P, P, P, D, P, P, P],
             "igs_op_trisolve": [I, P, I, P, P, P],
             "igs_qr": [I64, I, P, I64, P, I64, P, I, P, P],
@@ -194,6 +195,15 @@ def igs_bench_block_dot(n, p, V, ld, u, z, out, reps=10, stream=None) -> float:
     ms = ctypes.c_float(0.0)
     _check(lib().igs_bench_block_dot(int(n), int(p), _ptr(V), int(ld), _ptr(u), _ptr(z), _ptr(out), int(reps),
                                      ctypes.byref(ms), _stream_ptr(stream)), "igs_bench_block_dot")
+    return ms.value
+
+
+def igs_bench_update(n, p, V, ld, u, z, alpha, beta, gamma, v_out, u_next, reps=10, stream=None) -> float:
+    """Mean milliseconds per fused-update launch over `reps` back-to-back launches."""
+    ms = ctypes.c_float(0.0)
+    _check(lib().igs_bench_update(int(n), int(p), _ptr(V), int(ld), _ptr(u), _ptr(z), _ptr(alpha), _ptr(beta),
+                                  float(gamma), _ptr(v_out), _ptr(u_next), int(reps), ctypes.byref(ms),
+                                  _stream_ptr(stream)), "igs_bench_update")
     return ms.value
 
 

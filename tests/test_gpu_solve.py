@@ -247,6 +247,63 @@ def test_c4_full_size_first_columns(P, gs):
     np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-8)
 
 
+def _golden(name):
+    import json, os
+    with open(os.path.join(os.path.dirname(__file__), "golden", name)) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+def test_c4_as_specified_vs_oracle_record(P, gs):
+    """BASELINE configs[3] exactly as specified -- 256^3, GMRES(100) to a true relative
+    residual of 1e-12 -- in bench.py's launch configuration, against the oracle's run of the
+    same problem (tests/golden/oracle_c4_gs*.json, written by tools/oracle_records.py, which
+    calls only oracle/): iterations and cycles, termination, the Givens residual history
+    (P:1551-1553), and the backward error beta(x) with the oracle's ||A||_2."""
+    import torch
+    gold = _golden(f"oracle_c4_gs{gs}.json")
+    prob = W.config("c4")
+    s = P.Solver(prob.A)
+    g = s.solve(torch.from_numpy(prob.b).cuda(), k=3000, restart=100, tol=1e-12, gs_iters=gs, want_H=False)
+    s.close()
+    assert g["term"] == gold["term"] == "converged"
+    # the reduction order moves the residual at the 1e-12 crossing by a few ulps; the
+    # crossing iteration itself may move by one (none observed)
+    assert abs(g["iters"] - gold["iters"]) <= 1 and g["cycles"] == gold["cycles"], (g["iters"], gold["iters"])
+    assert g["true_relres"] <= 1e-12
+    ro = np.asarray(gold["res_hist"])
+    m = min(len(ro), len(g["res_hist"]))
+    # the residual history drifts by reordering noise times the growth of kappa over 14
+    # restarts (round 1: 2.5e-4 relative at worst near 1e-12): 1e-3 relative
+    np.testing.assert_allclose(g["res_hist"][:m], ro[:m], rtol=1e-3)
+    bg = _beta(prob, g["x"].cpu().numpy(), gold["normA_2"])
+    assert bg <= 1e-14 or gold["beta"] / 10 <= bg <= 10 * gold["beta"], (bg, gold["beta"])
+
+
+def test_c5_k100_vs_oracle_record(P):
+    """BASELINE configs[4] as specified on one GPU (512^3, n = 134M, int64 columns, k = 100
+    unrestarted, V = 108 GB in HBM) against the oracle's run on the same inputs
+    (tests/golden/oracle_c5_gs2.json, tools/oracle_records.py): the three north-star bars --
+    H column-normwise over the first 30 columns (R9), beta within 10x and
+    ||I - V^T V||_F within 10x."""
+    import torch
+    gold = _golden("oracle_c5_gs2.json")
+    prob = W.config("c5")
+    s = P.Solver(prob.A)
+    g = s.solve(torch.from_numpy(prob.b).cuda(), k=100, restart=0, tol=0.0, gs_iters=2, want_loo=True)
+    s.close()
+    assert g["iters"] == gold["iters"] == 100
+    Ho = np.zeros((31, 30))
+    for j, col in enumerate(gold["H_first30"]):
+        Ho[:, j] = col
+    d, _ = _compare_cols(g["H"][:31, :30], Ho, np.asarray(gold["res_hist"]), ncols=30)
+    assert d <= 1e-10, d
+    np.testing.assert_allclose(g["res_hist"], gold["res_hist"], rtol=1e-8)
+    bg = _beta(prob, g["x"].cpu().numpy(), gold["normA_2"])
+    assert bg <= 1e-14 or gold["beta"] / 10 <= bg <= 10 * gold["beta"], (bg, gold["beta"])
+    assert _loo_close(g["loo"], gold["loo"]), (g["loo"], gold["loo"])
+
+
 def test_c5_full_size_int64_first_columns(P):
     """BASELINE config c5 (512^3, n = 134M, nnz = 938M, int64 column indices) on one GPU:
     the int64 CSR path at full size, first 6 Hessenberg columns against the oracle."""
@@ -774,6 +831,40 @@ def test_persistent_two_forward_substitution_ctas(P, grid, case, monkeypatch):
     assert a["true_relres"] <= max(10 * pk["true_relres"], 1e-14)
 
 
+@pytest.mark.parametrize("gs", [1, 2])
+@pytest.mark.parametrize("N,m", [(420, 100), (434, 300)])
+def test_persistent_default_threshold_upper_range(P, N, m, gs, monkeypatch):
+    """The persistent cycle kernel is the default up to the measured crossover with the graph
+    path; this checks the upper end of that range with the DEFAULT threshold (no override):
+    c3-shaped stencils with n = 176,400 and 188,356 rows, cycles of 100 and 300 columns (the
+    long-cycle machinery), both sweeps: the path taken is the one the threshold says, the
+    result matches the oracle at the parity bars and the per-kernel path, bitwise
+    reproducible."""
+    import torch
+    for key in ("IGS_PC_MAX_N", "IGS_PERSIST", "IGS_PC_GRID", "IGS_PC_NTRI"):
+        monkeypatch.delenv(key, raising=False)
+    prob = W.config("c3", N=N)
+    b = torch.from_numpy(prob.b).cuda()
+    s = P.Solver(prob.A)
+    g = [s.solve(b, k=m, gs_iters=gs) for _ in range(2)]
+    used_pc = s.info()["pcycle_launches"] > 0
+    s.close()
+    monkeypatch.setenv("IGS_PERSIST", "0")
+    s = P.Solver(prob.A)
+    pk = s.solve(b, k=m, gs_iters=gs)
+    assert s.info()["pcycle_launches"] == 0
+    s.close()
+    assert used_pc, prob.A.n_rows   # both sizes are inside the default persistent range
+    assert g[0]["H"].tobytes() == g[1]["H"].tobytes()
+    assert g[0]["iters"] == pk["iters"] == m
+    o = oracle.gmres(prob.A, prob.b, m, variant=VARIANT[gs], dot_block=4096)
+    d, c = _compare_cols(g[0]["H"], o["H"], o["res_hist"])
+    floor = oracle.column_normwise_diff(oracle.gmres(prob.A, prob.b, m, variant=VARIANT[gs], dot_block=8)["H"],
+                                        o["H"], c)
+    assert d <= max(1e-10, 2 * floor), (d, floor)
+    np.testing.assert_allclose(g[0]["res_hist"], o["res_hist"], rtol=1e-6)
+
+
 @pytest.mark.parametrize("cfg,N", [("c3", 300), ("c4", 47)])
 def test_two_reduce_fused_update_dot(P, cfg, N, monkeypatch):
     """Alg. 2 two-reduce: the first update fused with the second sweep's
@@ -855,7 +946,9 @@ def test_tiny_systems(P, n, alg, persist, monkeypatch):
     assert g["iters"] == o["iters"] and g["term"] == o["term"], (g["iters"], o["iters"], g["term"], o["term"])
     d, c = _compare_cols(g["H"], o["H"], o["res_hist"])
     # one sweep / MGS: the oracle's own H moves with the reduction order (eps kappa(B_k),
-    # reading R19) -- the bar is 10x that spread (blocks of 8 vs sequential dots)
-    floor = oracle.column_normwise_diff(oracle.gmres(A, b, k, variant=ALG_ORACLE[alg], dot_block=8)["H"], o["H"], c)
-    assert d <= max(1e-10, 10 * floor), (d, floor)
+    # reading R19) -- the bar is 2x that spread (SURVEY §8(c) "parity noise floor"), the
+    # spread taken over blocked orders 2, 8, 64 against the sequential dots
+    floor = max(oracle.column_normwise_diff(oracle.gmres(A, b, k, variant=ALG_ORACLE[alg], dot_block=blk)["H"],
+                                            o["H"], c) for blk in (2, 8, 64))
+    assert d <= max(1e-10, 2 * floor), (d, floor)
     np.testing.assert_allclose(g["res_hist"], o["res_hist"], rtol=1e-6, atol=1e-14)

@@ -206,3 +206,54 @@ def test_sigma_min_known_spectrum():
     V = (U * s) @ Wm.T
     assert abs(oracle.sigma_min(V, 7) - 1e-3) <= 1e-14
     assert abs(oracle.sigma_min(U, 7) - 1.0) <= 1e-14
+
+
+def test_backward_error_spec_example_x0():
+    """beta(0) = ||b|| / (||b|| + ||A|| * 0) = 1, whatever A, b and ||A||."""
+    ex = GOLD["spec_examples"]["backward_error_x0"]
+    A = W.config("c1").A
+    b = np.random.default_rng(3).standard_normal(A.n_rows)
+    for normA in (1.0, 3.7, 1e6):
+        assert oracle.backward_error(A, b, np.zeros(A.n_rows), normA) == ex["beta"]
+
+
+def test_backward_error_exact_solution_and_scaling():
+    """beta(x) = 0 for the exact solution of a system the oracle SpMV reproduces exactly
+    (integer data), and beta is invariant under b, x -> s b, s x (homogeneous of degree 0)."""
+    A = W.tridiag_csr(50, -1.0, 4.0, -2.0)
+    x = np.arange(1.0, 51.0)
+    b = oracle.spmv(A, x)
+    assert oracle.backward_error(A, b, x, 6.0) == 0.0
+    rng = np.random.default_rng(9)
+    xa = x + 1e-3 * rng.standard_normal(50)
+    b1 = oracle.backward_error(A, b, xa, 6.0)
+    b2 = oracle.backward_error(A, 8.0 * b, 8.0 * xa, 6.0)   # powers of 2: exact scaling
+    assert b1 > 0 and b1 == b2
+    # against the definition written out with a dense matrix (independent of oracle.spmv)
+    D = A.to_dense()
+    ref = np.linalg.norm(b - D @ xa) / (np.linalg.norm(b) + 6.0 * np.linalg.norm(xa))
+    assert abs(b1 - ref) <= 1e-12 * ref
+
+
+def test_column_normwise_diff_detects_differences():
+    """The parity metric every GPU test rests on (reading R9): zero for identical H, exactly
+    the perturbation relative to the column's max for one changed entry, blind to columns past
+    ncols, and it sees a sign flip, a transposed pair and a shifted column."""
+    rng = np.random.default_rng(4)
+    m = 12
+    H = np.triu(rng.standard_normal((m + 1, m)), -1)
+    assert oracle.column_normwise_diff(H, H.copy(), m) == 0.0
+    G = H.copy()
+    G[3, 5] += 1e-9
+    want = 1e-9 / np.max(np.abs(H[:7, 5]))
+    assert abs(oracle.column_normwise_diff(G, H, m) - want) <= 1e-6 * want
+    assert oracle.column_normwise_diff(G, H, 5) == 0.0        # column 5 not compared
+    S = H.copy(); S[2, 4] = -S[2, 4]                          # a dropped sign
+    assert oracle.column_normwise_diff(S, H, m) >= 2 * abs(H[2, 4]) / np.max(np.abs(H[:6, 4])) * (1 - 1e-12)
+    T = H.copy(); T[[1, 2], 6] = T[[2, 1], 6]                 # two entries swapped
+    assert oracle.column_normwise_diff(T, H, m) > 1e-3
+    Z = H.copy(); Z[:, 7] = np.roll(H[:, 7], 1)               # off by one row
+    assert oracle.column_normwise_diff(Z, H, m) > 1e-3
+    # entries below the subdiagonal are outside the metric (the Hessenberg structure)
+    B = H.copy(); B[10, 2] = 1.0
+    assert oracle.column_normwise_diff(B, H, m) == 0.0

@@ -1,9 +1,11 @@
 #!/usr/bin/env python3
-"""Block-dot bandwidth vs p and leading dimension (isolated launches, CUDA events).
+"""Block-dot and fused-update bandwidth vs p and leading dimension (isolated back-to-back
+launches, CUDA events; igs_bench_block_dot / igs_bench_update).
 
   python tools/bdot_probe.py [--n 1048576] [--ps 10,50,100,200,300] [--pads 0,32] [--reps 10]
 
-Algorithmic bytes per launch: 8 n p (V_p) + 16 n (u, z).  Prints one JSON line per case.
+Algorithmic bytes per launch: block dot 8 n p + 16 n (V_p, u, z); Alg. 3
+update 8 n p + 32 n (V_p, u, z read; v_p, u' written).  One JSON line per case.
 """
 import argparse
 import json
@@ -35,7 +37,13 @@ def main():
         for p in ps:
             ms = P.igs.igs_bench_block_dot(n, p, V, ld, u, z, out, reps=a.reps)
             by = 8.0 * n * p + 16.0 * n
-            print(json.dumps({"n": n, "ld": ld, "p": p, "us": ms * 1e3, "gbs": by / (ms / 1e3) / 1e9}), flush=True)
+            coef = torch.rand(p + 1, dtype=torch.float64, device="cuda") * 1e-3
+            vo = torch.empty(n, dtype=torch.float64, device="cuda")
+            un = torch.empty(n, dtype=torch.float64, device="cuda")
+            ms_u = P.igs.igs_bench_update(n, p, V, ld, u, z, coef, coef, 1.5, vo, un, reps=a.reps)
+            by_u = 8.0 * n * p + 32.0 * n
+            print(json.dumps({"n": n, "ld": ld, "p": p, "bdot_us": ms * 1e3, "bdot_gbs": by / (ms / 1e3) / 1e9,
+                              "update_us": ms_u * 1e3, "update_gbs": by_u / (ms_u / 1e3) / 1e9}), flush=True)
         del V
 
 
