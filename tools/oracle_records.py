@@ -65,7 +65,9 @@ def main():
         rec["loo"] = oracle.loss_of_orthogonality(o["V"][:, :c])
         rec["t_loo_s"] = time.time() - t1
         rec["H_first30"] = o["H"][:31, :30].T.tolist()  # column j = H[:31, j]
-    rec.update(t_generate_s=t_gen, t_norm_s=t_norm, t_solve_s=t_solve)
+    import resource
+    rec.update(t_generate_s=t_gen, t_norm_s=t_norm, t_solve_s=t_solve,
+               host_peak_rss_gb=resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6)
     out = a.out or os.path.join(ROOT, "tests", "golden", f"oracle_{a.config}_gs{a.gs}.json")
     with open(out, "w") as f:
         json.dump(rec, f)
