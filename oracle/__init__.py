@@ -222,10 +222,19 @@ def backward_error(A, b, x, normA: float) -> float:
     return float(np.linalg.norm(r) / (np.linalg.norm(b) + normA * np.linalg.norm(x)))
 
 
-def loss_of_orthogonality(V) -> float:
-    """||I - V^T V||_F."""
+def loss_of_orthogonality(V, row_block: int = 0) -> float:
+    """||I - V^T V||_F.  row_block > 0: V^T V summed over blocks of that many rows
+    (the same sum over rows, in blocks, so a 100-column basis of 134M rows -- c5, 108 GB --
+    needs no second copy of V)."""
     V = np.asarray(V)
-    return float(np.linalg.norm(np.eye(V.shape[1]) - V.T @ V, "fro"))
+    if row_block > 0:
+        G = np.zeros((V.shape[1], V.shape[1]))
+        for i in range(0, V.shape[0], row_block):
+            B = np.array(V[i:i + row_block])
+            G += B.T @ B
+    else:
+        G = V.T @ V
+    return float(np.linalg.norm(np.eye(V.shape[1]) - G, "fro"))
 
 
 def arnoldi_relation(A, V, H, p: int) -> float:

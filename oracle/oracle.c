@@ -489,7 +489,10 @@ int oracle_gmres(int64_t n, const int64_t* rowptr, const int64_t* colind, const 
     memset(&W, 0, sizeof W);
     W.n = n; W.rowptr = rowptr; W.colind = colind; W.val = val;
     W.m = m1; W.ldh = m1 + 1;
-    W.V = (double*)calloc((size_t)n * (m1 + 1), sizeof(double));
+    /* the basis lives in the caller's V_out when given (storage only: a 108 GB basis, c5,
+       is not held twice); zeroed like the calloc'd workspace */
+    if (V_out) { memset(V_out, 0, sizeof(double) * (size_t)n * (m1 + 1)); W.V = V_out; }
+    else W.V = (double*)calloc((size_t)n * (m1 + 1), sizeof(double));
     W.H = (double*)calloc((size_t)(m1 + 1) * m1, sizeof(double));
     W.HP = (double*)calloc((size_t)(m1 + 1) * m1, sizeof(double));
     W.L = (double*)calloc((size_t)m1 * m1, sizeof(double));
@@ -568,13 +571,13 @@ int oracle_gmres(int64_t n, const int64_t* rowptr, const int64_t* colind, const 
     /* r holds b - A x for the final x on every exit path */
     *true_relres = sqrt(dot(n, r, r)) / W.nb;
 done:
-    if (V_out) memcpy(V_out, W.V, sizeof(double) * (size_t)n * (m1 + 1));
     if (L_out) memcpy(L_out, W.L, sizeof(double) * (size_t)m1 * m1);
     if (info) {
         info[0] = total; info[1] = cycles; info[2] = term; info[3] = h_cols;
         info[4] = W.basis_cols; info[5] = W.priming_reductions; info[6] = OR_OK; info[7] = W.p_done;
     }
-    free(W.V); free(W.H); free(W.HP); free(W.L); free(W.z); free(W.t); free(W.u);
+    if (W.V != V_out) free(W.V);
+    free(W.H); free(W.HP); free(W.L); free(W.z); free(W.t); free(W.u);
     free(W.a); free(W.c); free(W.r1); free(W.r2); free(W.r3); free(W.tmp);
     free(W.G.R); free(W.G.cs); free(W.G.sn); free(W.G.g); free(y);
     return OR_OK;

@@ -12,6 +12,7 @@
 //                        V_p (the paper's "merge ... into one GPU kernel")
 //   xupdate_kernel       x += V_p y
 //   gram/loo kernels     ||I - V^T V||_F diagnostic
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -498,6 +499,10 @@ constexpr int BT_RPL = BT_ROWS / 32;  // rows per lane
 constexpr int BT_STAGES = 6;
 constexpr int BT_STAGE_DOUBLES = BT_CONS_WARPS * BT_ROWS;  // 8 columns x 512 rows = 32 KB
 
+__device__ __forceinline__ void bdot_finish(const double* acc, int stride, double* __restrict__ part,
+                                            double* __restrict__ out, unsigned* counter, bool live,
+                                            const XchgDev* xc);
+
 template <int NV>
 __global__ void __launch_bounds__(BT_THREADS, 1)
     bdot_tma_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
@@ -642,14 +647,22 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         }
     }
     __syncthreads();
+    bdot_finish(acc, stride, part, out, counter, live, xc);
+}
+
+// Stage 2 of the bulk-copy block dots (whole CTA, after a __syncthreads that made acc
+// final): this CTA's partial to global memory, then the last K CTAs to finish (the grid is
+// co-resident: one CTA per SM) each sum a contiguous slice of the 2(p+1) outputs over the
+// partials in CTA order -- the same order as one finisher, K times the parallelism (c3,
+// p = 300: 602 outputs x 148 partials).  With the cross-rank exchange the slices go to this
+// rank's window slot and the last finisher runs the barrier and the sum over ranks
+// (xchg.cuh).
+__device__ __forceinline__ void bdot_finish(const double* acc, int stride, double* __restrict__ part,
+                                            double* __restrict__ out, unsigned* counter, bool live,
+                                            const XchgDev* xc) {
     for (int i = threadIdx.x; i < stride; i += blockDim.x) part[(int64_t)blockIdx.x * stride + i] = acc[i];
     __threadfence();
     __syncthreads();
-    // stage 2 on the last K CTAs to finish (the grid is co-resident: one CTA per SM), each
-    // summing a contiguous slice of the 2(p+1) outputs in CTA order -- the same order as one
-    // finisher, K times the parallelism (c3, p = 300: 602 outputs x 148 partials).  With the
-    // cross-rank exchange the slices go to this rank's window slot and the last finisher runs
-    // the barrier and the sum over ranks (xchg.cuh).
     const int G = (int)gridDim.x;
     const int K = min(G, max(1, min(16, stride / 32)));
     __shared__ unsigned s_ticket;
@@ -691,6 +704,197 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     if (threadIdx.x == 0) { counter[0] = 0u; counter[2] = 0u; counter[1] += live ? 1u : 0u; }
 }
 
+// ------------------------------------------------------------------------------------
+// K2, column-sweep form.  The tile-at-a-time kernel above lets every CTA run through all p
+// columns of one 512-row tile before the next; its CTAs drift apart, so at large p the
+// grid streams from hundreds of columns (2 MB pages, 8 MB apart at c3) at once.  Here the
+// CTAs sweep the columns together: a round gives CTA b the tiles r*G*S + j*G + b (j < S,
+// interleaved, so the G CTAs read one contiguous range of each column), and the producer
+// streams group g (8 columns) of all S tiles before group g+1.  u, z of the round's tiles
+// sit in a double-buffered shared slot (bulk copies, issued when the producer reaches the
+// round).  Consumer warp w owns rows 64w + 2l, +1 of every tile (16-B shared loads, u and z
+// for its 2 rows), accumulates the 8 columns of the group in registers over the S tiles,
+// then one butterfly transpose per group; the 8 warps' column sums meet in shared memory
+// and warp g%8 adds them into the CTA accumulator in warp order.  Fixed order everywhere:
+// bitwise deterministic.  Stage 2 as above (bdot_finish).
+// ------------------------------------------------------------------------------------
+constexpr int SW_STAGES = 4;
+constexpr int SW_S = 5;  // tiles per CTA per round
+
+static size_t bdot_sw_smem(int p, int nv) {
+    const size_t stride = (size_t)nv * (p + 1);
+    return (size_t)(SW_STAGES * BT_STAGE_DOUBLES + 2 * SW_S * 2 * BT_ROWS + 2 * BT_CONS_WARPS * 16) * sizeof(double) +
+           ((stride + 1) & ~(size_t)1) * sizeof(double) + (2 * SW_STAGES + 4) * sizeof(uint64_t);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(BT_THREADS, 1)
+    bdot_sw_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
+                   const double* __restrict__ u, const double* __restrict__ z,
+                   double* __restrict__ part, double* __restrict__ out, unsigned* counter,
+                   const int* istate, const XchgDev* xc) {
+    const bool live = running(istate);  // see bdot_kernel
+    if (!live && !xc) return;
+    extern __shared__ __align__(128) double smem_sw[];
+    double* ring = smem_sw;                                   // [STAGES][8][512]
+    double* uzs = ring + SW_STAGES * BT_STAGE_DOUBLES;        // [2 rounds][S tiles][u | z][512]
+    double* wsum = uzs + 2 * SW_S * 2 * BT_ROWS;              // [2][8 warps][16]
+    double* acc = wsum + 2 * BT_CONS_WARPS * 16;              // [NV*(p+1)]
+    const int ncols = p + 1;
+    const int stride = NV * ncols;
+    uint64_t* full = reinterpret_cast<uint64_t*>(acc + ((stride + 1) & ~1));
+    uint64_t* empty = full + SW_STAGES;
+    uint64_t* uzfull = empty + SW_STAGES;
+    uint64_t* uzempty = uzfull + 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < SW_STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, BT_CONS_WARPS); }
+        for (int s = 0; s < 2; s++) { mbar_init(uzfull + s, 1); mbar_init(uzempty + s, BT_CONS_WARPS); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t G = gridDim.x, b = blockIdx.x;
+    const int64_t ntiles = live ? (n + BT_ROWS - 1) / BT_ROWS : 0;
+    const int64_t per_round = G * SW_S;
+    const int64_t nrounds = (ntiles + per_round - 1) / per_round;
+    const int ngroups = (ncols + 7) / 8;
+    // tiles of this CTA in round r: r*G*S + j*G + b for j < nj(r)
+    auto tiles_in_round = [&](int64_t r) -> int {
+        const int64_t rem = ntiles - r * per_round - b;  // tiles at j*G + b < ntiles - r*G*S
+        return rem <= 0 ? 0 : (int)min((int64_t)SW_S, (rem + G - 1) / G);
+    };
+    if (warp == BT_CONS_WARPS) {
+        // ---------------- producer: one elected lane issues the bulk copies ----------------
+        if (lane == 0) {
+            uint32_t it = 0, kk = 0;
+            for (int64_t r = 0; r < nrounds; r++) {
+                const int nj = tiles_in_round(r);
+                if (nj == 0) continue;
+                const int slot = (int)(kk & 1);
+                mbar_wait(uzempty + slot, ((kk >> 1) & 1) ^ 1);
+                uint32_t uzb = 0;
+                for (int j = 0; j < nj; j++)
+                    if ((r * per_round + j * G + b + 1) * BT_ROWS <= n) uzb += (NV == 2 ? 2 : 1) * BT_ROWS * sizeof(double);
+                mbar_arrive_expect_tx(uzfull + slot, uzb);
+                for (int j = 0; j < nj; j++) {
+                    const int64_t row0 = (r * per_round + j * G + b) * BT_ROWS;
+                    if (row0 + BT_ROWS > n) continue;  // partial last tile: the consumers load it
+                    double* dst = uzs + ((size_t)slot * SW_S + j) * 2 * BT_ROWS;
+                    bulk_g2s(dst, u + row0, BT_ROWS * sizeof(double), uzfull + slot);
+                    if (NV == 2) bulk_g2s(dst + BT_ROWS, z + row0, BT_ROWS * sizeof(double), uzfull + slot);
+                }
+                for (int g = 0; g < ngroups; g++) {
+                    const int c0 = g * 8;
+                    const int nc = max(0, min(8, p - c0));  // V columns only (column p = u)
+                    for (int j = 0; j < nj; j++, it++) {
+                        const int s = it % SW_STAGES;
+                        mbar_wait(empty + s, ((it / SW_STAGES) & 1) ^ 1);
+                        const int64_t row0 = (r * per_round + j * G + b) * BT_ROWS;
+                        const int64_t rows = (n - row0 < BT_ROWS) ? n - row0 : BT_ROWS;
+                        const uint32_t bytes = (uint32_t)(((rows + 1) & ~1LL) * sizeof(double));
+                        mbar_arrive_expect_tx(full + s, (uint32_t)nc * bytes);
+                        for (int c = 0; c < nc; c++)
+                            bulk_g2s(ring + (size_t)s * BT_STAGE_DOUBLES + c * BT_ROWS,
+                                     V + (int64_t)(c0 + c) * ld + row0, bytes, full + s);
+                    }
+                }
+                kk++;
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int rr = 64 * warp + 2 * lane;  // this lane's two rows within a tile
+        uint32_t it = 0, kk = 0, gg = 0;      // gg: groups so far (wsum buffer parity)
+        for (int64_t r = 0; r < nrounds; r++) {
+            const int nj = tiles_in_round(r);
+            if (nj == 0) continue;
+            const int slot = (int)(kk & 1);
+            const double* uzr = uzs + (size_t)slot * SW_S * 2 * BT_ROWS;
+            // the partial last tile (at most one per launch): u, z straight from global memory
+            int jpart = -1;
+            int64_t prow0 = 0;
+            double pu0 = 0.0, pu1 = 0.0, pz0 = 0.0, pz1 = 0.0;
+            for (int j = 0; j < nj; j++) {
+                const int64_t row0 = (r * per_round + j * G + b) * BT_ROWS;
+                if (row0 + BT_ROWS > n) {
+                    jpart = j;
+                    prow0 = row0;
+                    const int64_t r0 = row0 + rr;
+                    if (r0 < n) { pu0 = __ldg(u + r0); if (NV == 2) pz0 = __ldg(z + r0); }
+                    if (r0 + 1 < n) { pu1 = __ldg(u + r0 + 1); if (NV == 2) pz1 = __ldg(z + r0 + 1); }
+                }
+            }
+            mbar_wait(uzfull + slot, (kk >> 1) & 1);
+            for (int g = 0; g < ngroups; g++) {
+                const int c0 = g * 8;
+                const int nvc = max(0, min(8, p - c0));  // V columns in this group
+                const int cu = p - c0;                   // column p (u itself) if 0 <= cu < 8
+                double au[8], az[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) { au[c] = 0.0; az[c] = 0.0; }
+                for (int j = 0; j < nj; j++, it++) {
+                    const int s = it % SW_STAGES;
+                    double u0, u1, z0 = 0.0, z1 = 0.0;
+                    const bool part_tile = (j == jpart);
+                    if (part_tile) {
+                        u0 = pu0; u1 = pu1; z0 = pz0; z1 = pz1;
+                    } else {
+                        const double2 uu = *reinterpret_cast<const double2*>(uzr + (size_t)j * 2 * BT_ROWS + rr);
+                        u0 = uu.x; u1 = uu.y;
+                        if (NV == 2) {
+                            const double2 zz = *reinterpret_cast<const double2*>(uzr + (size_t)j * 2 * BT_ROWS + BT_ROWS + rr);
+                            z0 = zz.x; z1 = zz.y;
+                        }
+                    }
+                    mbar_wait(full + s, (it / SW_STAGES) & 1);
+                    const double* st = ring + (size_t)s * BT_STAGE_DOUBLES + rr;
+                    const bool m0 = !part_tile || prow0 + rr < n, m1 = !part_tile || prow0 + rr + 1 < n;
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {
+                        double2 v;
+                        if (c < nvc) {
+                            v = *reinterpret_cast<const double2*>(st + c * BT_ROWS);
+                            if (part_tile) { v.x = m0 ? v.x : 0.0; v.y = m1 ? v.y : 0.0; }
+                        } else if (c == cu) {
+                            v = make_double2(u0, u1);
+                        } else {
+                            continue;
+                        }
+                        au[c] = fma(v.y, u1, fma(v.x, u0, au[c]));
+                        if (NV == 2) az[c] = fma(v.y, z1, fma(v.x, z0, az[c]));
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(empty + s);
+                }
+                // column c0 + (lane >> 2) summed over this warp's rows, in lanes 4c..4c+3
+                const double su = bfly8(au, lane);
+                const double sz = NV == 2 ? bfly8(az, lane) : 0.0;
+                double* ws = wsum + (gg++ & 1) * BT_CONS_WARPS * 16;
+                if ((lane & 3) == 0) {
+                    ws[warp * 16 + (lane >> 2)] = su;
+                    ws[warp * 16 + 8 + (lane >> 2)] = sz;
+                }
+                named_barrier(1, BT_CONS_WARPS * 32);
+                if (warp == (g & 7) && lane < 8 * NV) {  // lanes 0-7: V^T u column sums, 8-15: V^T z
+                    const int c = lane & 7, col = c0 + c;
+                    if (col < ncols) {
+                        double t = 0.0;
+#pragma unroll
+                        for (int w = 0; w < BT_CONS_WARPS; w++) t += ws[w * 16 + lane];
+                        acc[(lane >> 3) * ncols + col] += t;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(uzempty + slot);
+            kk++;
+        }
+    }
+    __syncthreads();
+    bdot_finish(acc, stride, part, out, counter, live, xc);
+}
+
 int bdot_grid_size(int64_t n, int num_sms) {
     const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
     int64_t g = (int64_t)num_sms * 2;  // also >= the bulk-copy kernel's grid (num_sms)
@@ -720,6 +924,22 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
         const int tg = (int)(ntiles < sms ? ntiles : sms);
+        static int sw_min_p = -1;  // A/B hook (IGS_BDOT_SW_MIN_P): column sweep from this p on
+        if (sw_min_p < 0) {
+            const char* e = std::getenv("IGS_BDOT_SW_MIN_P");
+            sw_min_p = e ? std::atoi(e) : (1 << 30);
+        }
+        const size_t wsmem = bdot_sw_smem(p, nv);
+        if (tg <= grid && p >= sw_min_p && wsmem <= 227 * 1024) {
+            if (nv == 2) {
+                cudaFuncSetAttribute(bdot_sw_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
+                bdot_sw_kernel<2><<<tg, BT_THREADS, wsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
+            } else {
+                cudaFuncSetAttribute(bdot_sw_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
+                bdot_sw_kernel<1><<<tg, BT_THREADS, wsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
+            }
+            return;
+        }
         if (tg <= grid) {
             if (nv == 2) {
                 cudaFuncSetAttribute(bdot_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);

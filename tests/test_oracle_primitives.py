@@ -257,3 +257,21 @@ def test_column_normwise_diff_detects_differences():
     # entries below the subdiagonal are outside the metric (the Hessenberg structure)
     B = H.copy(); B[10, 2] = 1.0
     assert oracle.column_normwise_diff(B, H, m) == 0.0
+
+
+def test_loss_of_orthogonality_closed_forms_and_row_blocks():
+    """||I - V^T V||_F against closed forms -- an orthonormal Q (QR) gives O(eps),
+    V = [e1, e1] gives ||[[0,-1],[-1,0]]||_F = sqrt(2), V = 2 I_k gives 3 sqrt(k) -- and the
+    row-blocked Gram (used for the 108 GB c5 basis) agrees with the one-shot Gram, including a
+    ragged last block."""
+    rng = np.random.default_rng(11)
+    Q, _ = np.linalg.qr(rng.standard_normal((1000, 20)))
+    assert oracle.loss_of_orthogonality(Q) <= 1e-14
+    E = np.zeros((50, 2)); E[0, :] = 1.0
+    assert abs(oracle.loss_of_orthogonality(E) - np.sqrt(2.0)) <= 1e-15
+    assert abs(oracle.loss_of_orthogonality(2.0 * np.eye(7)) - 3.0 * np.sqrt(7.0)) <= 1e-14
+    V = np.asfortranarray(rng.standard_normal((1003, 9)) * 0.3)
+    full = oracle.loss_of_orthogonality(V)
+    for rb in (1, 7, 1000, 5000):
+        assert abs(oracle.loss_of_orthogonality(V, row_block=rb) - full) <= 1e-13 * full
+    assert abs(oracle.loss_of_orthogonality(Q, row_block=64) - oracle.loss_of_orthogonality(Q)) <= 1e-14

@@ -41,12 +41,10 @@ def main():
     t0 = time.time()
     prob = W.config(a.config)
     t_gen = time.time() - t0
-    t0 = time.time()
-    normA = oracle.norm2_estimate(prob.A, maxit=a.norm_maxit)
-    t_norm = time.time() - t0
     rec = {"config": a.config, "gs": a.gs, "variant": var, "n": prob.A.n_rows, "nnz": prob.A.nnz,
-           "normA_2": normA, "normA_maxit": a.norm_maxit, "oracle_threads": oracle.num_threads(),
-           "written_by": "tools/oracle_records.py (oracle/ only)"}
+           "oracle_threads": oracle.num_threads(), "written_by": "tools/oracle_records.py (oracle/ only)"}
+    # memory order for c5 (V = 108 GB on a 196 GB host): the solve and the LOO first (the Gram
+    # in row blocks, no second copy of V), then V is dropped before ||A||_2 (scipy copy of A)
     t0 = time.time()
     if a.config == "c4":
         o = oracle.gmres(prob.A, prob.b, 3000, restart=100, tol=1e-12, variant=var, dot_block=4096)
@@ -57,14 +55,18 @@ def main():
     t_solve = time.time() - t0
     rec.update(iters=o["iters"], cycles=o["cycles"], term=o["term"], true_relres=o["true_relres"],
                basis_cols=o["basis_cols"], res_hist=[float(v) for v in o["res_hist"]],
-               beta=oracle.backward_error(prob.A, prob.b, o["x"], normA),
                x_norm=float(np.linalg.norm(o["x"])))
     if a.config == "c5":
         c = o["basis_cols"]
         t1 = time.time()
-        rec["loo"] = oracle.loss_of_orthogonality(o["V"][:, :c])
+        rec["loo"] = oracle.loss_of_orthogonality(o["V"][:, :c], row_block=1 << 20)
         rec["t_loo_s"] = time.time() - t1
         rec["H_first30"] = o["H"][:31, :30].T.tolist()  # column j = H[:31, j]
+        del o["V"]
+    t0 = time.time()
+    normA = oracle.norm2_estimate(prob.A, maxit=a.norm_maxit)
+    t_norm = time.time() - t0
+    rec.update(normA_2=normA, normA_maxit=a.norm_maxit, beta=oracle.backward_error(prob.A, prob.b, o["x"], normA))
     import resource
     rec.update(t_generate_s=t_gen, t_norm_s=t_norm, t_solve_s=t_solve,
                host_peak_rss_gb=resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6)
