@@ -151,6 +151,7 @@ struct igs_ctx {
     uint8_t* d_sell_len = nullptr;
     double* d_sell_val = nullptr;
     void* d_sell_col = nullptr;
+    longlong2* d_sell_xpf = nullptr;
     int64_t sell_entries = 0;
     // G > 1 with SELL: rows touching ghost columns run after the halo, the rest during it
     int64_t* d_bnd_rows = nullptr;
@@ -436,7 +437,7 @@ static void free_ctx(igs_ctx* c) {
     if (c->owns_ws) { cudaFree(c->d_V); }
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
     cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter); cudaFree(c->d_pcprof);
-    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col);
+    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col); cudaFree(c->d_sell_xpf);
     cudaFree(c->d_bnd_rows);
     if (c->hstream) cudaStreamDestroy(c->hstream);
     if (c->ev_x) cudaEventDestroy(c->ev_x);
@@ -516,6 +517,31 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     ctx->A.sell_val = ctx->d_sell_val;
     ctx->A.sell_col = ctx->d_sell_col;
     ctx->sell_entries = tot;
+    {
+        // first-touch x ranges per SpMV CTA (IGS_SPMV_XPF=0 disables; A/B hook)
+        const char* ex = std::getenv("IGS_SPMV_XPF");
+        if (!(ex && std::atoi(ex) == 0)) {
+            const int64_t nb = (n + SELL_CTA_ROWS - 1) / SELL_CTA_ROWS;
+            std::vector<longlong2> xpf((size_t)nb);
+            int64_t prevmax = -1;
+            for (int64_t cb = 0; cb < nb; cb++) {
+                int64_t hi = -1;
+                for (int64_t r = cb * SELL_CTA_ROWS; r < std::min<int64_t>(n, (cb + 1) * SELL_CTA_ROWS); r++)
+                    for (int64_t q = rowptr[r]; q < rowptr[r + 1]; q++) {
+                        const int64_t c = local_col[(size_t)q];
+                        if (c < n && c > hi) hi = c;
+                    }
+                const int64_t lo = (prevmax + 1) & ~(int64_t)1;
+                const int64_t cnt = (hi + 1 - lo) & ~(int64_t)1;  // even: 16-B bulk prefetch
+                xpf[(size_t)cb].x = lo;
+                xpf[(size_t)cb].y = (hi > prevmax && cnt > 0 && cnt <= 4096) ? cnt : 0;
+                prevmax = std::max(prevmax, hi);
+            }
+            CUDA_TRY(cudaMalloc(&ctx->d_sell_xpf, sizeof(longlong2) * xpf.size()));
+            CUDA_TRY(cudaMemcpy(ctx->d_sell_xpf, xpf.data(), sizeof(longlong2) * xpf.size(), cudaMemcpyHostToDevice));
+            ctx->A.sell_xpf = ctx->d_sell_xpf;
+        }
+    }
     if (!bnd.empty()) {
         CUDA_TRY(cudaMalloc(&ctx->d_bnd_rows, sizeof(int64_t) * bnd.size()));
         CUDA_TRY(cudaMemcpy(ctx->d_bnd_rows, bnd.data(), sizeof(int64_t) * bnd.size(), cudaMemcpyHostToDevice));

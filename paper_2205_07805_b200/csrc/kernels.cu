@@ -165,8 +165,16 @@ __global__ void __launch_bounds__(SELL_THREADS)
     spmv_sell_kernel(int64_t nrows, const int64_t* __restrict__ sptr, const uint8_t* __restrict__ slen,
                      const IT* __restrict__ col, const double* __restrict__ val,
                      const double* __restrict__ x, const double* __restrict__ ghost, int64_t nloc,
-                     double* __restrict__ y, const double* __restrict__ b, const int* istate, int ahead) {
+                     double* __restrict__ y, const double* __restrict__ b, const int* istate, int ahead,
+                     const longlong2* __restrict__ xpf) {
     if (!running(istate)) return;
+    if (ahead > 0 && xpf && threadIdx.x == 32) {  // the x range that CTA touches first
+        const int64_t fb = (int64_t)blockIdx.x + ahead;
+        if (fb < (int64_t)gridDim.x) {
+            const longlong2 rg = __ldg(xpf + fb);
+            if (rg.y > 0) bulk_prefetch_l2(x + rg.x, (uint32_t)(rg.y * sizeof(double)));
+        }
+    }
     if (ahead > 0 && threadIdx.x == 0) {
         // the CTA that runs about one resident wave later: its values and columns to L2 now
         const int64_t nb = (int64_t)gridDim.x, fb = (int64_t)blockIdx.x + ahead;
@@ -227,12 +235,14 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
         ahead = 4 * sms;
     }
     const IT* ci = static_cast<const IT*>(a.sell_col);
+    static_assert(SELL_THREADS == SELL_CTA_ROWS, "x prefetch ranges are per SpMV CTA");
+    const longlong2* xpf = ((uintptr_t)x % 16) == 0 ? a.sell_xpf : nullptr;
     if (a.ghost) {
-        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
-        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
+        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead, xpf);
+        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead, xpf);
     } else {
-        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
-        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
+        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead, xpf);
+        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead, xpf);
     }
 }
 
@@ -924,10 +934,13 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
         const int tg = (int)(ntiles < sms ? ntiles : sms);
-        static int sw_min_p = -1;  // A/B hook (IGS_BDOT_SW_MIN_P): column sweep from this p on
+        // the column sweep from p = 96 on (c3 p = 300: 6.39 -> 6.75 TB/s; at p = 10-75 the
+        // tile kernel is ahead: c4 p = 25 6.92 vs 5.79; profiles/r2/bdot_sweep_ab.md);
+        // IGS_BDOT_SW_MIN_P moves the switch (A/B and test hook)
+        static int sw_min_p = -1;
         if (sw_min_p < 0) {
             const char* e = std::getenv("IGS_BDOT_SW_MIN_P");
-            sw_min_p = e ? std::atoi(e) : (1 << 30);
+            sw_min_p = e ? std::atoi(e) : 96;
         }
         const size_t wsmem = bdot_sw_smem(p, nv);
         if (tg <= grid && p >= sw_min_p && wsmem <= 227 * 1024) {

@@ -24,13 +24,15 @@ def _dev(torch, a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-@pytest.mark.parametrize("n", [5, 1024 * 3 + 17, 70001, 1 << 20])
+@pytest.mark.parametrize("n", [5, 1024 * 3 + 17, 70001, 1 << 20, 2 * 740 * 512 + 777])
 @pytest.mark.parametrize("p", [0, 1, 7, 64, 300])
 def test_block_dot_vs_oracle(torch_cuda, n, p):
     torch = torch_cuda
     import paper_2205_07805_b200 as P
     if n == 1 << 20 and p == 300:
         p = 100
+    # (n = 2 * 740 * 512 + 777: three rounds of the column-sweep kernel -- 148 CTAs x 5 tiles --
+    #  the last with two tiles, one of them partial; p >= 96 takes that kernel)
     rng = np.random.default_rng(n + p)
     ld = n + (n % 2) + 32           # padded, even
     Vh = rng.standard_normal((p + 1, ld))   # column-major storage: row j = column j
