@@ -225,13 +225,23 @@ def backward_error(A, b, x, normA: float) -> float:
 def loss_of_orthogonality(V, row_block: int = 0) -> float:
     """||I - V^T V||_F.  row_block > 0: V^T V summed over blocks of that many rows
     (the same sum over rows, in blocks, so a 100-column basis of 134M rows -- c5, 108 GB --
-    needs no second copy of V)."""
+    needs no second copy of V), the block Grams added pairwise."""
     V = np.asarray(V)
     if row_block > 0:
-        G = np.zeros((V.shape[1], V.shape[1]))
+        # block Grams added pairwise (a binary tree over the blocks, the same sum over rows):
+        # the Gram of a 134M-row basis then carries O(log(blocks) eps) of rounding instead of
+        # O(blocks eps), below the orthogonality it is there to measure
+        stack = []
         for i in range(0, V.shape[0], row_block):
             B = np.array(V[i:i + row_block])
-            G += B.T @ B
+            G, lvl = B.T @ B, 0
+            while stack and stack[-1][0] == lvl:
+                G = stack.pop()[1] + G
+                lvl += 1
+            stack.append((lvl, G))
+        G = stack.pop()[1]
+        while stack:
+            G = stack.pop()[1] + G
     else:
         G = V.T @ V
     return float(np.linalg.norm(np.eye(V.shape[1]) - G, "fro"))

@@ -2039,8 +2039,18 @@ void launch_trisolve(int order, const double* L, int ldl, const double* b, doubl
 
 // ------------------------------------------------------------------------------------
 // LOO diagnostic: G = V^T V (tiled, deterministic), ||I - G||_F
+// Each thread sums 4096-row pieces with FMAs and adds the pieces into a compensated
+// (Neumaier) running sum; the splits are combined the same way.  A plain running sum over a
+// split of 2.1M rows (c5: 134M rows / 64) drifted by ~1e-12 per entry -- LOO 6.9e-11 against
+// ~1e-12 from the same basis -- i.e. the diagnostic measured its own rounding.
 // ------------------------------------------------------------------------------------
-constexpr int GR_T = 32, GR_R = 64;
+constexpr int GR_T = 32, GR_R = 64, GR_PIECE = 64;  // GR_PIECE tiles of GR_R rows per piece
+
+__device__ __forceinline__ void neumaier_add(double& s, double& comp, double x) {
+    const double t = s + x;
+    comp += (fabs(s) >= fabs(x)) ? (s - t) + x : (x - t) + s;
+    s = t;
+}
 
 __global__ void __launch_bounds__(256)
     gram_kernel(int64_t n, int c, const double* __restrict__ V, int64_t ld,
@@ -2057,6 +2067,8 @@ __global__ void __launch_bounds__(256)
     const int64_t rend = rbeg + chunk < n ? rbeg + chunk : n;
     const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double sum[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, comp[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    int pieces = 0;
     for (int64_t r0 = rbeg; r0 < rend; r0 += GR_R) {
         for (int e = threadIdx.x; e < GR_T * GR_R; e += 256) {
             const int cc = e / GR_R, rr = e % GR_R;
@@ -2076,11 +2088,17 @@ __global__ void __launch_bounds__(256)
             acc[1][1] = fma(a1, b1, acc[1][1]);
         }
         __syncthreads();
+        if (++pieces == GR_PIECE) {
+            pieces = 0;
+            for (int a = 0; a < 2; a++)
+                for (int b = 0; b < 2; b++) { neumaier_add(sum[a][b], comp[a][b], acc[a][b]); acc[a][b] = 0.0; }
+        }
     }
     for (int a = 0; a < 2; a++)
         for (int b = 0; b < 2; b++) {
+            neumaier_add(sum[a][b], comp[a][b], acc[a][b]);
             const int i = ti * GR_T + 2 * ty + a, j = tj * GR_T + 2 * tx + b;
-            if (i < c && j < c) part[((int64_t)split * c + i) * c + j] = acc[a][b];
+            if (i < c && j < c) part[((int64_t)split * c + i) * c + j] = sum[a][b] + comp[a][b];
         }
 }
 
@@ -2089,9 +2107,9 @@ __global__ void gram_reduce_kernel(int c, int splits, const double* __restrict__
     if (e >= (int64_t)c * c) return;
     const int i = (int)(e / c), j = (int)(e % c);
     const int a = i < j ? i : j, b = i < j ? j : i;  // computed entries live in the upper part
-    double s = 0.0;
-    for (int k = 0; k < splits; k++) s += part[((int64_t)k * c + a) * c + b];
-    G[e] = s;
+    double s = 0.0, comp = 0.0;
+    for (int k = 0; k < splits; k++) neumaier_add(s, comp, part[((int64_t)k * c + a) * c + b]);
+    G[e] = s + comp;
 }
 
 void launch_gram(int64_t n, int c, const double* V, int64_t ld, double* part, int splits,

@@ -275,3 +275,9 @@ def test_loss_of_orthogonality_closed_forms_and_row_blocks():
     for rb in (1, 7, 1000, 5000):
         assert abs(oracle.loss_of_orthogonality(V, row_block=rb) - full) <= 1e-13 * full
     assert abs(oracle.loss_of_orthogonality(Q, row_block=64) - oracle.loss_of_orthogonality(Q)) <= 1e-14
+    # the blocked form is accurate where a long running sum is not: one normalised constant
+    # column of 3 * 2^20 rows has ||I - V^T V||_F = 0 up to rounding (a running sum of its
+    # 3M squares drifts by ~1e-10)
+    n = 3 << 20
+    c = np.full((n, 1), 1.0 / np.sqrt(n))
+    assert oracle.loss_of_orthogonality(c, row_block=4096) <= 1e-13

@@ -59,7 +59,7 @@ def main():
     if a.config == "c5":
         c = o["basis_cols"]
         t1 = time.time()
-        rec["loo"] = oracle.loss_of_orthogonality(o["V"][:, :c], row_block=1 << 20)
+        rec["loo"] = oracle.loss_of_orthogonality(o["V"][:, :c], row_block=4096)
         rec["t_loo_s"] = time.time() - t1
         rec["H_first30"] = o["H"][:31, :30].T.tolist()  # column j = H[:31, j]
         del o["V"]
