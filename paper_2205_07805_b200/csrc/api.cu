@@ -108,6 +108,7 @@ struct igs_ctx {
     double* d_gram = nullptr;  // gram partials + G
     size_t gram_cap = 0;
     int bdot_grid = 1;
+    int part_rows = 1;  // capacity of d_part in rows (>= every reduction grid)
     Dev dev_state{};
     double* h_pinned = nullptr;  // small pinned staging
     int* h_pinned_int = nullptr;
@@ -151,7 +152,6 @@ struct igs_ctx {
     uint8_t* d_sell_len = nullptr;
     double* d_sell_val = nullptr;
     void* d_sell_col = nullptr;
-    longlong2* d_sell_xpf = nullptr;
     int64_t sell_entries = 0;
     // G > 1 with SELL: rows touching ghost columns run after the halo, the rest during it
     int64_t* d_bnd_rows = nullptr;
@@ -437,7 +437,7 @@ static void free_ctx(igs_ctx* c) {
     if (c->owns_ws) { cudaFree(c->d_V); }
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
     cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter); cudaFree(c->d_pcprof);
-    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col); cudaFree(c->d_sell_xpf);
+    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col);
     cudaFree(c->d_bnd_rows);
     if (c->hstream) cudaStreamDestroy(c->hstream);
     if (c->ev_x) cudaEventDestroy(c->ev_x);
@@ -517,31 +517,6 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     ctx->A.sell_val = ctx->d_sell_val;
     ctx->A.sell_col = ctx->d_sell_col;
     ctx->sell_entries = tot;
-    {
-        // first-touch x ranges per SpMV CTA (IGS_SPMV_XPF=0 disables; A/B hook)
-        const char* ex = std::getenv("IGS_SPMV_XPF");
-        if (!(ex && std::atoi(ex) == 0)) {
-            const int64_t nb = (n + SELL_CTA_ROWS - 1) / SELL_CTA_ROWS;
-            std::vector<longlong2> xpf((size_t)nb);
-            int64_t prevmax = -1;
-            for (int64_t cb = 0; cb < nb; cb++) {
-                int64_t hi = -1;
-                for (int64_t r = cb * SELL_CTA_ROWS; r < std::min<int64_t>(n, (cb + 1) * SELL_CTA_ROWS); r++)
-                    for (int64_t q = rowptr[r]; q < rowptr[r + 1]; q++) {
-                        const int64_t c = local_col[(size_t)q];
-                        if (c < n && c > hi) hi = c;
-                    }
-                const int64_t lo = (prevmax + 1) & ~(int64_t)1;
-                const int64_t cnt = (hi + 1 - lo) & ~(int64_t)1;  // even: 16-B bulk prefetch
-                xpf[(size_t)cb].x = lo;
-                xpf[(size_t)cb].y = (hi > prevmax && cnt > 0 && cnt <= 4096) ? cnt : 0;
-                prevmax = std::max(prevmax, hi);
-            }
-            CUDA_TRY(cudaMalloc(&ctx->d_sell_xpf, sizeof(longlong2) * xpf.size()));
-            CUDA_TRY(cudaMemcpy(ctx->d_sell_xpf, xpf.data(), sizeof(longlong2) * xpf.size(), cudaMemcpyHostToDevice));
-            ctx->A.sell_xpf = ctx->d_sell_xpf;
-        }
-    }
     if (!bnd.empty()) {
         CUDA_TRY(cudaMalloc(&ctx->d_bnd_rows, sizeof(int64_t) * bnd.size()));
         CUDA_TRY(cudaMemcpy(ctx->d_bnd_rows, bnd.data(), sizeof(int64_t) * bnd.size(), cudaMemcpyHostToDevice));
@@ -927,7 +902,10 @@ static igs_status ensure_workspace(igs_ctx* ctx, int m, int k, bool host_vec) {
         CUDA_TRY(cudaMemsetAsync(ctx->d_small, 0, nsd * sizeof(double), ctx->stream));
         CUDA_TRY(cudaMalloc(&ctx->d_int, sizeof(int) * ST_COUNT));
         CUDA_TRY(cudaMemsetAsync(ctx->d_int, 0, sizeof(int) * ST_COUNT, ctx->stream));
-        CUDA_TRY(cudaMalloc(&ctx->d_part, sizeof(double) * (size_t)ctx->bdot_grid * (2 * (mm + 1) + 2)));
+        // rows of partials: any reduction kernel's grid (block dots, the persistent kernel's
+        // row-block dots with up to one CTA per SM)
+        ctx->part_rows = std::max(ctx->bdot_grid, ctx->num_sms);
+        CUDA_TRY(cudaMalloc(&ctx->d_part, sizeof(double) * (size_t)ctx->part_rows * (2 * (mm + 1) + 2)));
         Dev& d = ctx->dev_state;
         d.m = mm;
         d.ldh = mm + 1;
@@ -1139,7 +1117,9 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
         const double by = (double)m * spmv_bytes(ctx) + 16.0 * n * 0.5 * m * (m + 1);
         TIMED(IGS_K_PERSIST, by, {
             // row-block dots above pc_rowsplit_n rows (each CTA would otherwise re-read u, z)
-            double* part = (n >= ctx->pc_rowsplit_n && grid - 1 <= ctx->bdot_grid) ? ctx->d_part : nullptr;
+            // (round 1 also required grid - 1 <= bdot_grid, the partials' old capacity: n = 90000
+            //  and 147456 fell back to whole-column dots at 0.37-0.47x the graph path's speed)
+            double* part = (n >= ctx->pc_rowsplit_n && grid - 1 <= ctx->part_rows) ? ctx->d_part : nullptr;
             // long rows on the CSR phase (no SELL copy): stage u in shared memory
             const int xs = ctx->xs_enabled && !ctx->A.sell_ptr && n <= pcycle_xs_max() &&
                            ctx->nnz >= 32 * n;

@@ -70,10 +70,6 @@ struct SpmvArgs {
     const uint8_t* sell_len = nullptr;  // [nrows] nonzeros of each row (<= 255)
     const double* sell_val = nullptr;
     const void* sell_col = nullptr;     // int32 or int64 (idx64), local column space
-    // per SpMV CTA (SELL_CTA_ROWS rows): the range of x it touches first -- local columns above
-    // every earlier CTA's largest, {first, count} in doubles, count 0 when none or > 32 KB --
-    // prefetched into L2 about one resident wave ahead (banded matrices: the +N^2 plane)
-    const longlong2* sell_xpf = nullptr;
     // G > 1: rows with a ghost column (sell_len == SELL_BOUNDARY, not in the SELL arrays),
     // multiplied by launch_spmv_rows once the halo has arrived.  With a SELL copy the CSR
     // arrays above hold only these rows (row t of the compact CSR is row bnd_rows[t])
@@ -81,7 +77,6 @@ struct SpmvArgs {
     int64_t n_bnd = 0;
 };
 constexpr uint8_t SELL_BOUNDARY = 255;
-constexpr int SELL_CTA_ROWS = 256;  // rows per CTA of the SELL SpMV kernel
 // y[r] = (b[r] -) A[r,:] x for the rows in a.bnd_rows (CSR arrays, ghosts), left-to-right
 void launch_spmv_rows(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
                       const int* istate, cudaStream_t s);

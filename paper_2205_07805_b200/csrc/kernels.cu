@@ -12,6 +12,7 @@
 //                        V_p (the paper's "merge ... into one GPU kernel")
 //   xupdate_kernel       x += V_p y
 //   gram/loo kernels     ||I - V^T V||_F diagnostic
+#include <algorithm>
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -165,16 +166,8 @@ __global__ void __launch_bounds__(SELL_THREADS)
     spmv_sell_kernel(int64_t nrows, const int64_t* __restrict__ sptr, const uint8_t* __restrict__ slen,
                      const IT* __restrict__ col, const double* __restrict__ val,
                      const double* __restrict__ x, const double* __restrict__ ghost, int64_t nloc,
-                     double* __restrict__ y, const double* __restrict__ b, const int* istate, int ahead,
-                     const longlong2* __restrict__ xpf) {
+                     double* __restrict__ y, const double* __restrict__ b, const int* istate, int ahead) {
     if (!running(istate)) return;
-    if (ahead > 0 && xpf && threadIdx.x == 32) {  // the x range that CTA touches first
-        const int64_t fb = (int64_t)blockIdx.x + ahead;
-        if (fb < (int64_t)gridDim.x) {
-            const longlong2 rg = __ldg(xpf + fb);
-            if (rg.y > 0) bulk_prefetch_l2(x + rg.x, (uint32_t)(rg.y * sizeof(double)));
-        }
-    }
     if (ahead > 0 && threadIdx.x == 0) {
         // the CTA that runs about one resident wave later: its values and columns to L2 now
         const int64_t nb = (int64_t)gridDim.x, fb = (int64_t)blockIdx.x + ahead;
@@ -235,14 +228,12 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
         ahead = 4 * sms;
     }
     const IT* ci = static_cast<const IT*>(a.sell_col);
-    static_assert(SELL_THREADS == SELL_CTA_ROWS, "x prefetch ranges are per SpMV CTA");
-    const longlong2* xpf = ((uintptr_t)x % 16) == 0 ? a.sell_xpf : nullptr;
     if (a.ghost) {
-        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead, xpf);
-        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead, xpf);
+        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
+        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
     } else {
-        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead, xpf);
-        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead, xpf);
+        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
+        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
     }
 }
 
@@ -907,8 +898,12 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
 
 int bdot_grid_size(int64_t n, int num_sms) {
     const int64_t ntiles = (n + BD_TILE - 1) / BD_TILE;
-    int64_t g = (int64_t)num_sms * 2;  // also >= the bulk-copy kernel's grid (num_sms)
+    int64_t g = (int64_t)num_sms * 2;
     if (g > ntiles) g = ntiles;
+    // also >= the bulk-copy kernels' grid (one CTA per 512-row tile, at most one per SM): with
+    // 1024-row register tiles alone, n in (75K, 151K) left the bulk-copy kernel out
+    const int64_t tg = std::min<int64_t>((n + BT_ROWS - 1) / BT_ROWS, num_sms);
+    if (g < tg) g = tg;
     if (g < 1) g = 1;
     return (int)g;
 }
