@@ -23,8 +23,10 @@
  *   dot_block == 0 : sequential left-to-right sum over all n entries;
  *   dot_block == B : sequential sums of consecutive blocks of B entries, then a
  *                    sequential sum of the block sums (used to measure the parity
- *                    noise floor, SURVEY §8(c) "Parity noise floor").
- * Both are deterministic for any OpenMP thread count.
+ *                    noise floor, SURVEY §8(c) "Parity noise floor");
+ *   dot_block == -B: the same blocks, the block sums added pairwise (reading R27; the
+ *                    c5 record, 134M rows).
+ * All are deterministic for any OpenMP thread count.
  *
  * Parity pins (tests/test_oracle_*.py): dense LU on tiny systems, the Arnoldi
  * relation, O(eps) orthogonality for two sweeps, eps*kappa(B_k) for one sweep and MGS,
@@ -71,8 +73,25 @@ void oracle_spmv(int64_t n, const int64_t* rowptr, const int64_t* colind, const 
     }
 }
 
-/* a . b with the reduction-order knob. */
+/* sum of x[0..m) as a pairwise (binary) tree: halves added recursively */
+static double pairwise_sum(const double* x, int64_t m) {
+    if (m <= 8) {
+        double s = 0.0;
+        for (int64_t i = 0; i < m; i++) s += x[i];
+        return s;
+    }
+    const int64_t h = m / 2;
+    return pairwise_sum(x, h) + pairwise_sum(x + h, m - h);
+}
+
+/* a . b with the reduction-order knob: block == 0 (or >= n) one running sum; block > 0
+ * running sums over blocks of `block` entries, the block sums added in order; block < 0
+ * blocks of -block entries, the block sums added pairwise (reading R27: at n = 134M the
+ * running sum over 32K block sums carries ~n_blocks eps of rounding into every inner
+ * product, which then dominates the basis' loss of orthogonality). */
 double oracle_dot(int64_t n, const double* a, const double* b, int64_t block) {
+    const int pairwise = block < 0;
+    if (block < 0) block = -block;
     if (block <= 0 || block >= n) {
         double s = 0.0;
         for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
@@ -88,7 +107,9 @@ double oracle_dot(int64_t n, const double* a, const double* b, int64_t block) {
         part[q] = s;
     }
     double s = 0.0;
-    for (int64_t q = 0; q < nb; q++) s += part[q];
+    if (pairwise) s = pairwise_sum(part, nb);
+    else
+        for (int64_t q = 0; q < nb; q++) s += part[q];
     free(part);
     return s;
 }

@@ -281,3 +281,23 @@ def test_loss_of_orthogonality_closed_forms_and_row_blocks():
     n = 3 << 20
     c = np.full((n, 1), 1.0 / np.sqrt(n))
     assert oracle.loss_of_orthogonality(c, row_block=4096) <= 1e-13
+
+
+def test_dot_pairwise_block_mode():
+    """oracle.dot with block = -B (blocks of B, block sums added pairwise; reading R27):
+    exact where every order is exact, the same value as the running-sum modes up to rounding,
+    and accurate where a running sum over many blocks is not: a normalised constant vector of
+    3 * 2^20 entries has v.v = 1 up to rounding."""
+    x = np.ldexp(np.arange(1, 100001, dtype=np.float64), -20)   # products and sums exact
+    exact = float(np.sum(x * x))
+    assert oracle.dot(x, x, -512) == oracle.dot(x, x, 512) == oracle.dot(x, x, 0) == exact
+    rng = np.random.default_rng(5)
+    a, b = rng.standard_normal(70001), rng.standard_normal(70001)
+    ref = float(np.dot(a, b))
+    for blk in (-1, -7, -4096, -70001, -100000):
+        assert abs(oracle.dot(a, b, blk) - ref) <= 1e-12 * np.abs(a) @ np.abs(b)
+    n = 3 << 20
+    v = np.full(n, 1.0 / np.sqrt(n))
+    assert abs(oracle.dot(v, v, -4096) - 1.0) <= 1e-13
+    assert abs(oracle.dot(v, v, 0) - 1.0) >= 1e-12   # (the single running sum: ~5e-11)
+
