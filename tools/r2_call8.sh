@@ -2,6 +2,8 @@
 # L1::no_allocate A/B, GPU suite
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/c8_build.log 2>&1 || { tail -30 gpurun_out/c8_build.log; exit 1; }
+( OMP_NUM_THREADS=14 python tools/oracle_records.py c5 --norm-maxit 60 --out gpurun_out/oracle_c5_gs2_v3.json > gpurun_out/c8_orc5.log 2>&1; echo "orc5 rc=$?" >> gpurun_out/c8_orc5.log ) &
+ORC=$!
 for na in 0 1; do
   IGS_UPDATE_NA=$na python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-solve > gpurun_out/c8_bench_na$na.json 2> gpurun_out/c8_bench_na$na.err
   python -c "import json; d=json.load(open('gpurun_out/c8_bench_na$na.json')); print('na=$na', round(d['value'],1), d['kernels']['update'], d['clocks']['sm_mhz'])"
@@ -16,4 +18,9 @@ import sys, json
 for l in sys.stdin:
     if not l.startswith('{'): continue
     d = json.loads(l); print(d['N'], d['n'], d['alg'], d['m'], round(d['persistent'].get('it_s', 0)), round(d['graphs'].get('it_s', 0)), round(d['ratio'] or 0, 3))"
-timeout 2400 python -m pytest tests -m gpu -q ${PYK:-} > gpurun_out/c8_pytest.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/c8_pytest.log
+timeout 2400 python -m pytest tests -m gpu -q -k "not c5_k100" > gpurun_out/c8_pytest.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/c8_pytest.log
+for i in $(seq 1 240); do kill -0 $ORC 2>/dev/null || break; sleep 15; done
+wait $ORC
+tail -c 1200 gpurun_out/c8_orc5.log
+cp gpurun_out/oracle_c5_gs2_v3.json tests/golden/oracle_c5_gs2.json && \
+timeout 1200 python -m pytest tests/test_gpu_solve.py -q -m gpu -k "c5_k100" > gpurun_out/c8_c5test.log 2>&1; echo "c5 test rc=$?"; tail -15 gpurun_out/c8_c5test.log
