@@ -303,6 +303,22 @@ igs_status igs_create_virtual(igs_ctx** out, int nranks, int64_t n_global, const
                               const double* values, int cuda_device, void* cuda_stream);
 igs_status igs_virtual_spmv(igs_ctx* const* ctxs, int nranks, const double* const* x, double* const* y,
                             const double* const* b);
+/* igs_virtual_solve runs igs_solve_alg(ctxs[r], IGS_MEM_DEVICE, b[r], NULL, k, restart, tol,
+ * algorithm, &res[r]) for every member r of one virtual group at once -- one host thread and
+ * one private stream per member -- i.e. the G > 1 solve of SURVEY §8(e) (row-block SpMV with
+ * the halo overlapped with the interior rows, one cross-rank sum of the 2(p+1) dots per
+ * iteration, replicated small state, uniform stops at the checkpoints) on a single device,
+ * with the two NCCL transports emulated: the cross-rank sum stages every member's vector and
+ * sums the G copies in member order (host barrier, cross-stream events, device copies; no
+ * kernel ever waits on another member), the halo packs into the send buffers and copies the
+ * ghosts from them.  The fused NVLink exchange, graphs and the persistent kernel are not
+ * used (as at G > 1 without a symmetric window).  b[r] and res[r].x are rank r's rows
+ * (device); every other igs_result field as for igs_solve.  Test hook for the one-GPU pool:
+ * it checks the product's G > 1 control flow and numerics against the oracle, not NCCL.
+ * Errors: as igs_solve, prefixed with the failing member; a member that fails releases the
+ * others (IGS_ERR_STATE "a member failed") instead of leaving them at a barrier. */
+igs_status igs_virtual_solve(igs_ctx* const* ctxs, int nranks, const double* const* b, int k, int restart,
+                             double tol, int algorithm, igs_result* res);
 
 /* ---------------------------------------------------------------------------------
  * Host-only halo planning (no device needed; used by igs_create and by CPU tests).

@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <map>
 #include <utility>
@@ -176,6 +178,13 @@ struct igs_ctx {
     // virtual ranks (igs_create_virtual, test hook): G contexts of one process on one device;
     // the halo copies from the owning context's send buffer instead of NCCL send/recv
     struct VGroup* vgroup = nullptr;
+    // igs_virtual_solve: the member runs igs_solve on its own host thread and stream; its
+    // collectives are emulated (vallreduce / vhalo: host barrier + cross-stream events +
+    // device copies, no device-side waiting between members)
+    bool vsolve = false;
+    uint64_t v_ar_calls = 0, v_halo_calls = 0;
+    double* d_vstage = nullptr;  // [2][vstage_cap] allreduce staging (call parity)
+    size_t vstage_cap = 0;
 };
 
 // ------------------------------------------------------------------------------ misc
@@ -314,6 +323,50 @@ struct VGroup {
     int G = 0;
     std::vector<igs_ctx*> members;
     int alive = 0;
+    // igs_virtual_solve: a host barrier per emulated collective (members enqueue, then meet),
+    // and per (call parity, member) events: staged copy done, sum done, pack done, ghost
+    // copies done
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t gen = 0;
+    bool broken = false;
+    double timeout_s = 120.0;
+    std::vector<cudaEvent_t> ev_copy[2], ev_sum[2], ev_pack, ev_hcopy;
+    const double** d_stage_ptrs = nullptr;  // [2][G] device array of the members' staging slots
+    ~VGroup() {
+        for (int q = 0; q < 2; q++) {
+            for (cudaEvent_t e : ev_copy[q]) cudaEventDestroy(e);
+            for (cudaEvent_t e : ev_sum[q]) cudaEventDestroy(e);
+        }
+        for (cudaEvent_t e : ev_pack) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_hcopy) cudaEventDestroy(e);
+        if (d_stage_ptrs) cudaFree(d_stage_ptrs);
+    }
+    // all G members arrive (enqueue-time rendezvous); false if a member failed or time ran out
+    bool barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        if (broken) return false;
+        const uint64_t g0 = gen;
+        if (++arrived == G) {
+            arrived = 0;
+            gen++;
+            cv.notify_all();
+            return true;
+        }
+        const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return gen != g0 || broken; });
+        if (!ok || broken) {
+            broken = true;
+            cv.notify_all();
+            return false;
+        }
+        return true;
+    }
+    void fail() {
+        std::lock_guard<std::mutex> lk(mu);
+        broken = true;
+        cv.notify_all();
+    }
 };
 
 static igs_status setup_halo(igs_ctx* ctx, const int64_t* rowptr, const void* colind, int bits,
@@ -437,7 +490,7 @@ static void free_ctx(igs_ctx* c) {
     if (c->owns_ws) { cudaFree(c->d_V); }
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
     cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter); cudaFree(c->d_pcprof);
-    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col);
+    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col); cudaFree(c->d_vstage);
     cudaFree(c->d_bnd_rows);
     if (c->hstream) cudaStreamDestroy(c->hstream);
     if (c->ev_x) cudaEventDestroy(c->ev_x);
@@ -969,7 +1022,37 @@ static double spmv_bytes(const igs_ctx* c) {
            8.0 * c->n_ghost;
 }
 
+// igs_virtual_solve's allreduce: every member stages its vector (call parity slot), meets
+// the others at the host barrier, then sums the G slots in member order into its own
+// buffer after cross-stream waits on the peers' staging copies -- the same order on every
+// member, so the replicated small state stays bitwise identical, as with NCCL.  A slot is
+// rewritten two calls later only after every member's sum that read it (events).
+static igs_status vallreduce(igs_ctx* ctx, double* buf, int64_t count) {
+    VGroup& g = *ctx->vgroup;
+    const int r = ctx->rank, G = g.G;
+    const uint64_t call = ctx->v_ar_calls++;
+    const int par = (int)(call & 1);
+    ARG_CHECK((size_t)count <= ctx->vstage_cap, "virtual allreduce: staging slot too small");
+    cudaStream_t st = ctx->stream;
+    if (call >= 2)
+        for (int q = 0; q < G; q++) CUDA_TRY(cudaStreamWaitEvent(st, g.ev_sum[par][q], 0));
+    double* slot = ctx->d_vstage + (size_t)par * ctx->vstage_cap;
+    CUDA_TRY(cudaMemcpyAsync(slot, buf, sizeof(double) * count, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaEventRecord(g.ev_copy[par][r], st));
+    if (!g.barrier()) {
+        set_error("virtual allreduce: a member failed or did not arrive");
+        return IGS_ERR_STATE;
+    }
+    for (int q = 0; q < G; q++) CUDA_TRY(cudaStreamWaitEvent(st, g.ev_copy[par][q], 0));
+    launch_rank_sum(g.d_stage_ptrs + (size_t)par * G, G, count, buf, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(g.ev_sum[par][r], st));
+    ctx->n_allreduce++;
+    return IGS_OK;
+}
+
 static igs_status allreduce(igs_ctx* ctx, double* buf, int64_t count) {
+    if (ctx->vsolve) return vallreduce(ctx, buf, count);
     if (ctx->nranks == 1 && !ctx->force_nccl) return IGS_OK;
     TIMED(IGS_K_ALLREDUCE, 0.0,
           { NCCL_TRY(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, ctx->comm, ctx->stream)); });
@@ -977,7 +1060,44 @@ static igs_status allreduce(igs_ctx* ctx, double* buf, int64_t count) {
     return IGS_OK;
 }
 
+// igs_virtual_solve's halo: barrier A (every member has enqueued its ghost copies of the
+// previous exchange), pack once the peers' copies out of this member's send buffer are done,
+// barrier B (every member has packed), then this member's ghost copies from the owners' send
+// buffers after cross-stream waits on their pack events.  Every member takes part even with
+// no peers (the barriers count calls).
+static igs_status vhalo(igs_ctx* ctx, const double* x, const int* istate, cudaStream_t st) {
+    VGroup& g = *ctx->vgroup;
+    const int r = ctx->rank;
+    ctx->v_halo_calls++;
+    if (!g.barrier()) {
+        set_error("virtual halo: a member failed or did not arrive");
+        return IGS_ERR_STATE;
+    }
+    for (size_t i = 0; i < ctx->peers.size(); i++)
+        if (ctx->send_cnt[i]) CUDA_TRY(cudaStreamWaitEvent(st, g.ev_hcopy[(size_t)ctx->peers[i]], 0));
+    launch_pack(ctx->n_send, ctx->d_send_idx, x, ctx->d_send, istate, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(g.ev_pack[(size_t)r], st));
+    if (!g.barrier()) {
+        set_error("virtual halo: a member failed or did not arrive");
+        return IGS_ERR_STATE;
+    }
+    for (size_t i = 0; i < ctx->peers.size(); i++) {
+        if (!ctx->recv_cnt[i]) continue;
+        const igs_ctx* q = g.members[(size_t)ctx->peers[i]];
+        const size_t j = (size_t)(std::find(q->peers.begin(), q->peers.end(), ctx->rank) - q->peers.begin());
+        ARG_CHECK(j < q->peers.size() && q->send_cnt[j] == ctx->recv_cnt[i], "virtual halo: inconsistent plan");
+        CUDA_TRY(cudaStreamWaitEvent(st, g.ev_pack[(size_t)ctx->peers[i]], 0));
+        CUDA_TRY(cudaMemcpyAsync(ctx->d_ghost + ctx->recv_off[i], q->d_send + q->send_off[j],
+                                 sizeof(double) * ctx->recv_cnt[i], cudaMemcpyDeviceToDevice, st));
+    }
+    CUDA_TRY(cudaEventRecord(g.ev_hcopy[(size_t)r], st));
+    ctx->n_halo += (int64_t)ctx->peers.size();
+    return IGS_OK;
+}
+
 static igs_status halo_on(igs_ctx* ctx, const double* x, const int* istate, cudaStream_t st) {
+    if (ctx->vsolve) return vhalo(ctx, x, istate, st);
     if (ctx->vgroup) {
         // virtual ranks (test hook): the ghosts come from the owners' send buffers, which
         // igs_virtual_spmv packed (pack kernel) before any rank's SpMV was enqueued
@@ -1004,7 +1124,7 @@ static igs_status halo_on(igs_ctx* ctx, const double* x, const int* istate, cuda
 }
 
 static igs_status halo(igs_ctx* ctx, const double* x, const int* istate) {
-    if (ctx->nranks == 1 || ctx->peers.empty()) return IGS_OK;
+    if ((ctx->nranks == 1 || ctx->peers.empty()) && !ctx->vsolve) return IGS_OK;
     TIMED(IGS_K_HALO, 16.0 * ctx->n_send + 8.0 * ctx->n_ghost, { TRY(halo_on(ctx, x, istate, ctx->stream)); });
     return IGS_OK;
 }
@@ -1018,7 +1138,7 @@ static igs_status spmv(igs_ctx* ctx, const double* x, double* y, const double* b
     if (ctx->A.n_bnd > 0 && ctx->hstream) {
         CUDA_TRY(cudaEventRecord(ctx->ev_x, ctx->stream));
         CUDA_TRY(cudaStreamWaitEvent(ctx->hstream, ctx->ev_x, 0));
-        if (!ctx->peers.empty()) TRY(halo_on(ctx, x, istate, ctx->hstream));
+        if (!ctx->peers.empty() || ctx->vsolve) TRY(halo_on(ctx, x, istate, ctx->hstream));
         CUDA_TRY(cudaEventRecord(ctx->ev_h, ctx->hstream));
         TIMED(kind, by, {
             launch_spmv(ctx->A, x, y, b, resid, istate, ctx->stream);            // interior rows
@@ -1268,7 +1388,7 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             // with collectives in the loop the copied status must be the same on every rank:
             // read it after tail(p) (the status through iteration p is then final), so all
             // ranks leave the loop at the same checkpoint and issue the same collectives
-            if (ctx->comm) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
+            if (ctx->comm || ctx->vsolve) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_tail, 0));
             CUDA_TRY(cudaMemcpyAsync(h_status + ev_slot, ist + ST_STATUS, sizeof(int), cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaEventRecord(ev[ev_slot], st));
             if (ev_pending >= 0) {
@@ -1377,7 +1497,7 @@ static igs_status launch_cycle(igs_ctx* ctx, int m, int alg, int t0) {
     // (G > 1 too: the halo send/recv, ncclAllReduce and the exchange kernels are captured;
     //  every rank captures the same sequence, and a stop inside the cycle turns the remaining
     //  work into no-ops while the collectives still run on every rank)
-    const bool use_graph = ctx->graphs_enabled && !ctx->timing && !use_pcycle(ctx, alg) &&
+    const bool use_graph = ctx->graphs_enabled && !ctx->timing && !ctx->vsolve && !use_pcycle(ctx, alg) &&
                            ctx->n_local <= ((int64_t)1 << 21) && m <= 512 &&
                            (alg != IGS_ALG_MGS || (int64_t)m * (m + 7) / 2 <= 50000);  // MGS: O(m^2) nodes
     if (!use_graph) return run_cycle(ctx, m, alg, t0);
@@ -1440,7 +1560,8 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         return IGS_ERR_STATE;
     }
     ARG_CHECK(ctx && ctx->ok, "igs_solve: bad context");
-    ARG_CHECK(!ctx->vgroup, "igs_solve: virtual-rank contexts (igs_create_virtual) only run igs_virtual_spmv");
+    ARG_CHECK(!ctx->vgroup || ctx->vsolve,
+              "igs_solve: virtual-rank contexts (igs_create_virtual) run igs_virtual_spmv / igs_virtual_solve");
     ARG_CHECK(res && res->x && b, "igs_solve: NULL b / res / res->x");
     ARG_CHECK(algorithm >= IGS_ALG_IGS1 && algorithm <= IGS_ALG_MGS, "igs_solve_alg: unknown algorithm");
     ARG_CHECK(k >= 1 && (int64_t)k < ctx->n_global - 1, "igs_solve: need 1 <= k < n_global - 1 (P:873)");
@@ -1694,6 +1815,96 @@ extern "C" igs_status igs_virtual_spmv(igs_ctx* const* ctxs, int nranks, const d
     for (int r = 0; r < nranks; r++)
         TRY(spmv(ctxs[r], x[r], y[r], b ? b[r] : nullptr, b != nullptr, nullptr, IGS_K_SPMV));
     for (int r = 0; r < nranks; r++) TRY(wait_for(ctxs[r], nullptr, ctxs[r]->stream, "igs_virtual_spmv"));
+    return IGS_OK;
+}
+
+extern "C" igs_status igs_virtual_solve(igs_ctx* const* ctxs, int nranks, const double* const* b, int k,
+                                        int restart, double tol, int algorithm, igs_result* res) {
+    ARG_CHECK(ctxs && b && res && nranks >= 1, "igs_virtual_solve: bad argument");
+    VGroup* g = ctxs[0] ? ctxs[0]->vgroup : nullptr;
+    ARG_CHECK(g && g->G == nranks, "igs_virtual_solve: not one complete virtual group");
+    for (int r = 0; r < nranks; r++)
+        ARG_CHECK(ctxs[r] == g->members[r] && (b[r] || ctxs[r]->n_local == 0) && (res[r].x || ctxs[r]->n_local == 0),
+                  "igs_virtual_solve: contexts not in rank order / NULL vector");
+    ARG_CHECK(k >= 1 && restart >= 0, "igs_virtual_solve: bad k / restart");
+    CUDA_TRY(cudaSetDevice(ctxs[0]->dev));
+    const int G = nranks;
+    const int m1 = (restart > 0 && restart < k) ? restart : k;
+    const size_t cap = std::max<size_t>((size_t)(m1 + 2) * (m1 + 2), 2 * (size_t)(m1 + 1) + 2);
+    // events and staging (the members' threads only enqueue; nothing here is shared mutably)
+    for (int q = 0; q < 2; q++)
+        while ((int)g->ev_copy[q].size() < G) {
+            cudaEvent_t a, c;
+            CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+            g->ev_copy[q].push_back(a);
+            g->ev_sum[q].push_back(c);
+        }
+    while ((int)g->ev_pack.size() < G) {
+        cudaEvent_t a, c;
+        CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+        g->ev_pack.push_back(a);
+        g->ev_hcopy.push_back(c);
+    }
+    if (!g->d_stage_ptrs) CUDA_TRY(cudaMalloc(&g->d_stage_ptrs, sizeof(double*) * 2 * G));
+    std::vector<const double*> hp(2 * (size_t)G);
+    std::vector<cudaStream_t> saved(G), own(G, nullptr);
+    for (int r = 0; r < G; r++) {
+        igs_ctx* c = ctxs[r];
+        if (c->vstage_cap < cap) {
+            cudaFree(c->d_vstage);
+            c->d_vstage = nullptr;
+            CUDA_TRY(cudaMalloc(&c->d_vstage, sizeof(double) * 2 * cap));
+            c->vstage_cap = cap;
+        }
+        hp[r] = c->d_vstage;
+        hp[(size_t)G + r] = c->d_vstage + c->vstage_cap;
+        c->v_ar_calls = c->v_halo_calls = 0;
+    }
+    CUDA_TRY(cudaMemcpy(g->d_stage_ptrs, hp.data(), sizeof(double*) * 2 * G, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaDeviceSynchronize());
+    for (int r = 0; r < G; r++) {  // every member on its own stream and host thread
+        saved[r] = ctxs[r]->stream;
+        CUDA_TRY(cudaStreamCreateWithFlags(&own[r], cudaStreamNonBlocking));
+        ctxs[r]->stream = own[r];
+        ctxs[r]->vsolve = true;
+    }
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->broken = false;
+        g->arrived = 0;
+        g->timeout_s = ctxs[0]->timeout_s;
+    }
+    std::vector<igs_status> st(G, IGS_OK);
+    std::vector<std::string> msg(G);
+    std::vector<std::thread> th;
+    for (int r = 0; r < G; r++)
+        th.emplace_back([&, r] {
+            cudaSetDevice(ctxs[r]->dev);
+            st[r] = igs_solve_alg(ctxs[r], IGS_MEM_DEVICE, b[r], nullptr, k, restart, tol, algorithm, &res[r]);
+            if (st[r] != IGS_OK) {
+                msg[r] = igs_last_error();
+                g->fail();
+            }
+        });
+    for (auto& t : th) t.join();
+    cudaDeviceSynchronize();
+    for (int r = 0; r < G; r++) {
+        ctxs[r]->stream = saved[r];
+        ctxs[r]->vsolve = false;
+        cudaStreamDestroy(own[r]);
+    }
+    for (int r = 0; r < G; r++)
+        if (st[r] != IGS_OK && msg[r].find("a member failed") == std::string::npos) {
+            set_error("igs_virtual_solve: member " + std::to_string(r) + ": " + msg[r]);
+            return st[r];
+        }
+    for (int r = 0; r < G; r++)
+        if (st[r] != IGS_OK) {
+            set_error("igs_virtual_solve: member " + std::to_string(r) + ": " + msg[r]);
+            return st[r];
+        }
     return IGS_OK;
 }
 

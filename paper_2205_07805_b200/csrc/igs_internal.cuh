@@ -178,5 +178,7 @@ void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, 
 
 // small helpers
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
+// out[i] = sum_q stage[q][i] in member order (igs_virtual_solve's emulated allreduce)
+void launch_rank_sum(const double* const* stage, int G, int64_t count, double* out, cudaStream_t s);
 
 }  // namespace igs

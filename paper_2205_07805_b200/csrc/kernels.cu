@@ -1002,7 +1002,7 @@ __global__ void __launch_bounds__(UP_THREADS)
     if (mode == 0) return;
     const bool want_next = (mode & 2) != 0;
     double* sa = coef;
-    double* sb = coef + p;
+    double* sb = coef + ((p + 1) & ~1);  // 16-B aligned: the column loop reads beta in pairs
     if (HAS_ALPHA)
         for (int j = threadIdx.x; j < p; j += blockDim.x) sa[j] = alpha[j];
     if (want_next)
@@ -1378,7 +1378,7 @@ void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* 
     const int64_t nthreads = (n + 1) / 2;
     const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
     if (blocks == 0) return;
-    const size_t smem = (size_t)(2 * p + 1) * sizeof(double);
+    const size_t smem = (size_t)(((p + 1) & ~1) + p + 1) * sizeof(double);
     const int dmode = 1 | (u_next ? 2 : 0);
     static int na = -1;  // A/B hook IGS_UPDATE_NA: V loads with L1::no_allocate
     if (na < 0) { const char* e = std::getenv("IGS_UPDATE_NA"); na = e ? std::atoi(e) != 0 : 0; }
@@ -2285,6 +2285,22 @@ void launch_pack(int64_t cnt, const int64_t* idx, const double* x, double* buf, 
 __global__ void fill_kernel(double* p, int64_t n, double v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
+}
+
+// out[i] = sum over q = 0..G-1 of stage[q][i], in member order (igs_virtual_solve's
+// emulated allreduce; the same order on every member)
+__global__ void rank_sum_kernel(const double* const* __restrict__ stage, int G, int64_t count,
+                                double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    double s = 0.0;
+    for (int q = 0; q < G; q++) s += stage[q][i];
+    out[i] = s;
+}
+
+void launch_rank_sum(const double* const* stage, int G, int64_t count, double* out, cudaStream_t s) {
+    if (count <= 0) return;
+    rank_sum_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(stage, G, count, out);
 }
 
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {

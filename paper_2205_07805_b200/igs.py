@@ -29,7 +29,7 @@ EXPORTS = ["igs_create", "igs_nccl_unique_id", "igs_workspace_bytes", "igs_bind_
            "igs_last_error", "igs_op_block_dot", "igs_op_spmv", "igs_op_update",
            "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap", "igs_qr",
            "igs_op_basis_diag", "igs_bench_block_dot", "igs_set_timeout", "igs_create_virtual",
-           "igs_virtual_spmv", "igs_info", "igs_bench_update"]
+           "igs_virtual_spmv", "igs_virtual_solve", "igs_info", "igs_bench_update"]
 
 
 class IgsError(RuntimeError):
@@ -72,6 +72,7 @@ def lib() -> ctypes.CDLL:
             "igs_info": [P, I, P],
             "igs_create_virtual": [P, I, I64, P, P, P, I, P, I, P],
             "igs_virtual_spmv": [P, I, P, P, P],
+            "igs_virtual_solve": [P, I, P, I, I, D, I, P],
             "igs_kernel_stats": [P, I, P, P, P],
             "igs_destroy": [P],
             "igs_last_error": [],
@@ -312,6 +313,37 @@ class VirtualGroup:
         py = (ctypes.c_void_p * G)(*[_ptr(t) for t in ys])
         pb = (ctypes.c_void_p * G)(*[_ptr(t) for t in bs]) if bs is not None else None
         _check(lib().igs_virtual_spmv(self._arr, G, px, py, pb), "igs_virtual_spmv")
+
+    def solve(self, bs, xs, *, k: int, restart: int = 0, tol: float = 0.0, algorithm: str = "igs2",
+              want_loo: bool = False) -> list:
+        """All members' igs_solve_alg at once (igs_virtual_solve): bs / xs are per-rank device
+        tensors (rank r's rows); returns one result dict per member (H replicated)."""
+        G = self.G
+        m1 = restart if 0 < restart < k else k
+        res = (igs_result * G)()
+        keep = []
+        for r in range(G):
+            H = np.zeros((m1 + 1) * m1)
+            rh = np.full(k + 1, np.nan)
+            lh = np.full(k + 1, np.nan)
+            keep.append((H, rh, lh))
+            res[r].x = _ptr(xs[r])
+            res[r].H = H.ctypes.data
+            res[r].res_hist = rh.ctypes.data
+            res[r].lnorm_hist = lh.ctypes.data
+            res[r].want_loo = int(want_loo)
+        pb = (ctypes.c_void_p * G)(*[_ptr(t) for t in bs])
+        _check(lib().igs_virtual_solve(self._arr, G, pb, int(k), int(restart), float(tol),
+                                       ALGORITHMS[algorithm], res), "igs_virtual_solve")
+        out = []
+        for r in range(G):
+            H, rh, lh = keep[r]
+            q = res[r]
+            out.append(dict(iters=q.iters, cycles=q.cycles, term=TERM[q.term], true_relres=q.true_relres,
+                            loo=q.loo_frob, h_cols=q.h_cols, basis_cols=q.basis_cols,
+                            allreduces=q.allreduces, reductions=q.reductions,
+                            res_hist=rh[:q.iters + 1], H=H.reshape(m1, m1 + 1).T, m=m1))
+        return out
 
     def stats(self) -> list:
         return [igs_stats(c) for c in self.ctxs]
