@@ -212,8 +212,9 @@ igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value);
 
 /* Failure detection.  With a communicator (nranks > 1, or the 1-rank test
  * communicators), every host wait of igs_create / igs_solve polls ncclCommGetAsyncError and
- * gives up after `seconds` without progress; the fused exchange's device barrier is bounded
- * by the same time.  Either failure aborts the communicator (ncclCommAbort) and returns
+ * gives up after 2 x `seconds` without progress; the fused exchange's device barrier is
+ * bounded by `seconds` (so a peer that stops arriving there is reported as a barrier
+ * timeout, not as a host deadline).  Either failure aborts the communicator (ncclCommAbort) and returns
  * IGS_ERR_NCCL with the reason in igs_last_error(); later solves on the context return
  * IGS_ERR_STATE and only igs_destroy is valid.  Default 120 s (env IGS_NCCL_TIMEOUT_S at
  * create).  Test hook: env IGS_TEST_XCHG_STALL=c makes exchange number c wait for a peer

@@ -143,7 +143,11 @@ struct igs_ctx {
     bool two_fused = true;    // IGS_TWO_FUSED=0: Alg. 2 two-reduce with a separate second block dot
     double two_fused_l2 = 80e6;  // IGS_TWO_FUSED_L2_MB: L2 budget of the fused update + dot
     int pc_ntri = 0;          // IGS_PC_NTRI: forward-substitution CTAs of the persistent kernel (0 = auto)
-    int64_t pc_max_n = 190000;  // crossover vs the graph-replayed per-kernel path
+    // crossover with the graph-replayed per-kernel path, per algorithm (m = 100 and 300,
+    // profiles/r2/pc_crossover.jsonl): Alg. 3 ahead through n = 196249 (1.02 / 1.16), behind
+    // from 262144; IGS(1) ahead through 90000 (1.16 / 1.28), behind from 147456.
+    // IGS_PC_MAX_N overrides both.
+    int64_t pc_max_n = -1;
     int pc_grid = 0;          // IGS_PC_GRID overrides the size heuristic
     int64_t pc_rowsplit_n = 4096;  // IGS_PC_ROWSPLIT_N: row-block dots from this many rows
     int64_t n_pcycle = 0;
@@ -273,7 +277,10 @@ static igs_status wait_for(igs_ctx* ctx, cudaEvent_t ev, cudaStream_t st, const 
             return abort_comm(ctx, std::string(what) + ": NCCL asynchronous error: " + ncclGetErrorString(ar));
         if ((spin & 255u) == 255u) {
             const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            if (el > ctx->timeout_s)
+            // twice the device bound of the exchange barrier (xchg.cuh, timeout_s): a peer that
+            // stops arriving there is reported by the device path ("barrier timeout"); the
+            // host deadline catches what the device cannot see (send/recv, NCCL kernels)
+            if (el > 2.0 * ctx->timeout_s)
                 return abort_comm(ctx, std::string(what) + ": timeout, no progress for " +
                                            std::to_string(ctx->timeout_s) + " s (a peer rank stopped or hung?)");
         }
@@ -1195,7 +1202,7 @@ static igs_status run_cycle_mgs(igs_ctx* ctx, int m, int t0);
 // IGS_ALG_MGS (4).  Algorithms 1 and 3 share the gs = 1 small-step stages.
 static bool use_pcycle(const igs_ctx* ctx, int alg) {
     return ctx->pc_enabled && ctx->nranks == 1 && !ctx->xchg_req && !ctx->force_nccl && ctx->A.n_bnd == 0 &&
-           ctx->n_local <= ctx->pc_max_n &&
+           ctx->n_local <= (ctx->pc_max_n >= 0 ? ctx->pc_max_n : (alg == IGS_ALG_IGS2 ? 210000 : 120000)) &&
            (alg == IGS_ALG_IGS1 || alg == IGS_ALG_IGS2) && ctx->dev_state.m <= 1024;
 }
 

@@ -978,14 +978,7 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
 // ------------------------------------------------------------------------------------
 constexpr int UP_THREADS = 256;
 
-// streaming 16-B load that does not allocate in L1 (each V element is used once here)
-__device__ __forceinline__ double2 ld_stream2(const double* p) {
-    double2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-    return r;
-}
-
-template <bool HAS_ALPHA, bool NA>
+template <bool HAS_ALPHA>
 __global__ void __launch_bounds__(UP_THREADS)
     update_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
                   const double* u, const double* __restrict__ z,
@@ -1020,9 +1013,7 @@ __global__ void __launch_bounds__(UP_THREADS)
             for (; j + 8 <= p; j += 8) {
                 double2 v[8];
 #pragma unroll
-                for (int c = 0; c < 8; c++)
-                    v[c] = NA ? ld_stream2(V + (int64_t)(j + c) * ld + r)
-                              : __ldg(reinterpret_cast<const double2*>(V + (int64_t)(j + c) * ld + r));
+                for (int c = 0; c < 8; c++) v[c] = __ldg(reinterpret_cast<const double2*>(V + (int64_t)(j + c) * ld + r));
 #pragma unroll
                 for (int c = 0; c < 8; c++) {
                     if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
@@ -1380,16 +1371,13 @@ void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* 
     if (blocks == 0) return;
     const size_t smem = (size_t)(((p + 1) & ~1) + p + 1) * sizeof(double);
     const int dmode = 1 | (u_next ? 2 : 0);
-    static int na = -1;  // A/B hook IGS_UPDATE_NA: V loads with L1::no_allocate
-    if (na < 0) { const char* e = std::getenv("IGS_UPDATE_NA"); na = e ? std::atoi(e) != 0 : 0; }
-#define UPD_LAUNCH(A_, N_)                                                                                        \
-    do {                                                                                                          \
-        if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<A_, N_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        update_kernel<A_, N_><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev); \
-    } while (0)
-    if (alpha) { if (na) UPD_LAUNCH(true, true); else UPD_LAUNCH(true, false); }
-    else { if (na) UPD_LAUNCH(false, true); else UPD_LAUNCH(false, false); }
-#undef UPD_LAUNCH
+    if (alpha) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_kernel<true><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
+    } else {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        update_kernel<false><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
+    }
 }
 
 // x += V[:, :p] y   (p = istate[ST_PDONE])

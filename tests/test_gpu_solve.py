@@ -831,15 +831,15 @@ def test_persistent_two_forward_substitution_ctas(P, grid, case, monkeypatch):
     assert a["true_relres"] <= max(10 * pk["true_relres"], 1e-14)
 
 
-@pytest.mark.parametrize("gs", [1, 2])
-@pytest.mark.parametrize("N,m", [(420, 100), (434, 300)])
-def test_persistent_default_threshold_upper_range(P, N, m, gs, monkeypatch):
+@pytest.mark.parametrize("gs,N,m,inside", [(2, 420, 100, True), (2, 443, 300, True), (2, 470, 100, False),
+                                           (1, 300, 100, True), (1, 340, 300, True), (1, 384, 100, False)])
+def test_persistent_default_threshold_upper_range(P, N, m, gs, inside, monkeypatch):
     """The persistent cycle kernel is the default up to the measured crossover with the graph
-    path; this checks the upper end of that range with the DEFAULT threshold (no override):
-    c3-shaped stencils with n = 176,400 and 188,356 rows, cycles of 100 and 300 columns (the
-    long-cycle machinery), both sweeps: the path taken is the one the threshold says, the
-    result matches the oracle at the parity bars and the per-kernel path, bitwise
-    reproducible."""
+    path, per algorithm (profiles/r2/pc_crossover.jsonl: Alg. 3 n <= 210000, IGS(1) n <=
+    120000); this checks both ends of each range with the DEFAULT thresholds (no override):
+    c3-shaped stencils, cycles of 100 and 300 columns (the long-cycle machinery): the path
+    taken is the one the threshold says, the result matches the oracle at the parity bars
+    and the per-kernel path, bitwise reproducible."""
     import torch
     for key in ("IGS_PC_MAX_N", "IGS_PERSIST", "IGS_PC_GRID", "IGS_PC_NTRI"):
         monkeypatch.delenv(key, raising=False)
@@ -854,7 +854,7 @@ def test_persistent_default_threshold_upper_range(P, N, m, gs, monkeypatch):
     pk = s.solve(b, k=m, gs_iters=gs)
     assert s.info()["pcycle_launches"] == 0
     s.close()
-    assert used_pc, prob.A.n_rows   # both sizes are inside the default persistent range
+    assert used_pc == inside, (prob.A.n_rows, used_pc)
     assert g[0]["H"].tobytes() == g[1]["H"].tobytes()
     assert g[0]["iters"] == pk["iters"] == m
     o = oracle.gmres(prob.A, prob.b, m, variant=VARIANT[gs], dot_block=4096)
