@@ -25,35 +25,6 @@
 
 namespace igs {
 
-// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
-// predecessor in the stream drains; every PDL kernel calls pdl_wait() before touching global
-// memory, so only its launch and CTA dispatch overlap the predecessor's tail.  IGS_PDL=0
-// launches normally (A/B hook).
-static bool pdl_on() {
-    static int on = -1;
-    if (on < 0) { const char* e = std::getenv("IGS_PDL"); on = e ? std::atoi(e) != 0 : 1; }
-    return on != 0;
-}
-template <typename... KArgs, typename... Args>
-static void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
-    if (!pdl_on()) {
-        k<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
-        return;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
-}
-
-
 #define FULL_MASK 0xffffffffu
 
 // ------------------------------------------------------------------------------------
@@ -196,8 +167,6 @@ __global__ void __launch_bounds__(SELL_THREADS)
                      const IT* __restrict__ col, const double* __restrict__ val,
                      const double* __restrict__ x, const double* __restrict__ ghost, int64_t nloc,
                      double* __restrict__ y, const double* __restrict__ b, const int* istate, int ahead) {
-    pdl_wait();
-    pdl_trigger();
     if (!running(istate)) return;
     if (ahead > 0 && threadIdx.x == 0) {
         // the CTA that runs about one resident wave later: its values and columns to L2 now
@@ -260,11 +229,11 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
     }
     const IT* ci = static_cast<const IT*>(a.sell_col);
     if (a.ghost) {
-        if (resid) launch_k(spmv_sell_kernel<IT, true, true>, dim3(blocks), dim3(SELL_THREADS), 0, s, a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
-        else launch_k(spmv_sell_kernel<IT, true, false>, dim3(blocks), dim3(SELL_THREADS), 0, s, a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
+        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
+        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
     } else {
-        if (resid) launch_k(spmv_sell_kernel<IT, false, true>, dim3(blocks), dim3(SELL_THREADS), 0, s, a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
-        else launch_k(spmv_sell_kernel<IT, false, false>, dim3(blocks), dim3(SELL_THREADS), 0, s, a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
+        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
+        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
     }
 }
 
@@ -541,8 +510,6 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                     const double* __restrict__ u, const double* __restrict__ z,
                     double* __restrict__ part, double* __restrict__ out, unsigned* counter,
                     const int* istate, const XchgDev* xc) {
-    pdl_wait();
-    pdl_trigger();
     const bool live = running(istate);  // see bdot_kernel
     if (!live && !xc) return;
     extern __shared__ __align__(128) double smem_bt[];
@@ -767,8 +734,6 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                    const double* __restrict__ u, const double* __restrict__ z,
                    double* __restrict__ part, double* __restrict__ out, unsigned* counter,
                    const int* istate, const XchgDev* xc) {
-    pdl_wait();
-    pdl_trigger();
     const bool live = running(istate);  // see bdot_kernel
     if (!live && !xc) return;
     extern __shared__ __align__(128) double smem_sw[];
@@ -976,20 +941,20 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
         if (tg <= grid && p >= sw_min_p && wsmem <= 227 * 1024) {
             if (nv == 2) {
                 cudaFuncSetAttribute(bdot_sw_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
-                launch_k(bdot_sw_kernel<2>, dim3(tg), dim3(BT_THREADS), wsmem, s, n, p, V, ld, u, z, part, out, counter, istate, xc);
+                bdot_sw_kernel<2><<<tg, BT_THREADS, wsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
             } else {
                 cudaFuncSetAttribute(bdot_sw_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
-                launch_k(bdot_sw_kernel<1>, dim3(tg), dim3(BT_THREADS), wsmem, s, n, p, V, ld, u, z, part, out, counter, istate, xc);
+                bdot_sw_kernel<1><<<tg, BT_THREADS, wsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
             }
             return;
         }
         if (tg <= grid) {
             if (nv == 2) {
                 cudaFuncSetAttribute(bdot_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-                launch_k(bdot_tma_kernel<2>, dim3(tg), dim3(BT_THREADS), tsmem, s, n, p, V, ld, u, z, part, out, counter, istate, xc);
+                bdot_tma_kernel<2><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
             } else {
                 cudaFuncSetAttribute(bdot_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-                launch_k(bdot_tma_kernel<1>, dim3(tg), dim3(BT_THREADS), tsmem, s, n, p, V, ld, u, z, part, out, counter, istate, xc);
+                bdot_tma_kernel<1><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
             }
             return;
         }
@@ -1020,8 +985,6 @@ __global__ void __launch_bounds__(UP_THREADS)
                   const double* __restrict__ alpha, const double* __restrict__ beta,
                   const double* __restrict__ gamma_dev, double* v_out, double* u_next,
                   const int* istate, int it, int default_mode, const double* __restrict__ zdiv_dev) {
-    pdl_wait();
-    pdl_trigger();
     extern __shared__ double coef[];  // alpha[p] | beta[p+1]
     int mode = default_mode;
     if (istate) {
@@ -1032,7 +995,7 @@ __global__ void __launch_bounds__(UP_THREADS)
     if (mode == 0) return;
     const bool want_next = (mode & 2) != 0;
     double* sa = coef;
-    double* sb = coef + ((p + 1) & ~1);  // 16-B aligned: the column loop reads beta in pairs
+    double* sb = coef + p;
     if (HAS_ALPHA)
         for (int j = threadIdx.x; j < p; j += blockDim.x) sa[j] = alpha[j];
     if (want_next)
@@ -1406,14 +1369,14 @@ void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* 
     const int64_t nthreads = (n + 1) / 2;
     const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
     if (blocks == 0) return;
-    const size_t smem = (size_t)(((p + 1) & ~1) + p + 1) * sizeof(double);
+    const size_t smem = (size_t)(2 * p + 1) * sizeof(double);
     const int dmode = 1 | (u_next ? 2 : 0);
     if (alpha) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        launch_k(update_kernel<true>, dim3(blocks), dim3(UP_THREADS), smem, s, n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
+        update_kernel<true><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
     } else {
         if (smem > 48 * 1024) cudaFuncSetAttribute(update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        launch_k(update_kernel<false>, dim3(blocks), dim3(UP_THREADS), smem, s, n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
+        update_kernel<false><<<blocks, UP_THREADS, smem, s>>>(n, p, V, ld, u, z, alpha, beta, gamma_dev, v_out, u_next, istate, it, dmode, zdiv_dev);
     }
 }
 
@@ -1985,8 +1948,6 @@ __device__ __forceinline__ void small_body(const Dev& d, int stage, int gs, int 
 
 __global__ void __launch_bounds__(SS_THREADS)
     small_kernel(Dev d, int stage, int gs, int p, int m, int t0_unused) {
-    pdl_wait();
-    pdl_trigger();
     extern __shared__ double sm[];
     __shared__ double red[40];
     small_body(d, stage, gs, p, m, sm, red);
@@ -1997,7 +1958,7 @@ static size_t small_smem(int M) { return (size_t)(7 * (M + 2)) * sizeof(double);
 void launch_small(const Dev& d, int stage, int gs, int p, int m, int t0, cudaStream_t s) {
     const size_t smem = small_smem(d.m);
     if (smem > 48 * 1024) cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_k(small_kernel, dim3(1), dim3(SS_THREADS), smem, s, d, stage, gs, p, m, t0);
+    small_kernel<<<1, SS_THREADS, smem, s>>>(d, stage, gs, p, m, t0);
 }
 
 // ------------------------------------------------------------------------------------
