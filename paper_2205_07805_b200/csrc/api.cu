@@ -162,6 +162,8 @@ struct igs_ctx {
     // G > 1 with SELL: rows touching ghost columns run after the halo, the rest during it
     int64_t* d_bnd_rows = nullptr;
     cudaStream_t hstream = nullptr;  // halo exchange stream
+    cudaStream_t cstream = nullptr;  // host-vector solves: D2H of x chunks behind the last x update
+    cudaEvent_t ev_xc[8] = {};
     cudaEvent_t ev_x = nullptr, ev_h = nullptr;
     // fused block dot + allreduce over NVLink (IGS_XCHG=1): NCCL symmetric window + device comm
     bool xchg_req = false;
@@ -500,6 +502,8 @@ static void free_ctx(igs_ctx* c) {
     cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col); cudaFree(c->d_vstage);
     cudaFree(c->d_bnd_rows);
     if (c->hstream) cudaStreamDestroy(c->hstream);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
+    for (cudaEvent_t e : c->ev_xc) if (e) cudaEventDestroy(e);
     if (c->ev_x) cudaEventDestroy(c->ev_x);
     if (c->ev_h) cudaEventDestroy(c->ev_h);
     cudaFree(c->d_gram);
@@ -1644,7 +1648,7 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         CUDA_TRY(cudaMemcpyAsync(dsc, hs, sizeof(hs), cudaMemcpyHostToDevice, st));
     }
     int total = 0, cycles = 0, last_basis = 0;
-    bool breakdown = false;
+    bool breakdown = false, x_sent = false;
     double rn = 0.0;
     for (;;) {
         // r = b - A x into z (not V[:,0]: the final basis must survive for the LOO
@@ -1686,8 +1690,32 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
         }
         // y = argmin ||rho e1 - H y|| ; x += V_p y
         TIMED(IGS_K_CYCLE, 0.0, launch_small(d, SS_LSQ, gs_iters, 0, m, total, st));
-        TIMED(IGS_K_CYCLE, 8.0 * n * p + 16.0 * n,
-              launch_xupdate(n, ctx->d_V, ctx->ldv, d.y, dx, d.istate, m, st));
+        // host vectors, and this cycle is the last (it runs to k: the loop ends after the
+        // residual below): x += V_p y in 8 row chunks, each chunk's D2H on a copy stream
+        // behind its update, so the PCIe copy of x overlaps the rest of the update
+        const bool last_host = hostv && !ctx->timing && ctx->nranks == 1 && total + p >= k &&
+                               status != STOP_BREAKDOWN && n >= 8 * 4096;
+        if (last_host) {
+            if (!ctx->cstream) {
+                CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+                for (cudaEvent_t& e : ctx->ev_xc) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            }
+            const int64_t ch = round_up((n + 7) / 8, 256);
+            for (int c = 0; c < 8; c++) {
+                const int64_t r0 = (int64_t)c * ch, r1 = std::min<int64_t>(n, r0 + ch);
+                if (r1 <= r0) break;
+                launch_xupdate(r1 - r0, ctx->d_V + r0, ctx->ldv, d.y, dx + r0, d.istate, m, st);
+                CUDA_TRY(cudaEventRecord(ctx->ev_xc[c], st));
+                CUDA_TRY(cudaStreamWaitEvent(ctx->cstream, ctx->ev_xc[c], 0));
+                CUDA_TRY(cudaMemcpyAsync(res->x + r0, dx + r0, sizeof(double) * (r1 - r0), cudaMemcpyDeviceToHost,
+                                         ctx->cstream));
+            }
+            CUDA_TRY(cudaGetLastError());
+            x_sent = true;
+        } else {
+            TIMED(IGS_K_CYCLE, 8.0 * n * p + 16.0 * n,
+                  launch_xupdate(n, ctx->d_V, ctx->ldv, d.y, dx, d.istate, m, st));
+        }
         total += p;
         cycles++;
         last_basis = istate[ST_BASIS];
@@ -1735,8 +1763,9 @@ extern "C" igs_status igs_solve_alg(igs_ctx* ctx, igs_mem vec_mem, const double*
             res->sigma_min = sd[1];
         }
     }
-    if (hostv) CUDA_TRY(cudaMemcpyAsync(res->x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    if (hostv && !x_sent) CUDA_TRY(cudaMemcpyAsync(res->x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     TRY(wait_for(ctx, nullptr, st, "igs_solve"));
+    if (x_sent) CUDA_TRY(cudaStreamSynchronize(ctx->cstream));
     CUDA_TRY(cudaGetLastError());
     if (res->res_hist) std::memcpy(res->res_hist, hres.data(), sizeof(double) * (total + 1));
     if (res->lnorm_hist) {

@@ -174,6 +174,23 @@ def test_host_and_device_paths_identical(P):
     s.close()
 
 
+@pytest.mark.parametrize("N,k,restart", [(200, 60, 0), (200, 130, 50), (256, 40, 0)])
+def test_host_vectors_chunked_last_update(P, N, k, restart):
+    """Host b / x (the e2e path): the last cycle's x update runs in row chunks with each
+    chunk's D2H behind it on a copy stream (n >= 32768); x must be bitwise the device path's
+    -- unrestarted, and restarted with a short last cycle (130 = 50 + 50 + 30), with a ragged
+    last chunk (n = 40000)."""
+    import torch
+    prob = W.config("c3", N=N)
+    s = P.Solver(prob.A)
+    gd = s.solve(torch.from_numpy(prob.b).cuda(), k=k, restart=restart, gs_iters=2)
+    gh = s.solve(prob.b.copy(), k=k, restart=restart, gs_iters=2)
+    s.close()
+    assert gd["iters"] == gh["iters"] == k and gd["cycles"] == gh["cycles"]
+    assert gd["x"].cpu().numpy().tobytes() == gh["x"].tobytes()
+    assert gd["true_relres"] == gh["true_relres"]
+
+
 def test_x0_restart_resume(P):
     import torch
     prob = W.config("c4", N=16)
