@@ -566,6 +566,27 @@ def test_fused_block_dot_allreduce_one_rank(P, cfg, alg, monkeypatch):
         assert 0 < g["reductions"] <= g["allreduces"] and u["allreduces"] == 0
 
 
+@pytest.mark.parametrize("alg", ["igs2", "igs1"])
+def test_fused_exchange_column_sweep_block_dot(P, alg, monkeypatch):
+    """The column-sweep block dot (p >= 96) finishing through the fused exchange (IGS_XCHG=1,
+    1-rank communicator): a 120-column cycle on c3's operator at 160^2 crosses the switch from
+    the tile kernel; same bits as the plain path, one exchange per reduction."""
+    import torch
+    prob = W.config("c3", N=160)
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for x in ("1", "0"):
+        monkeypatch.setenv("IGS_XCHG", x)
+        monkeypatch.setenv("IGS_PERSIST", "0")
+        s = P.Solver(prob.A)
+        outs[x] = s.solve(b, k=120, restart=0, tol=0.0, algorithm=alg)
+        s.close()
+    g, u = outs["1"], outs["0"]
+    assert g["iters"] == u["iters"] == 120 and g["H"].tobytes() == u["H"].tobytes()
+    assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+    assert 0 < g["reductions"] <= g["allreduces"] and u["allreduces"] == 0
+
+
 def test_basis_diagnostics_simoncini(P):
     """P:1274-1283 on the device: after 98 iterations on the Simoncini matrix MGS has lost
     orthogonality (||S_k||_2 -> 1, sigma_min(V) -> 0) while the two-sweep IGS keeps
