@@ -326,6 +326,10 @@ def run_ours(args, rank, world, local) -> int:
     # ---- preflight (N > 1): the first cycle runs the collective path end to end; if any rank
     # fails (e.g. the fused NVLink exchange times out), every rank rebuilds on ncclAllReduce
     path_note = None
+    if world > 1:
+        # a peer that never arrives at the fused exchange's barrier fails the preflight in
+        # seconds (device bound 20 s, host deadline 40 s), not after the 120 s default
+        solver.set_timeout(20.0)
     try:
         r = step_dev()
         ok = r["iters"] == M
@@ -344,6 +348,8 @@ def run_ours(args, rank, world, local) -> int:
         path_note = path_note or "a peer rank failed the preflight"
         r = step_dev()
         assert r["iters"] == M, r
+    if world > 1:
+        solver.set_timeout(120.0)
     info = solver.info()
     # replicated k x k state must be bit-identical on every rank
     replicated_ok = None
