@@ -207,6 +207,33 @@ def test_graph_capture_with_collectives_one_rank(P, mode, alg, monkeypatch):
         assert g["allreduces"] >= g["reductions"] > 0
 
 
+@pytest.mark.parametrize("mode", ["xchg", "nccl"])
+def test_graph_capture_split_spmv_one_rank(P, mode, monkeypatch):
+    """The G > 1 SpMV split inside a captured cycle: IGS_TEST_BND_EVERY routes every 7th row
+    through the boundary pass, so each SpMV forks to the halo stream and joins back (event
+    record / wait inside the capture) around the interior rows, with the exchange kernels or
+    ncclAllReduce captured too (1-rank communicator).  Bitwise the plain graph-less path."""
+    import torch
+    prob = W.config("c4", N=40)
+    b = torch.from_numpy(prob.b).cuda()
+    outs = {}
+    for variant in ("comm", "plain"):
+        monkeypatch.setenv("IGS_PERSIST", "0")
+        monkeypatch.setenv("IGS_XCHG", "1" if variant == "comm" and mode == "xchg" else "0")
+        monkeypatch.setenv("IGS_FORCE_NCCL", "1" if variant == "comm" and mode == "nccl" else "0")
+        monkeypatch.setenv("IGS_GRAPHS", "1" if variant == "comm" else "0")
+        monkeypatch.setenv("IGS_TEST_BND_EVERY", "7" if variant == "comm" else "0")
+        s = P.Solver(prob.A)
+        outs[variant] = s.solve(b, k=120, restart=50, tol=1e-11, algorithm="igs2")
+        info = s.info()
+        s.close()
+        if variant == "comm":
+            assert info["graph_launches"] > 0 and info["n_bnd"] > 0, info
+    g, u = outs["comm"], outs["plain"]
+    assert g["iters"] == u["iters"] and g["cycles"] == u["cycles"] and g["H"].tobytes() == u["H"].tobytes()
+    assert g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+
+
 # ------------------------------------------------------------------ G > 1 solve, one device
 def _virtual_solve(P, prob, bounds, **kw):
     import torch
