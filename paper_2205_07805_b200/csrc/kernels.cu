@@ -1003,48 +1003,66 @@ __global__ void __launch_bounds__(UP_THREADS)
     __syncthreads();
     const double gamma = *gamma_dev;
     const double zdiv = zdiv_dev ? *zdiv_dev : gamma;  // z / gamma (Arnoldi) or z / 1 (QR)
-    const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
-    if (r >= n) return;
-    const bool pair = (r + 1 < n);
-    double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
-    if (HAS_ALPHA || want_next) {
-        int j = 0;
-        if (pair) {
-            for (; j + 8 <= p; j += 8) {
-                double2 v[8];
+    // grid-stride over 2 * blockDim-row tiles (the grid is at most a few waves: the prologue
+    // above -- mode word, coefficients, gamma -- is paid once per CTA, not once per tile)
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; r < n;
+         r += (int64_t)gridDim.x * blockDim.x * 2) {
+        const bool pair = (r + 1 < n);
+        // u and z first: their latency overlaps the column loop
+        const double2 uu = ld2_guard(u, r, n);
+        const double2 zz = want_next ? ld2_guard(z, r, n) : make_double2(0.0, 0.0);
+        double2 t1 = make_double2(0.0, 0.0), t2 = make_double2(0.0, 0.0);
+        if (HAS_ALPHA || want_next) {
+            int j = 0;
+            if (pair) {
+                for (; j + 8 <= p; j += 8) {
+                    double2 v[8];
 #pragma unroll
-                for (int c = 0; c < 8; c++) v[c] = __ldg(reinterpret_cast<const double2*>(V + (int64_t)(j + c) * ld + r));
+                    for (int c = 0; c < 8; c++) v[c] = __ldg(reinterpret_cast<const double2*>(V + (int64_t)(j + c) * ld + r));
 #pragma unroll
-                for (int c = 0; c < 8; c++) {
-                    if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
-                    if (want_next) { t2.x = fma(v[c].x, sb[j + c], t2.x); t2.y = fma(v[c].y, sb[j + c], t2.y); }
+                    for (int c = 0; c < 8; c++) {
+                        if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
+                        if (want_next) { t2.x = fma(v[c].x, sb[j + c], t2.x); t2.y = fma(v[c].y, sb[j + c], t2.y); }
+                    }
+                }
+                if (j < p) {  // the last p mod 8 columns: loads issued together, then the FMAs in order
+                    double2 v[8];
+#pragma unroll
+                    for (int c = 0; c < 8; c++)
+                        v[c] = (j + c < p) ? __ldg(reinterpret_cast<const double2*>(V + (int64_t)(j + c) * ld + r))
+                                           : make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {
+                        if (j + c >= p) break;
+                        if (HAS_ALPHA) { t1.x = fma(v[c].x, sa[j + c], t1.x); t1.y = fma(v[c].y, sa[j + c], t1.y); }
+                        if (want_next) { t2.x = fma(v[c].x, sb[j + c], t2.x); t2.y = fma(v[c].y, sb[j + c], t2.y); }
+                    }
+                    j = p;
                 }
             }
+            for (; j < p; j++) {
+                const double2 v = ld2_guard(V + (int64_t)j * ld, r, n);
+                if (HAS_ALPHA) { t1.x = fma(v.x, sa[j], t1.x); t1.y = fma(v.y, sa[j], t1.y); }
+                if (want_next) { t2.x = fma(v.x, sb[j], t2.x); t2.y = fma(v.y, sb[j], t2.y); }
+            }
         }
-        for (; j < p; j++) {
-            const double2 v = ld2_guard(V + (int64_t)j * ld, r, n);
-            if (HAS_ALPHA) { t1.x = fma(v.x, sa[j], t1.x); t1.y = fma(v.y, sa[j], t1.y); }
-            if (want_next) { t2.x = fma(v.x, sb[j], t2.x); t2.y = fma(v.y, sb[j], t2.y); }
+        double2 w = uu;
+        if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
+        double2 v;
+        v.x = w.x / gamma;
+        v.y = w.y / gamma;
+        if (want_next) {
+            const double bp = sb[p];
+            double2 un;
+            un.x = zz.x / zdiv - fma(v.x, bp, t2.x);
+            un.y = zz.y / zdiv - fma(v.y, bp, t2.y);
+            u_next[r] = un.x;
+            if (pair) u_next[r + 1] = un.y;
         }
-    }
-    const double2 uu = ld2_guard(u, r, n);
-    double2 w = uu;
-    if (HAS_ALPHA) { w.x = uu.x - t1.x; w.y = uu.y - t1.y; }
-    double2 v;
-    v.x = w.x / gamma;
-    v.y = w.y / gamma;
-    if (want_next) {
-        const double2 zz = ld2_guard(z, r, n);
-        const double bp = sb[p];
-        double2 un;
-        un.x = zz.x / zdiv - fma(v.x, bp, t2.x);
-        un.y = zz.y / zdiv - fma(v.y, bp, t2.y);
-        u_next[r] = un.x;
-        if (pair) u_next[r + 1] = un.y;
-    }
-    if (mode & 1) {
-        v_out[r] = v.x;
-        if (pair) v_out[r + 1] = v.y;
+        if (mode & 1) {
+            v_out[r] = v.x;
+            if (pair) v_out[r + 1] = v.y;
+        }
     }
 }
 
@@ -1367,8 +1385,18 @@ void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* 
                    const double* gamma_dev, double* v_out, double* u_next, const int* istate,
                    int it, cudaStream_t s, const double* zdiv_dev) {
     const int64_t nthreads = (n + 1) / 2;
-    const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
+    unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
     if (blocks == 0) return;
+    static int cap = -1;  // resident CTAs: 4 per SM (64 registers x 256 threads); IGS_UPDATE_WAVES
+    if (cap < 0) {        // (A/B hook) sets how many resident waves the grid may span
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char* e = std::getenv("IGS_UPDATE_WAVES");
+        const int waves = e ? std::max(1, std::atoi(e)) : 1;
+        cap = (int)std::min<int64_t>((int64_t)sms * 4 * waves, 1 << 30);
+    }
+    if (blocks > (unsigned)cap) blocks = (unsigned)cap;
     const size_t smem = (size_t)(2 * p + 1) * sizeof(double);
     const int dmode = 1 | (u_next ? 2 : 0);
     if (alpha) {
