@@ -1003,8 +1003,7 @@ __global__ void __launch_bounds__(UP_THREADS)
     __syncthreads();
     const double gamma = *gamma_dev;
     const double zdiv = zdiv_dev ? *zdiv_dev : gamma;  // z / gamma (Arnoldi) or z / 1 (QR)
-    // grid-stride over 2 * blockDim-row tiles (the grid is at most a few waves: the prologue
-    // above -- mode word, coefficients, gamma -- is paid once per CTA, not once per tile)
+    // grid-stride form; launch_update gives every CTA one tile
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; r < n;
          r += (int64_t)gridDim.x * blockDim.x * 2) {
         const bool pair = (r + 1 < n);
@@ -1385,18 +1384,10 @@ void launch_update(int64_t n, int p, const double* V, int64_t ld, const double* 
                    const double* gamma_dev, double* v_out, double* u_next, const int* istate,
                    int it, cudaStream_t s, const double* zdiv_dev) {
     const int64_t nthreads = (n + 1) / 2;
-    unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
+    // one 512-row tile per CTA: capping the grid at the resident CTAs (grid-stride, prologue
+    // once per CTA) measured slower beyond p ~ 10 (c4 399.5 vs 403.7 it/s)
+    const unsigned blocks = (unsigned)((nthreads + UP_THREADS - 1) / UP_THREADS);
     if (blocks == 0) return;
-    static int cap = -1;  // resident CTAs: 4 per SM (64 registers x 256 threads); IGS_UPDATE_WAVES
-    if (cap < 0) {        // (A/B hook) sets how many resident waves the grid may span
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char* e = std::getenv("IGS_UPDATE_WAVES");
-        const int waves = e ? std::max(1, std::atoi(e)) : 1;
-        cap = (int)std::min<int64_t>((int64_t)sms * 4 * waves, 1 << 30);
-    }
-    if (blocks > (unsigned)cap) blocks = (unsigned)cap;
     const size_t smem = (size_t)(2 * p + 1) * sizeof(double);
     const int dmode = 1 | (u_next ? 2 : 0);
     if (alpha) {
