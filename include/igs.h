@@ -206,7 +206,9 @@ typedef enum {
     IGS_INFO_GRAPH_LAUNCHES = 6,   /* restart cycles replayed from CUDA graphs              */
     IGS_INFO_PCYCLE_LAUNCHES = 7,  /* restart cycles run by the persistent kernel           */
     IGS_INFO_SELL = 8,             /* 1: the SpMV uses the SELL-32 copy of A               */
-    IGS_INFO_CSR_COMPACT = 9       /* 1: the CSR arrays hold only the boundary rows         */
+    IGS_INFO_CSR_COMPACT = 9,      /* 1: the CSR arrays hold only the boundary rows         */
+    IGS_INFO_SELL_DIAG_SLICES = 10 /* SELL slices stored as diagonal offsets (no column
+                                      indices)                                */
 } igs_info_key;
 igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value);
 

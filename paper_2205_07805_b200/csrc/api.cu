@@ -158,7 +158,10 @@ struct igs_ctx {
     uint8_t* d_sell_len = nullptr;
     double* d_sell_val = nullptr;
     void* d_sell_col = nullptr;
-    int64_t sell_entries = 0;
+    int64_t* d_sell_cptr = nullptr;
+    int32_t* d_sell_diag = nullptr;
+    uint8_t* d_sell_mask = nullptr;
+    int64_t sell_entries = 0, sell_diag_slices = 0;
     // G > 1 with SELL: rows touching ghost columns run after the halo, the rest during it
     int64_t* d_bnd_rows = nullptr;
     cudaStream_t hstream = nullptr;  // halo exchange stream
@@ -499,7 +502,8 @@ static void free_ctx(igs_ctx* c) {
     if (c->owns_ws) { cudaFree(c->d_V); }
     cudaFree(c->d_z); cudaFree(c->d_b); cudaFree(c->d_x);
     cudaFree(c->d_small); cudaFree(c->d_int); cudaFree(c->d_part); cudaFree(c->d_counter); cudaFree(c->d_pcprof);
-    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col); cudaFree(c->d_vstage);
+    cudaFree(c->d_sell_ptr); cudaFree(c->d_sell_len); cudaFree(c->d_sell_val); cudaFree(c->d_sell_col);
+    cudaFree(c->d_sell_cptr); cudaFree(c->d_sell_diag); cudaFree(c->d_sell_mask); cudaFree(c->d_vstage);
     cudaFree(c->d_bnd_rows);
     if (c->hstream) cudaStreamDestroy(c->hstream);
     if (c->cstream) cudaStreamDestroy(c->cstream);
@@ -556,14 +560,63 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
         sp[(size_t)s + 1] = sp[(size_t)s] + 32 * mx;
     }
     const int64_t tot = std::max<int64_t>(sp[(size_t)ns], 1);
+    // diagonal slices: every column local, each row's offsets c - r strictly
+    // increasing in CSR order (so the row's order is the slice list's order), at most 8
+    // distinct offsets in the slice.  Test hook IGS_SELL_DIAG=0 keeps every slice explicit.
+    const char* edg = std::getenv("IGS_SELL_DIAG");
+    const bool want_diag = !(edg && std::atoi(edg) == 0);
+    std::vector<int64_t> cp((size_t)ns, 0);
+    std::vector<int32_t> dg((size_t)ns * 8, 0);
+    std::vector<uint8_t> mk((size_t)n, 0);
+    int64_t ctot = 0, ndiag = 0;
+    for (int64_t s = 0; s < ns; s++) {
+        const int64_t r0 = 32 * s, r1 = std::min<int64_t>(n, r0 + 32);
+        bool ok = want_diag;
+        int64_t D[8];
+        int nd = 0;
+        for (int64_t r = r0; r < r1 && ok; r++) {
+            if (len[(size_t)r] == SELL_BOUNDARY) continue;
+            int64_t prev = INT64_MIN;
+            for (int64_t q = rowptr[r]; q < rowptr[r + 1] && ok; q++) {
+                const int64_t c = local_col[(size_t)q], o = c - r;
+                if (c < 0 || c >= n || o <= prev || o > INT32_MAX || o < INT32_MIN) { ok = false; break; }
+                prev = o;
+                bool seen = false;
+                for (int i = 0; i < nd; i++) seen = seen || D[i] == o;
+                if (!seen) {
+                    if (nd == 8) { ok = false; break; }
+                    D[nd++] = o;
+                }
+            }
+        }
+        if (ok) {
+            std::sort(D, D + nd);
+            for (int i = 0; i < nd; i++) dg[(size_t)s * 8 + i] = (int32_t)D[i];
+            for (int64_t r = r0; r < r1; r++) {
+                if (len[(size_t)r] == SELL_BOUNDARY) continue;
+                unsigned m = 0;
+                for (int64_t q = rowptr[r]; q < rowptr[r + 1]; q++) {
+                    const int64_t o = local_col[(size_t)q] - r;
+                    m |= 1u << (int)(std::lower_bound(D, D + nd, o) - D);
+                }
+                mk[(size_t)r] = (uint8_t)m;
+            }
+            cp[(size_t)s] = -1;
+            ndiag++;
+        } else {
+            cp[(size_t)s] = ctot;
+            ctot += sp[(size_t)s + 1] - sp[(size_t)s];
+        }
+    }
     std::vector<double> sv((size_t)tot, 0.0);
-    std::vector<char> sc((size_t)tot * (idx64 ? 8 : 4), 0);
+    std::vector<char> sc((size_t)std::max<int64_t>(ctot, 1) * (idx64 ? 8 : 4), 0);
     for (int64_t r = 0; r < n; r++) {
         if (len[(size_t)r] == SELL_BOUNDARY) continue;
-        const int64_t base = sp[(size_t)(r >> 5)] + (r & 31);
+        const int64_t base = sp[(size_t)(r >> 5)] + (r & 31), cb = cp[(size_t)(r >> 5)] + (r & 31);
         for (int64_t q = rowptr[r], k = 0; q < rowptr[r + 1]; q++, k++) {
-            const int64_t at = base + 32 * k;
-            sv[(size_t)at] = values[q];
+            sv[(size_t)(base + 32 * k)] = values[q];
+            if (cp[(size_t)(r >> 5)] < 0) continue;
+            const int64_t at = cb + 32 * k;
             if (idx64) reinterpret_cast<int64_t*>(sc.data())[at] = local_col[(size_t)q];
             else reinterpret_cast<int32_t*>(sc.data())[at] = (int32_t)local_col[(size_t)q];
         }
@@ -572,14 +625,24 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     CUDA_TRY(cudaMalloc(&ctx->d_sell_len, len.size()));
     CUDA_TRY(cudaMalloc(&ctx->d_sell_val, sizeof(double) * sv.size()));
     CUDA_TRY(cudaMalloc(&ctx->d_sell_col, sc.size()));
+    CUDA_TRY(cudaMalloc(&ctx->d_sell_cptr, sizeof(int64_t) * cp.size()));
+    CUDA_TRY(cudaMalloc(&ctx->d_sell_diag, sizeof(int32_t) * dg.size()));
+    CUDA_TRY(cudaMalloc(&ctx->d_sell_mask, mk.size()));
     CUDA_TRY(cudaMemcpy(ctx->d_sell_ptr, sp.data(), sizeof(int64_t) * sp.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(ctx->d_sell_len, len.data(), len.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(ctx->d_sell_val, sv.data(), sizeof(double) * sv.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(ctx->d_sell_col, sc.data(), sc.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->d_sell_cptr, cp.data(), sizeof(int64_t) * cp.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->d_sell_diag, dg.data(), sizeof(int32_t) * dg.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->d_sell_mask, mk.data(), mk.size(), cudaMemcpyHostToDevice));
     ctx->A.sell_ptr = ctx->d_sell_ptr;
     ctx->A.sell_len = ctx->d_sell_len;
     ctx->A.sell_val = ctx->d_sell_val;
     ctx->A.sell_col = ctx->d_sell_col;
+    ctx->A.sell_cptr = ctx->d_sell_cptr;
+    ctx->A.sell_diag = ctx->d_sell_diag;
+    ctx->A.sell_mask = ctx->d_sell_mask;
+    ctx->sell_diag_slices = ndiag;
     ctx->sell_entries = tot;
     if (!bnd.empty()) {
         CUDA_TRY(cudaMalloc(&ctx->d_bnd_rows, sizeof(int64_t) * bnd.size()));
@@ -1966,6 +2029,7 @@ extern "C" igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value) {
         case IGS_INFO_PCYCLE_LAUNCHES: *value = ctx->n_pcycle; break;
         case IGS_INFO_SELL: *value = ctx->A.sell_ptr != nullptr; break;
         case IGS_INFO_CSR_COMPACT: *value = ctx->csr_compact; break;
+        case IGS_INFO_SELL_DIAG_SLICES: *value = ctx->sell_diag_slices; break;
         default: ARG_CHECK(false, "igs_info: unknown key");
     }
     return IGS_OK;

@@ -70,6 +70,14 @@ struct SpmvArgs {
     const uint8_t* sell_len = nullptr;  // [nrows] nonzeros of each row (<= 255)
     const double* sell_val = nullptr;
     const void* sell_col = nullptr;     // int32 or int64 (idx64), local column space
+    // Diagonal slices: a slice whose rows use at most 8 distinct offsets
+    // c - r (all columns local), each row's offsets strictly increasing in CSR order, keeps
+    // no column indices: slice s lists its offsets in sell_diag[8s..8s+7] (ascending) and row
+    // r's k-th entry has column r + sell_diag[8s + (k-th set bit of sell_mask[r])].  Other
+    // slices store entry k of row 32s+l at sell_col[sell_cptr[s] + 32k + l].
+    const int64_t* sell_cptr = nullptr;  // [nslices]: column offset of a slice, -1 = diagonal
+    const int32_t* sell_diag = nullptr;  // [nslices * 8]
+    const uint8_t* sell_mask = nullptr;  // [nrows]
     // G > 1: rows with a ghost column (sell_len == SELL_BOUNDARY, not in the SELL arrays),
     // multiplied by launch_spmv_rows once the halo has arrived.  With a SELL copy the CSR
     // arrays above hold only these rows (row t of the compact CSR is row bnd_rows[t])

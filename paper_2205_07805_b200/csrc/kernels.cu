@@ -152,63 +152,131 @@ __global__ void __launch_bounds__(SPS_THREADS)
 }
 
 // ------------------------------------------------------------------------------------
-// K1 (default for short rows): SELL-32.  One thread per row; the k-th nonzero of the 32
-// rows of a slice are 32 consecutive entries, so the column / value loads of a warp are
-// fully coalesced and, for stencil rows, the x gathers of a warp are one contiguous range
-// per k.  No shared memory, no barrier.  The row is summed left to right in CSR order with
-// separate multiply and add (bitwise equal to the oracle's row loop, like the CSR-stream
-// kernel).  8 entries per batch are loaded before use (memory-level parallelism).
+// K1 (default for short rows): the SELL-32 copy of A, with diagonal slices
 // ------------------------------------------------------------------------------------
 constexpr int SELL_THREADS = 256;
 
+// The SELL-32 arrays as the kernels see them (SpmvArgs, igs_internal.cuh).
+template <typename IT>
+struct SellDev {
+    const int64_t* __restrict__ ptr;   // [nslices + 1] value offset of slice s
+    const int64_t* __restrict__ cptr;  // [nslices] column offset, -1: diagonal slice
+    const int32_t* __restrict__ diag;  // [nslices * 8] offsets of a diagonal slice, ascending
+    const uint8_t* __restrict__ len;   // [nrows]
+    const uint8_t* __restrict__ mask;  // [nrows] offsets a row of a diagonal slice uses
+    const IT* __restrict__ col;
+    const double* __restrict__ val;
+};
+
+template <typename IT>
+static SellDev<IT> sell_dev(const SpmvArgs& a) {
+    return SellDev<IT>{a.sell_ptr, a.sell_cptr, a.sell_diag, a.sell_len, a.sell_mask,
+                       static_cast<const IT*>(a.sell_col), a.sell_val};
+}
+
+template <bool CG>
+__device__ __forceinline__ double ldx(const double* p) {
+    if (CG) return __ldcg(p);  // written earlier in the same launch (persistent kernel)
+    return __ldg(p);
+}
+
+// Row r of the SELL-32 copy, summed left to right in the row's CSR order with separate
+// multiply and add (bitwise the oracle's row loop).  Called by all 32 lanes of a warp for
+// the 32 rows of slice r >> 5 (rows >= nrows pass valid = false).  In a diagonal slice the
+// column of entry k is r + offset, the offset taken from the slice's list by a shuffle (no
+// column index is read: 4 or 8 bytes less per nonzero, and the x gathers no longer wait
+// for a column load).  Returns false for rows it must not store (past the end, boundary).
+template <typename IT, bool GHOST, bool CG>
+__device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool valid, const double* __restrict__ x,
+                                         const double* __restrict__ ghost, int64_t nloc, double& out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t s = r >> 5;
+    int len = valid ? (int)__ldg(A.len + r) : 0;
+    const bool bnd = (len == SELL_BOUNDARY);  // G > 1 boundary row: launch_spmv_rows, after the halo
+    if (bnd) len = 0;
+    const int64_t base = __ldg(A.ptr + s) + (r & 31);
+    const int64_t cb = A.cptr ? __ldg(A.cptr + s) : 0;
+    double sum = 0.0;
+    if (cb < 0) {  // diagonal slice (warp-uniform branch)
+        const int dl = __ldg(A.diag + 8 * s + (lane & 7));
+        unsigned m = valid ? (unsigned)__ldg(A.mask + r) : 0u;
+        int64_t cc[8];
+        double vv[8], xv[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            cc[k] = r + __shfl_sync(FULL_MASK, dl, bit & 7);
+            vv[k] = k < len ? __ldg(A.val + base + 32 * k) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) xv[k] = k < len ? ldx<CG>(x + cc[k]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            if (k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
+    } else {
+        const int64_t cbase = cb + (r & 31);
+        for (int k0 = 0; k0 < len; k0 += 8) {
+            IT cc[8];
+            double vv[8], xv[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const bool in = k0 + k < len;
+                cc[k] = in ? __ldg(A.col + cbase + 32 * (int64_t)(k0 + k)) : (IT)0;
+                vv[k] = in ? __ldg(A.val + base + 32 * (int64_t)(k0 + k)) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                if (k0 + k < len) {
+                    if (GHOST && (int64_t)cc[k] >= nloc) xv[k] = __ldg(ghost + ((int64_t)cc[k] - nloc));
+                    else xv[k] = ldx<CG>(x + (int64_t)cc[k]);
+                } else {
+                    xv[k] = 0.0;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (k0 + k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
+        }
+    }
+    out = sum;
+    return valid && !bnd;
+}
+
+// K1 (default for short rows): SELL-32.  One thread per row; the k-th nonzero of the 32
+// rows of a slice are 32 consecutive entries, so the value (and column) loads of a warp
+// are fully coalesced and, for stencil rows, the x gathers of a warp are one contiguous
+// range per k.  No shared memory, no barrier.  8 entries per batch are loaded before use
+// (memory-level parallelism).
 template <typename IT, bool GHOST, bool RESID>
 __global__ void __launch_bounds__(SELL_THREADS)
-    spmv_sell_kernel(int64_t nrows, const int64_t* __restrict__ sptr, const uint8_t* __restrict__ slen,
-                     const IT* __restrict__ col, const double* __restrict__ val,
-                     const double* __restrict__ x, const double* __restrict__ ghost, int64_t nloc,
-                     double* __restrict__ y, const double* __restrict__ b, const int* istate, int ahead) {
+    spmv_sell_kernel(int64_t nrows, SellDev<IT> A, const double* __restrict__ x, const double* __restrict__ ghost,
+                     int64_t nloc, double* __restrict__ y, const double* __restrict__ b, const int* istate,
+                     int ahead) {
     if (!running(istate)) return;
     if (ahead > 0 && threadIdx.x == 0) {
-        // the CTA that runs about one resident wave later: its values and columns to L2 now
+        // the CTA that runs about one resident wave later: its values (and columns) to L2 now
         const int64_t nb = (int64_t)gridDim.x, fb = (int64_t)blockIdx.x + ahead;
         if (fb < nb) {
             const int64_t ns = (nrows + 31) / 32;
             const int64_t s0 = fb * (SELL_THREADS / 32), s1 = min(s0 + SELL_THREADS / 32, ns);
-            const int64_t e0 = __ldg(sptr + s0), e1 = __ldg(sptr + s1);
-            if (e1 > e0) {
-                bulk_prefetch_l2(val + e0, (uint32_t)((e1 - e0) * sizeof(double)));
-                bulk_prefetch_l2(col + e0, (uint32_t)((e1 - e0) * sizeof(IT)));
+            const int64_t e0 = __ldg(A.ptr + s0), e1 = __ldg(A.ptr + s1);
+            if (e1 > e0) bulk_prefetch_l2(A.val + e0, (uint32_t)((e1 - e0) * sizeof(double)));
+            // column indices of the explicit slices among them (contiguous, in slice order)
+            int64_t c0 = -1, c1 = -1;
+            for (int64_t q = s0; q < s1; q++) {
+                const int64_t cq = __ldg(A.cptr + q);
+                if (cq < 0) continue;
+                if (c0 < 0) c0 = cq;
+                c1 = cq + (__ldg(A.ptr + q + 1) - __ldg(A.ptr + q));
             }
+            if (c1 > c0 && c0 >= 0) bulk_prefetch_l2(A.col + c0, (uint32_t)((c1 - c0) * sizeof(IT)));
         }
     }
     const int64_t r = (int64_t)blockIdx.x * SELL_THREADS + threadIdx.x;
-    if (r >= nrows) return;
-    const int len = __ldg(slen + r);
-    if (len == SELL_BOUNDARY) return;  // G > 1 boundary row: launch_spmv_rows, after the halo
-    const int64_t base = __ldg(sptr + (r >> 5)) + (r & 31);
-    double sum = 0.0;
-    for (int k0 = 0; k0 < len; k0 += 8) {
-        IT cc[8];
-        double vv[8], xv[8];
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const bool in = k0 + k < len;
-            cc[k] = in ? __ldg(col + base + 32 * (int64_t)(k0 + k)) : (IT)0;
-            vv[k] = in ? __ldg(val + base + 32 * (int64_t)(k0 + k)) : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            if (k0 + k < len) {
-                if (GHOST && (int64_t)cc[k] >= nloc) xv[k] = __ldg(ghost + ((int64_t)cc[k] - nloc));
-                else xv[k] = __ldg(x + (int64_t)cc[k]);
-            } else {
-                xv[k] = 0.0;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < 8; k++)
-            if (k0 + k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
-    }
+    if ((r & ~(int64_t)31) >= nrows) return;  // whole warps only (sell_row shuffles)
+    double sum;
+    if (!sell_row<IT, GHOST, false>(A, r, r < nrows, x, ghost, nloc, sum)) return;
     y[r] = RESID ? b[r] - sum : sum;
 }
 
@@ -227,13 +295,13 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         ahead = 4 * sms;
     }
-    const IT* ci = static_cast<const IT*>(a.sell_col);
+    const SellDev<IT> A = sell_dev<IT>(a);
     if (a.ghost) {
-        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
-        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, a.ghost, a.nloc, y, b, istate, ahead);
+        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, a.ghost, a.nloc, y, b, istate, ahead);
+        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, a.ghost, a.nloc, y, b, istate, ahead);
     } else {
-        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
-        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_len, ci, a.sell_val, x, nullptr, a.nloc, y, b, istate, ahead);
+        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, nullptr, a.nloc, y, b, istate, ahead);
+        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, nullptr, a.nloc, y, b, istate, ahead);
     }
 }
 
@@ -2382,8 +2450,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     pcycle_kernel(Dev d, int64_t n, int m, int gs, const PT* __restrict__ rowptr,
                   const IT* __restrict__ col, const double* __restrict__ val, int lpr, double* V,
                   int64_t ld, double* z, unsigned* flags, unsigned* counter, unsigned long long* prof,
-                  double* part, const int64_t* __restrict__ sell_ptr, const uint8_t* __restrict__ sell_len,
-                  const IT* __restrict__ sell_col, const double* __restrict__ sell_val, int xs, int ntri) {
+                  double* part, SellDev<IT> sell, int xs, int ntri) {
     extern __shared__ double sm[];
     __shared__ double red[40];
     __shared__ int s_go;
@@ -2512,29 +2579,12 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         const double* u = V + (int64_t)p * ld;
         if (b == 0) stamp(p, 0);
         // ---- A: z = A u (Step 4) ---------------------------------------------------------
-        if (!drain && sell_ptr) {
-            // SELL-32 copy (short rows): one thread per row, coalesced entries, left-to-right
-            // separate multiply and add (bitwise the oracle's row loop, like spmv_sell_kernel)
-            for (int64_t r = (int64_t)b * PC_THREADS + tid; r < n; r += (int64_t)W * PC_THREADS) {
-                const int len = __ldg(sell_len + r);
-                const int64_t base = __ldg(sell_ptr + (r >> 5)) + (r & 31);
-                double sum = 0.0;
-                for (int k0 = 0; k0 < len; k0 += 8) {
-                    IT cc[8];
-                    double vv[8], xv[8];
-#pragma unroll
-                    for (int k = 0; k < 8; k++) {
-                        const bool in = k0 + k < len;
-                        cc[k] = in ? __ldg(sell_col + base + 32 * (int64_t)(k0 + k)) : (IT)0;
-                        vv[k] = in ? __ldg(sell_val + base + 32 * (int64_t)(k0 + k)) : 0.0;
-                    }
-#pragma unroll
-                    for (int k = 0; k < 8; k++) xv[k] = k0 + k < len ? __ldcg(u + (int64_t)cc[k]) : 0.0;
-#pragma unroll
-                    for (int k = 0; k < 8; k++)
-                        if (k0 + k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
-                }
-                z[r] = sum;
+        if (!drain && sell.ptr) {
+            // SELL-32 copy (short rows): one thread per row, whole warps per slice (sell_row
+            // shuffles), left-to-right separate multiply and add (bitwise the oracle's row loop)
+            for (int64_t r = (int64_t)b * PC_THREADS + tid; (r & ~(int64_t)31) < n; r += (int64_t)W * PC_THREADS) {
+                double sum;
+                if (sell_row<IT, false, true>(sell, r, r < n, u, nullptr, n, sum)) z[r] = sum;
             }
             grid_barrier(flags, W, epoch);
         } else if (!drain) {
@@ -2841,12 +2891,9 @@ static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t
     const IT* ci = static_cast<const IT*>(a.col);
     const double* va = a.val;
     int lpr = a.lpr > 0 ? a.lpr : 4;
-    const int64_t* sp = a.sell_ptr;
-    const uint8_t* sl = a.sell_len;
-    const IT* sc = static_cast<const IT*>(a.sell_col);
-    const double* sv = a.sell_val;
+    SellDev<IT> sell = sell_dev<IT>(a);
     void* args[] = {&dd, &n, &m, &gs, (void*)&rp, (void*)&ci, (void*)&va, &lpr, &V, &ld, &z, &flags, &counter, &prof,
-                    &part, (void*)&sp, (void*)&sl, (void*)&sc, (void*)&sv, &xs, &ntri};
+                    &part, (void*)&sell, &xs, &ntri};
     return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(PC_THREADS), args, smem, s);
 }
 

@@ -152,6 +152,87 @@ def test_spmv_vs_oracle(torch_cuda, name):
     s.close()
 
 
+# ---------------------------------------- SELL-32 diagonal slices (a1 SpMV)
+def _csr_banded(n, offs, drop, rng, shuffle_rows=0, dtype=np.int32):
+    """Rows r with columns r + o (o in offs, inside [0, n)), each entry dropped with
+    probability `drop` (row masks vary inside a slice; some rows end up empty); the first
+    `shuffle_rows` rows listed in a random (unsorted) order."""
+    cols = []
+    for r in range(n):
+        c = np.array([r + o for o in offs if 0 <= r + o < n and rng.random() >= drop], dtype=np.int64)
+        if r < shuffle_rows and c.size > 1:
+            c = c[rng.permutation(c.size)]
+        cols.append(c)
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum([c.size for c in cols], out=rowptr[1:])
+    colind = np.concatenate(cols).astype(dtype)
+    return W.Csr(n, n, 0, rowptr, colind, rng.standard_normal(colind.size))
+
+
+def _sell_case(name):
+    rng = np.random.default_rng(7)
+    if name == "band7_masked":      # 7 offsets, 20% of entries missing, ragged last slice
+        return _csr_banded(5013, [-70, -7, -1, 0, 1, 7, 70], 0.2, rng), "all"
+    if name == "band9":             # 9 distinct offsets: every slice explicit
+        return _csr_banded(2000, [-90, -40, -9, -1, 0, 1, 9, 40, 90], 0.0, rng), "none"
+    if name == "band8_unsorted":    # rows 0..99 unsorted: their slices explicit, the rest diagonal
+        return _csr_banded(3001, [-300, -17, -1, 0, 1, 17, 300, 301], 0.1, rng, shuffle_rows=100), "some"
+    if name == "band5_int64":
+        return _csr_banded(4099, [-64, -1, 0, 1, 64], 0.05, rng, dtype=np.int64), "all"
+    A = W.config(name.split("_")[0], N=int(name.split("_")[1])).A if "_" in name else W.config(name).A
+    return A, "most"
+
+
+@pytest.mark.parametrize("diag", ["1", "0"])
+@pytest.mark.parametrize("name", ["band7_masked", "band9", "band8_unsorted", "band5_int64", "c1", "c4_24", "c4_33", "c5_12"])
+def test_sell_diag_slices_bitwise(torch_cuda, name, diag, monkeypatch):
+    """The SELL-32 copy with diagonal slices (column = row + the slice's offset picked by the
+    row's mask) and with every slice explicit (IGS_SELL_DIAG=0) both equal the oracle's row
+    loop (P:1059 Step 4) bit for bit; the slice classification is the one the matrix implies."""
+    torch = torch_cuda
+    import paper_2205_07805_b200 as P
+    monkeypatch.setenv("IGS_SELL_DIAG", diag)
+    A, expect = _sell_case(name)
+    s = P.Solver(A)
+    info = s.info()
+    assert info["sell"] == 1
+    ns = (A.n_rows + 31) // 32
+    nd = info["sell_diag_slices"]
+    if diag == "0" or expect == "none":
+        assert nd == 0
+    elif expect == "all":
+        assert nd == ns
+    else:
+        assert 0 < nd < ns or (expect == "most" and nd == ns)
+    rng = np.random.default_rng(11)
+    for _ in range(2):
+        x = rng.standard_normal(A.n_rows)
+        y = torch.full((A.n_rows,), float("nan"), dtype=torch.float64, device="cuda")
+        s.spmv(_dev(torch, x), y)
+        assert y.cpu().numpy().tobytes() == oracle.spmv(A, x).tobytes()
+    s.close()
+
+
+@pytest.mark.parametrize("N", [24, 66])
+def test_sell_diag_slices_solve_bitwise(torch_cuda, N, monkeypatch):
+    """A GMRES(30) Alg. 3 cycle (persistent kernel at 24^3, graph-replayed kernels at 66^3)
+    gives the same H and residual history bit for bit with and without diagonal slices."""
+    torch = torch_cuda
+    import paper_2205_07805_b200 as P
+    prob = W.config("c4", N=N)
+    out = {}
+    for diag in ("1", "0"):
+        monkeypatch.setenv("IGS_SELL_DIAG", diag)
+        s = P.Solver(prob.A)
+        assert (s.info()["sell_diag_slices"] > 0) == (diag == "1")
+        b = _dev(torch, prob.b)
+        x = torch.zeros_like(b)
+        r = s.solve(b, k=30, restart=30, tol=0.0, gs_iters=2, x_out=x)
+        out[diag] = (np.asarray(r["H"]).tobytes(), np.asarray(r["res_hist"]).tobytes(), x.cpu().numpy().tobytes())
+        s.close()
+    assert out["1"] == out["0"]
+
+
 # ------------------------------------------------------------- Algorithm 1 (QR), P:386-429
 def _graded_qr(n, m, kappa, seed):
     rng = np.random.default_rng(seed)
