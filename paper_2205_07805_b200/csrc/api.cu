@@ -565,7 +565,7 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     // distinct offsets in the slice.  Test hook IGS_SELL_DIAG=0 keeps every slice explicit.
     const char* edg = std::getenv("IGS_SELL_DIAG");
     const bool want_diag = !(edg && std::atoi(edg) == 0);
-    std::vector<int64_t> cp((size_t)ns, 0);
+    std::vector<int64_t> cp((size_t)ns + 1, 0);
     std::vector<int32_t> dg((size_t)ns * 8, 0);
     std::vector<uint8_t> mk((size_t)n, 0);
     int64_t ctot = 0, ndiag = 0;
@@ -601,12 +601,11 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
                 }
                 mk[(size_t)r] = (uint8_t)m;
             }
-            cp[(size_t)s] = -1;
             ndiag++;
         } else {
-            cp[(size_t)s] = ctot;
             ctot += sp[(size_t)s + 1] - sp[(size_t)s];
         }
+        cp[(size_t)s + 1] = ctot;
     }
     std::vector<double> sv((size_t)tot, 0.0);
     std::vector<char> sc((size_t)std::max<int64_t>(ctot, 1) * (idx64 ? 8 : 4), 0);
@@ -615,7 +614,7 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
         const int64_t base = sp[(size_t)(r >> 5)] + (r & 31), cb = cp[(size_t)(r >> 5)] + (r & 31);
         for (int64_t q = rowptr[r], k = 0; q < rowptr[r + 1]; q++, k++) {
             sv[(size_t)(base + 32 * k)] = values[q];
-            if (cp[(size_t)(r >> 5)] < 0) continue;
+            if (cp[(size_t)(r >> 5) + 1] == cp[(size_t)(r >> 5)]) continue;
             const int64_t at = cb + 32 * k;
             if (idx64) reinterpret_cast<int64_t*>(sc.data())[at] = local_col[(size_t)q];
             else reinterpret_cast<int32_t*>(sc.data())[at] = (int32_t)local_col[(size_t)q];

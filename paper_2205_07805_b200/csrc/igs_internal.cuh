@@ -74,8 +74,9 @@ struct SpmvArgs {
     // c - r (all columns local), each row's offsets strictly increasing in CSR order, keeps
     // no column indices: slice s lists its offsets in sell_diag[8s..8s+7] (ascending) and row
     // r's k-th entry has column r + sell_diag[8s + (k-th set bit of sell_mask[r])].  Other
-    // slices store entry k of row 32s+l at sell_col[sell_cptr[s] + 32k + l].
-    const int64_t* sell_cptr = nullptr;  // [nslices]: column offset of a slice, -1 = diagonal
+    // slices store entry k of row 32s+l at sell_col[sell_cptr[s] + 32k + l]; a slice with
+    // sell_cptr[s+1] == sell_cptr[s] stores no columns (diagonal, or no entries at all).
+    const int64_t* sell_cptr = nullptr;  // [nslices + 1]
     const int32_t* sell_diag = nullptr;  // [nslices * 8]
     const uint8_t* sell_mask = nullptr;  // [nrows]
     // G > 1: rows with a ghost column (sell_len == SELL_BOUNDARY, not in the SELL arrays),

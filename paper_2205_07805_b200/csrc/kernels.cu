@@ -160,7 +160,7 @@ constexpr int SELL_THREADS = 256;
 template <typename IT>
 struct SellDev {
     const int64_t* __restrict__ ptr;   // [nslices + 1] value offset of slice s
-    const int64_t* __restrict__ cptr;  // [nslices] column offset, -1: diagonal slice
+    const int64_t* __restrict__ cptr;  // [nslices + 1] column offset; cptr[s+1] == cptr[s]: diagonal
     const int32_t* __restrict__ diag;  // [nslices * 8] offsets of a diagonal slice, ascending
     const uint8_t* __restrict__ len;   // [nrows]
     const uint8_t* __restrict__ mask;  // [nrows] offsets a row of a diagonal slice uses
@@ -195,22 +195,23 @@ __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool v
     const bool bnd = (len == SELL_BOUNDARY);  // G > 1 boundary row: launch_spmv_rows, after the halo
     if (bnd) len = 0;
     const int64_t base = __ldg(A.ptr + s) + (r & 31);
-    const int64_t cb = A.cptr ? __ldg(A.cptr + s) : 0;
+    const int64_t cb = __ldg(A.cptr + s), ce = __ldg(A.cptr + s + 1);
     double sum = 0.0;
-    if (cb < 0) {  // diagonal slice (warp-uniform branch)
+    if (ce == cb) {  // diagonal (or empty) slice: warp-uniform branch
         const int dl = __ldg(A.diag + 8 * s + (lane & 7));
         unsigned m = valid ? (unsigned)__ldg(A.mask + r) : 0u;
-        int64_t cc[8];
+        const double* xr = x + r;
+        int dk[8];
         double vv[8], xv[8];
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             const int bit = __ffs(m) - 1;
             m &= m - 1;
-            cc[k] = r + __shfl_sync(FULL_MASK, dl, bit & 7);
+            dk[k] = __shfl_sync(FULL_MASK, dl, bit & 7);
             vv[k] = k < len ? __ldg(A.val + base + 32 * k) : 0.0;
         }
 #pragma unroll
-        for (int k = 0; k < 8; k++) xv[k] = k < len ? ldx<CG>(x + cc[k]) : 0.0;
+        for (int k = 0; k < 8; k++) xv[k] = k < len ? ldx<CG>(xr + dk[k]) : 0.0;
 #pragma unroll
         for (int k = 0; k < 8; k++)
             if (k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
@@ -261,16 +262,10 @@ __global__ void __launch_bounds__(SELL_THREADS)
             const int64_t ns = (nrows + 31) / 32;
             const int64_t s0 = fb * (SELL_THREADS / 32), s1 = min(s0 + SELL_THREADS / 32, ns);
             const int64_t e0 = __ldg(A.ptr + s0), e1 = __ldg(A.ptr + s1);
+            const int64_t c0 = __ldg(A.cptr + s0), c1 = __ldg(A.cptr + s1);
             if (e1 > e0) bulk_prefetch_l2(A.val + e0, (uint32_t)((e1 - e0) * sizeof(double)));
             // column indices of the explicit slices among them (contiguous, in slice order)
-            int64_t c0 = -1, c1 = -1;
-            for (int64_t q = s0; q < s1; q++) {
-                const int64_t cq = __ldg(A.cptr + q);
-                if (cq < 0) continue;
-                if (c0 < 0) c0 = cq;
-                c1 = cq + (__ldg(A.ptr + q + 1) - __ldg(A.ptr + q));
-            }
-            if (c1 > c0 && c0 >= 0) bulk_prefetch_l2(A.col + c0, (uint32_t)((c1 - c0) * sizeof(IT)));
+            if (c1 > c0) bulk_prefetch_l2(A.col + c0, (uint32_t)((c1 - c0) * sizeof(IT)));
         }
     }
     const int64_t r = (int64_t)blockIdx.x * SELL_THREADS + threadIdx.x;
