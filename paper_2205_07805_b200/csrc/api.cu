@@ -620,6 +620,9 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
             else reinterpret_cast<int32_t*>(sc.data())[at] = (int32_t)local_col[(size_t)q];
         }
     }
+    // row lengths and masks padded to whole slices: the SpMV's L2 prefetch reads whole slices
+    len.resize((size_t)ns * 32, 0);
+    mk.resize((size_t)ns * 32, 0);
     CUDA_TRY(cudaMalloc(&ctx->d_sell_ptr, sizeof(int64_t) * sp.size()));
     CUDA_TRY(cudaMalloc(&ctx->d_sell_len, len.size()));
     CUDA_TRY(cudaMalloc(&ctx->d_sell_val, sizeof(double) * sv.size()));
@@ -642,6 +645,7 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     ctx->A.sell_diag = ctx->d_sell_diag;
     ctx->A.sell_mask = ctx->d_sell_mask;
     ctx->sell_diag_slices = ndiag;
+    ctx->A.sell_kind = ndiag == ns ? 1 : (ndiag == 0 ? 2 : 0);
     ctx->sell_entries = tot;
     if (!bnd.empty()) {
         CUDA_TRY(cudaMalloc(&ctx->d_bnd_rows, sizeof(int64_t) * bnd.size()));

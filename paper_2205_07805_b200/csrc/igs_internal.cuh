@@ -79,6 +79,7 @@ struct SpmvArgs {
     const int64_t* sell_cptr = nullptr;  // [nslices + 1]
     const int32_t* sell_diag = nullptr;  // [nslices * 8]
     const uint8_t* sell_mask = nullptr;  // [nrows]
+    int sell_kind = 0;                   // 0 mixed, 1 every slice diagonal, 2 none diagonal
     // G > 1: rows with a ghost column (sell_len == SELL_BOUNDARY, not in the SELL arrays),
     // multiplied by launch_spmv_rows once the halo has arrived.  With a SELL copy the CSR
     // arrays above hold only these rows (row t of the compact CSR is row bnd_rows[t])

@@ -186,7 +186,12 @@ __device__ __forceinline__ double ldx(const double* p) {
 // column of entry k is r + offset, the offset taken from the slice's list by a shuffle (no
 // column index is read: 4 or 8 bytes less per nonzero, and the x gathers no longer wait
 // for a column load).  Returns false for rows it must not store (past the end, boundary).
-template <typename IT, bool GHOST, bool CG>
+// KIND: SELL_MIXED (either slice kind), SELL_ALL_DIAG (every slice diagonal: no column
+// offsets read, no explicit path compiled -- fewer registers, more resident warps),
+// SELL_NO_DIAG (every slice explicit).
+enum { SELL_MIXED = 0, SELL_ALL_DIAG = 1, SELL_NO_DIAG = 2 };
+
+template <typename IT, bool GHOST, bool CG, int KIND>
 __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool valid, const double* __restrict__ x,
                                          const double* __restrict__ ghost, int64_t nloc, double& out) {
     const int lane = threadIdx.x & 31;
@@ -195,9 +200,11 @@ __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool v
     const bool bnd = (len == SELL_BOUNDARY);  // G > 1 boundary row: launch_spmv_rows, after the halo
     if (bnd) len = 0;
     const int64_t base = __ldg(A.ptr + s) + (r & 31);
-    const int64_t cb = __ldg(A.cptr + s), ce = __ldg(A.cptr + s + 1);
+    int64_t cb = 0, ce = 0;
+    if (KIND == SELL_MIXED) { cb = __ldg(A.cptr + s); ce = __ldg(A.cptr + s + 1); }
+    if (KIND == SELL_NO_DIAG) cb = __ldg(A.cptr + s);
     double sum = 0.0;
-    if (ce == cb) {  // diagonal (or empty) slice: warp-uniform branch
+    if (KIND == SELL_ALL_DIAG || (KIND == SELL_MIXED && ce == cb)) {  // diagonal (or empty) slice: warp-uniform
         const int dl = __ldg(A.diag + 8 * s + (lane & 7));
         unsigned m = valid ? (unsigned)__ldg(A.mask + r) : 0u;
         const double* xr = x + r;
@@ -215,7 +222,7 @@ __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool v
 #pragma unroll
         for (int k = 0; k < 8; k++)
             if (k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
-    } else {
+    } else if (KIND != SELL_ALL_DIAG) {
         const int64_t cbase = cb + (r & 31);
         for (int k0 = 0; k0 < len; k0 += 8) {
             IT cc[8];
@@ -249,30 +256,40 @@ __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool v
 // are fully coalesced and, for stencil rows, the x gathers of a warp are one contiguous
 // range per k.  No shared memory, no barrier.  8 entries per batch are loaded before use
 // (memory-level parallelism).
-template <typename IT, bool GHOST, bool RESID>
-__global__ void __launch_bounds__(SELL_THREADS)
+template <typename IT, bool GHOST, bool RESID, int KIND>
+__global__ void __launch_bounds__(SELL_THREADS, KIND == SELL_ALL_DIAG ? 6 : 1)
     spmv_sell_kernel(int64_t nrows, SellDev<IT> A, const double* __restrict__ x, const double* __restrict__ ghost,
                      int64_t nloc, double* __restrict__ y, const double* __restrict__ b, const int* istate,
                      int ahead) {
-    if (!running(istate)) return;
-    if (ahead > 0 && threadIdx.x == 0) {
+    // the status word gates only the store: its load overlaps the row's first loads (a
+    // stopped solve's SpMV computes and discards; x is always a valid vector)
+    const bool live = running(istate);
+    if (ahead > 0 && threadIdx.x == 0 && live) {
         // the CTA that runs about one resident wave later: its values (and columns) to L2 now
         const int64_t nb = (int64_t)gridDim.x, fb = (int64_t)blockIdx.x + ahead;
         if (fb < nb) {
             const int64_t ns = (nrows + 31) / 32;
             const int64_t s0 = fb * (SELL_THREADS / 32), s1 = min(s0 + SELL_THREADS / 32, ns);
             const int64_t e0 = __ldg(A.ptr + s0), e1 = __ldg(A.ptr + s1);
-            const int64_t c0 = __ldg(A.cptr + s0), c1 = __ldg(A.cptr + s1);
             if (e1 > e0) bulk_prefetch_l2(A.val + e0, (uint32_t)((e1 - e0) * sizeof(double)));
-            // column indices of the explicit slices among them (contiguous, in slice order)
-            if (c1 > c0) bulk_prefetch_l2(A.col + c0, (uint32_t)((c1 - c0) * sizeof(IT)));
+            if (KIND != SELL_ALL_DIAG) {  // column indices of its explicit slices (contiguous)
+                const int64_t c0 = __ldg(A.cptr + s0), c1 = __ldg(A.cptr + s1);
+                if (c1 > c0) bulk_prefetch_l2(A.col + c0, (uint32_t)((c1 - c0) * sizeof(IT)));
+            }
+            // and the row lengths / masks / slice offsets its first loads wait on
+            const int64_t r0 = s0 * 32, nr = min(s1 * 32, nrows) - r0;
+            bulk_prefetch_l2(A.len + (r0 & ~(int64_t)15), (uint32_t)((nr + 31) & ~31));
+            if (KIND != SELL_NO_DIAG) {
+                bulk_prefetch_l2(A.mask + (r0 & ~(int64_t)15), (uint32_t)((nr + 31) & ~31));
+                bulk_prefetch_l2(A.diag + 8 * s0, (uint32_t)(32 * (s1 - s0)));
+            }
         }
     }
     const int64_t r = (int64_t)blockIdx.x * SELL_THREADS + threadIdx.x;
     if ((r & ~(int64_t)31) >= nrows) return;  // whole warps only (sell_row shuffles)
     double sum;
-    if (!sell_row<IT, GHOST, false>(A, r, r < nrows, x, ghost, nloc, sum)) return;
-    y[r] = RESID ? b[r] - sum : sum;
+    const bool st = sell_row<IT, GHOST, false, KIND>(A, r, r < nrows, x, ghost, nloc, sum);
+    if (st && live) y[r] = RESID ? b[r] - sum : sum;
 }
 
 template <typename IT>
@@ -291,12 +308,20 @@ static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const doubl
         ahead = 4 * sms;
     }
     const SellDev<IT> A = sell_dev<IT>(a);
-    if (a.ghost) {
-        if (resid) spmv_sell_kernel<IT, true, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, a.ghost, a.nloc, y, b, istate, ahead);
-        else spmv_sell_kernel<IT, true, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, a.ghost, a.nloc, y, b, istate, ahead);
-    } else {
-        if (resid) spmv_sell_kernel<IT, false, true><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, nullptr, a.nloc, y, b, istate, ahead);
-        else spmv_sell_kernel<IT, false, false><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, nullptr, a.nloc, y, b, istate, ahead);
+    const double* g = a.ghost;
+    switch (a.sell_kind * 4 + (g ? 2 : 0) + (resid ? 1 : 0)) {
+#define IGS_SELL_CASE(K, GH, RS)                                                                            \
+    case K * 4 + (GH ? 2 : 0) + (RS ? 1 : 0):                                                             \
+        spmv_sell_kernel<IT, GH, RS, K><<<blocks, SELL_THREADS, 0, s>>>(a.nrows, A, x, g, a.nloc, y, b, istate, ahead); \
+        break;
+        IGS_SELL_CASE(SELL_MIXED, false, false) IGS_SELL_CASE(SELL_MIXED, false, true)
+        IGS_SELL_CASE(SELL_MIXED, true, false) IGS_SELL_CASE(SELL_MIXED, true, true)
+        IGS_SELL_CASE(SELL_ALL_DIAG, false, false) IGS_SELL_CASE(SELL_ALL_DIAG, false, true)
+        IGS_SELL_CASE(SELL_ALL_DIAG, true, false) IGS_SELL_CASE(SELL_ALL_DIAG, true, true)
+        IGS_SELL_CASE(SELL_NO_DIAG, false, false) IGS_SELL_CASE(SELL_NO_DIAG, false, true)
+        IGS_SELL_CASE(SELL_NO_DIAG, true, false) IGS_SELL_CASE(SELL_NO_DIAG, true, true)
+#undef IGS_SELL_CASE
+        default: break;
     }
 }
 
@@ -2579,7 +2604,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
             // shuffles), left-to-right separate multiply and add (bitwise the oracle's row loop)
             for (int64_t r = (int64_t)b * PC_THREADS + tid; (r & ~(int64_t)31) < n; r += (int64_t)W * PC_THREADS) {
                 double sum;
-                if (sell_row<IT, false, true>(sell, r, r < n, u, nullptr, n, sum)) z[r] = sum;
+                if (sell_row<IT, false, true, SELL_MIXED>(sell, r, r < n, u, nullptr, n, sum)) z[r] = sum;
             }
             grid_barrier(flags, W, epoch);
         } else if (!drain) {

@@ -174,7 +174,7 @@ def _sell_case(name):
     if name == "band7_masked":      # 7 offsets, 20% of entries missing, ragged last slice
         return _csr_banded(5013, [-70, -7, -1, 0, 1, 7, 70], 0.2, rng), "all"
     if name == "band9":             # 9 distinct offsets: explicit slices but at the two ends
-        return _csr_banded(2000, [-90, -40, -9, -1, 0, 1, 9, 40, 90], 0.0, rng), "ends"
+        return _csr_banded(2000, [-90, -40, -9, -1, 0, 1, 9, 40, 90], 0.2, rng), "ends"
     if name == "band8_unsorted":    # rows 0..99 unsorted: their slices explicit, the rest diagonal
         return _csr_banded(3001, [-300, -17, -1, 0, 1, 17, 300, 301], 0.1, rng, shuffle_rows=100), "some"
     if name == "band5_int64":
