@@ -153,15 +153,16 @@ def test_spmv_vs_oracle(torch_cuda, name):
 
 
 # ---------------------------------------- SELL-32 diagonal slices (a1 SpMV)
-def _csr_banded(n, offs, drop, rng, shuffle_rows=0, dtype=np.int32):
+def _csr_banded(n, offs, drop, rng, scatter_rows=0, dtype=np.int32):
     """Rows r with columns r + o (o in offs, inside [0, n)), each entry dropped with
     probability `drop` (row masks vary inside a slice; some rows end up empty); the first
-    `shuffle_rows` rows listed in a random (unsorted) order."""
+    `scatter_rows` rows get three more columns anywhere in the row (their slices then hold
+    far more than 8 distinct offsets).  Columns strictly increasing per row (igs.h)."""
     cols = []
     for r in range(n):
         c = np.array([r + o for o in offs if 0 <= r + o < n and rng.random() >= drop], dtype=np.int64)
-        if r < shuffle_rows and c.size > 1:
-            c = c[rng.permutation(c.size)]
+        if r < scatter_rows:
+            c = np.union1d(c, rng.integers(0, n, 3))
         cols.append(c)
     rowptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum([c.size for c in cols], out=rowptr[1:])
@@ -175,8 +176,8 @@ def _sell_case(name):
         return _csr_banded(5013, [-70, -7, -1, 0, 1, 7, 70], 0.2, rng), "all"
     if name == "band9":             # 9 distinct offsets: explicit slices but at the two ends
         return _csr_banded(2000, [-90, -40, -9, -1, 0, 1, 9, 40, 90], 0.2, rng), "ends"
-    if name == "band8_unsorted":    # rows 0..99 unsorted: their slices explicit, the rest diagonal
-        return _csr_banded(3001, [-300, -17, -1, 0, 1, 17, 300, 301], 0.1, rng, shuffle_rows=100), "some"
+    if name == "band8_mixed":       # rows 0..99 with scattered columns: their slices explicit, the rest diagonal
+        return _csr_banded(3001, [-300, -17, -1, 0, 1, 17, 300, 301], 0.1, rng, scatter_rows=100), "some"
     if name == "band5_int64":
         return _csr_banded(4099, [-64, -1, 0, 1, 64], 0.05, rng, dtype=np.int64), "all"
     A = W.config(name.split("_")[0], N=int(name.split("_")[1])).A if "_" in name else W.config(name).A
@@ -184,7 +185,7 @@ def _sell_case(name):
 
 
 @pytest.mark.parametrize("diag", ["1", "0"])
-@pytest.mark.parametrize("name", ["band7_masked", "band9", "band8_unsorted", "band5_int64", "c1", "c4_24", "c4_33", "c5_12"])
+@pytest.mark.parametrize("name", ["band7_masked", "band9", "band8_mixed", "band5_int64", "c1", "c4_24", "c4_33", "c5_12"])
 def test_sell_diag_slices_bitwise(torch_cuda, name, diag, monkeypatch):
     """The SELL-32 copy with diagonal slices (column = row + the slice's offset picked by the
     row's mask) and with every slice explicit (IGS_SELL_DIAG=0) both equal the oracle's row
