@@ -207,8 +207,13 @@ typedef enum {
     IGS_INFO_PCYCLE_LAUNCHES = 7,  /* restart cycles run by the persistent kernel           */
     IGS_INFO_SELL = 8,             /* 1: the SpMV uses the SELL-32 copy of A               */
     IGS_INFO_CSR_COMPACT = 9,      /* 1: the CSR arrays hold only the boundary rows         */
-    IGS_INFO_SELL_DIAG_SLICES = 10 /* SELL slices stored as diagonal offsets (no column
+    IGS_INFO_SELL_DIAG_SLICES = 10,/* SELL slices stored as diagonal offsets (no column
                                       indices)                                */
+    IGS_INFO_SELL_PIPE = 11,       /* 1: every slice is diagonal and the SpMV is the bulk-copy
+                                      pipeline kernel                        */
+    IGS_INFO_SPMV_BYTES = 12       /* bytes one SpMV launch streams in the stored format (SELL
+                                      copy or CSR) incl. x and y; the byte model of the
+                                      roofline keeps the CSR definition       */
 } igs_info_key;
 igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value);
 

@@ -161,7 +161,7 @@ struct igs_ctx {
     int64_t* d_sell_cptr = nullptr;
     int32_t* d_sell_diag = nullptr;
     uint8_t* d_sell_mask = nullptr;
-    int64_t sell_entries = 0, sell_diag_slices = 0;
+    int64_t sell_entries = 0, sell_diag_slices = 0, sell_stream_bytes = 0;
     // G > 1 with SELL: rows touching ghost columns run after the halo, the rest during it
     int64_t* d_bnd_rows = nullptr;
     cudaStream_t hstream = nullptr;  // halo exchange stream
@@ -547,30 +547,30 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     if (const char* e = std::getenv("IGS_TEST_BND_EVERY"))
         if (ctx->nranks == 1 && std::atoi(e) > 0)
             for (int64_t r = 0; r < n; r += std::atoi(e)) bnd.push_back(r);
-    size_t bi = 0;
-    for (int64_t s = 0; s < ns; s++) {
-        int64_t mx = 0;
-        for (int64_t r = 32 * s; r < std::min<int64_t>(n, 32 * s + 32); r++) {
-            if (bi < bnd.size() && bnd[bi] == r) { len[(size_t)r] = SELL_BOUNDARY; bi++; continue; }
-            const int64_t l = rowptr[r + 1] - rowptr[r];
-            if (l >= SELL_BOUNDARY) { bnd.clear(); return IGS_OK; }  // long rows: keep the CSR kernels
-            len[(size_t)r] = (uint8_t)l;
-            mx = std::max(mx, l);
-        }
-        sp[(size_t)s + 1] = sp[(size_t)s] + 32 * mx;
-    }
-    const int64_t tot = std::max<int64_t>(sp[(size_t)ns], 1);
     // diagonal slices: every column local, each row's offsets c - r strictly
     // increasing in CSR order (so the row's order is the slice list's order), at most 8
-    // distinct offsets in the slice.  Test hook IGS_SELL_DIAG=0 keeps every slice explicit.
+    // distinct offsets in the slice.  A diagonal slice is stored by list position: the entry
+    // of row 32s+l with offset list[j] sits at sell_ptr[s] + 32j + l (rows without that
+    // offset: a zero that is never read), so the value loads need no per-row index at all;
+    // an explicit slice by entry index k as before.  Test hook IGS_SELL_DIAG=0 keeps every
+    // slice explicit.
     const char* edg = std::getenv("IGS_SELL_DIAG");
     const bool want_diag = !(edg && std::atoi(edg) == 0);
     std::vector<int64_t> cp((size_t)ns + 1, 0);
     std::vector<int32_t> dg((size_t)ns * 8, 0);
     std::vector<uint8_t> mk((size_t)n, 0);
     int64_t ctot = 0, ndiag = 0;
+    size_t bi = 0;
     for (int64_t s = 0; s < ns; s++) {
         const int64_t r0 = 32 * s, r1 = std::min<int64_t>(n, r0 + 32);
+        int64_t mx = 0;
+        for (int64_t r = r0; r < r1; r++) {
+            if (bi < bnd.size() && bnd[bi] == r) { len[(size_t)r] = SELL_BOUNDARY; bi++; continue; }
+            const int64_t l = rowptr[r + 1] - rowptr[r];
+            if (l >= SELL_BOUNDARY) { bnd.clear(); return IGS_OK; }  // long rows: keep the CSR kernels
+            len[(size_t)r] = (uint8_t)l;
+            mx = std::max(mx, l);
+        }
         bool ok = want_diag;
         int64_t D[8];
         int nd = 0;
@@ -602,19 +602,29 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
                 mk[(size_t)r] = (uint8_t)m;
             }
             ndiag++;
+            sp[(size_t)s + 1] = sp[(size_t)s] + 32 * nd;
         } else {
-            ctot += sp[(size_t)s + 1] - sp[(size_t)s];
+            sp[(size_t)s + 1] = sp[(size_t)s] + 32 * mx;
+            ctot += 32 * mx;
         }
         cp[(size_t)s + 1] = ctot;
     }
+    const int64_t tot = std::max<int64_t>(sp[(size_t)ns], 1);
     std::vector<double> sv((size_t)tot, 0.0);
     std::vector<char> sc((size_t)std::max<int64_t>(ctot, 1) * (idx64 ? 8 : 4), 0);
     for (int64_t r = 0; r < n; r++) {
         if (len[(size_t)r] == SELL_BOUNDARY) continue;
-        const int64_t base = sp[(size_t)(r >> 5)] + (r & 31), cb = cp[(size_t)(r >> 5)] + (r & 31);
+        const int64_t s = r >> 5, base = sp[(size_t)s] + (r & 31), cb = cp[(size_t)s] + (r & 31);
+        const bool diag = cp[(size_t)s + 1] == cp[(size_t)s];
+        const int32_t* D = dg.data() + 8 * s;
+        const int nd = (int)((sp[(size_t)s + 1] - sp[(size_t)s]) / 32);
         for (int64_t q = rowptr[r], k = 0; q < rowptr[r + 1]; q++, k++) {
+            if (diag) {
+                const int jpos = (int)(std::lower_bound(D, D + nd, (int32_t)(local_col[(size_t)q] - r)) - D);
+                sv[(size_t)(base + 32 * jpos)] = values[q];
+                continue;
+            }
             sv[(size_t)(base + 32 * k)] = values[q];
-            if (cp[(size_t)(r >> 5) + 1] == cp[(size_t)(r >> 5)]) continue;
             const int64_t at = cb + 32 * k;
             if (idx64) reinterpret_cast<int64_t*>(sc.data())[at] = local_col[(size_t)q];
             else reinterpret_cast<int32_t*>(sc.data())[at] = (int32_t)local_col[(size_t)q];
@@ -646,7 +656,15 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     ctx->A.sell_mask = ctx->d_sell_mask;
     ctx->sell_diag_slices = ndiag;
     ctx->A.sell_kind = ndiag == ns ? 1 : (ndiag == 0 ? 2 : 0);
+    // test / A-B hook: row count from which an all-diagonal matrix takes the bulk-copy
+    // pipeline SpMV (0: always, so the tests reach it at small n; -1: never)
+    if (const char* e = std::getenv("IGS_SELL_PIPE_MIN_N")) ctx->A.sell_pipe_min_n = std::atoll(e);
     ctx->sell_entries = tot;
+    // bytes one SpMV launch streams from the SELL copy (IGS_INFO_SPMV_BYTES): stored values,
+    // column indices of the explicit slices, row lengths, masks / offset lists when any slice
+    // is diagonal, slice offsets; + x and y
+    ctx->sell_stream_bytes = 8 * tot + (idx64 ? 8 : 4) * ctot + 32 * ns + (ndiag ? 64 * ns : 0) +
+                             8 * (ns + 1) * (ndiag == ns ? 1 : 2) + 16 * n;
     if (!bnd.empty()) {
         CUDA_TRY(cudaMalloc(&ctx->d_bnd_rows, sizeof(int64_t) * bnd.size()));
         CUDA_TRY(cudaMemcpy(ctx->d_bnd_rows, bnd.data(), sizeof(int64_t) * bnd.size(), cudaMemcpyHostToDevice));
@@ -2033,6 +2051,13 @@ extern "C" igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value) {
         case IGS_INFO_SELL: *value = ctx->A.sell_ptr != nullptr; break;
         case IGS_INFO_CSR_COMPACT: *value = ctx->csr_compact; break;
         case IGS_INFO_SELL_DIAG_SLICES: *value = ctx->sell_diag_slices; break;
+        case IGS_INFO_SPMV_BYTES:
+            *value = ctx->A.sell_ptr ? ctx->sell_stream_bytes + 8 * ctx->n_ghost : (int64_t)spmv_bytes(ctx);
+            break;
+        case IGS_INFO_SELL_PIPE:
+            *value = ctx->A.sell_ptr && ctx->A.sell_kind == 1 && ctx->A.sell_pipe_min_n >= 0 &&
+                     ctx->A.nrows >= ctx->A.sell_pipe_min_n;
+            break;
         default: ARG_CHECK(false, "igs_info: unknown key");
     }
     return IGS_OK;

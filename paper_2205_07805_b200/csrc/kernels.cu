@@ -183,9 +183,10 @@ __device__ __forceinline__ double ldx(const double* p) {
 // Row r of the SELL-32 copy, summed left to right in the row's CSR order with separate
 // multiply and add (bitwise the oracle's row loop).  Called by all 32 lanes of a warp for
 // the 32 rows of slice r >> 5 (rows >= nrows pass valid = false).  In a diagonal slice the
-// column of entry k is r + offset, the offset taken from the slice's list by a shuffle (no
-// column index is read: 4 or 8 bytes less per nonzero, and the x gathers no longer wait
-// for a column load).  Returns false for rows it must not store (past the end, boundary).
+// column of an entry is r + offset, the offset one of the slice's list (read by every lane:
+// one 32-byte broadcast) and the entries present named by the row's mask (no column index is
+// read: 4 or 8 bytes less per nonzero, and the x gathers no longer wait for a column
+// load).  Returns false for rows it must not store (past the end, boundary).
 // KIND: SELL_MIXED (either slice kind), SELL_ALL_DIAG (every slice diagonal: no column
 // offsets read, no explicit path compiled -- fewer registers, more resident warps),
 // SELL_NO_DIAG (every slice explicit).
@@ -194,7 +195,6 @@ enum { SELL_MIXED = 0, SELL_ALL_DIAG = 1, SELL_NO_DIAG = 2 };
 template <typename IT, bool GHOST, bool CG, int KIND>
 __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool valid, const double* __restrict__ x,
                                          const double* __restrict__ ghost, int64_t nloc, double& out) {
-    const int lane = threadIdx.x & 31;
     const int64_t s = r >> 5;
     int len = valid ? (int)__ldg(A.len + r) : 0;
     const bool bnd = (len == SELL_BOUNDARY);  // G > 1 boundary row: launch_spmv_rows, after the halo
@@ -205,23 +205,31 @@ __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool v
     if (KIND == SELL_NO_DIAG) cb = __ldg(A.cptr + s);
     double sum = 0.0;
     if (KIND == SELL_ALL_DIAG || (KIND == SELL_MIXED && ce == cb)) {  // diagonal (or empty) slice: warp-uniform
-        const int dl = __ldg(A.diag + 8 * s + (lane & 7));
-        unsigned m = valid ? (unsigned)__ldg(A.mask + r) : 0u;
-        const double* xr = x + r;
-        int dk[8];
+        // stored by list position: the entry with offset list[j] of row 32s+l at ptr[s] + 32j + l,
+        // present iff bit j of the row's mask; the list ascends like the row's columns, so
+        // position order is the row's CSR order.  Value loads: one base + immediates; nothing
+        // depends on the row length (it only marks boundary rows, which have mask 0).
+        const int4 d0 = __ldg(reinterpret_cast<const int4*>(A.diag + 8 * s));
+        const int4 d1 = __ldg(reinterpret_cast<const int4*>(A.diag + 8 * s) + 1);
+        const int dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        const unsigned m = valid ? (unsigned)__ldg(A.mask + r) : 0u;
+        const char* xb = reinterpret_cast<const char*>(x + r);
+        const double* vp = A.val + base;
+        // Absent positions contribute 0.0 * 0.0 = +0.0 (neither the padding nor x is read):
+        // a sum that starts at +0.0 is never -0.0, so adding +0.0 leaves every bit of it --
+        // the 8 multiply-adds run unconditionally and equal the row's own shorter sum.
         double vv[8], xv[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            const int bit = __ffs(m) - 1;
-            m &= m - 1;
-            dk[k] = __shfl_sync(FULL_MASK, dl, bit & 7);
-            vv[k] = k < len ? __ldg(A.val + base + 32 * k) : 0.0;
+        for (int j = 0; j < 8; j++) {
+            vv[j] = 0.0;
+            xv[j] = 0.0;
+            if ((m >> j) & 1u) {
+                vv[j] = __ldg(vp + 32 * j);
+                xv[j] = ldx<CG>(reinterpret_cast<const double*>(xb + 8 * (int64_t)dd[j]));
+            }
         }
 #pragma unroll
-        for (int k = 0; k < 8; k++) xv[k] = k < len ? ldx<CG>(xr + dk[k]) : 0.0;
-#pragma unroll
-        for (int k = 0; k < 8; k++)
-            if (k < len) sum = __dadd_rn(sum, __dmul_rn(vv[k], xv[k]));
+        for (int j = 0; j < 8; j++) sum = __dadd_rn(sum, __dmul_rn(vv[j], xv[j]));
     } else if (KIND != SELL_ALL_DIAG) {
         const int64_t cbase = cb + (r & 31);
         for (int k0 = 0; k0 < len; k0 += 8) {
@@ -257,7 +265,7 @@ __device__ __forceinline__ bool sell_row(const SellDev<IT>& A, int64_t r, bool v
 // range per k.  No shared memory, no barrier.  8 entries per batch are loaded before use
 // (memory-level parallelism).
 template <typename IT, bool GHOST, bool RESID, int KIND>
-__global__ void __launch_bounds__(SELL_THREADS, KIND == SELL_ALL_DIAG ? 6 : 1)
+__global__ void __launch_bounds__(SELL_THREADS, KIND == SELL_ALL_DIAG ? 5 : 1)
     spmv_sell_kernel(int64_t nrows, SellDev<IT> A, const double* __restrict__ x, const double* __restrict__ ghost,
                      int64_t nloc, double* __restrict__ y, const double* __restrict__ b, const int* istate,
                      int ahead) {
@@ -292,11 +300,232 @@ __global__ void __launch_bounds__(SELL_THREADS, KIND == SELL_ALL_DIAG ? 6 : 1)
     if (st && live) y[r] = RESID ? b[r] - sum : sum;
 }
 
+// K1 for matrices whose slices are all diagonal (the stencil configs c1, c3, c4, c5): resident
+// CTAs, each warp walking slices s, s + W, s + 2W, ... (W = warps in the grid), software-
+// pipelined by one slice.  A slice costs two dependent rounds of loads: its metadata (value
+// offset, masks, boundary marks, offset list: ~100 bytes per warp) and then its values and x
+// gathers (~2 KB per warp).  With one short-lived warp per slice half of the resident warps
+// sit in the first round, where they keep almost nothing in flight (ncu: 31 warps per SM,
+// 5.9 TB/s, issue slots 30% busy, every stall a long-scoreboard wait); here the metadata of
+// slice s + W is requested before the values of slice s, so every resident warp always has
+// a slice's values and gathers in flight.  Same arithmetic as sell_row.
+constexpr int SD_CTAS_PER_SM = 4;
+
+template <bool RESID>
+__global__ void __launch_bounds__(SELL_THREADS, SD_CTAS_PER_SM)
+    spmv_sell_diag_kernel(int64_t nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ diag,
+                          const uint8_t* __restrict__ len8, const uint8_t* __restrict__ mask8,
+                          const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                          const double* __restrict__ b, const int* istate) {
+    if (!running(istate)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t ns = (nrows + 31) >> 5;
+    const int64_t W = (int64_t)gridDim.x * (SELL_THREADS / 32);
+    int64_t s = (int64_t)blockIdx.x * (SELL_THREADS / 32) + (threadIdx.x >> 5);
+    if (s >= ns) return;
+    // round 1 of the first slice (masks / lengths are padded to whole slices)
+    int64_t p0 = __ldg(ptr + s);
+    unsigned m = __ldg(mask8 + 32 * s + lane), ln = __ldg(len8 + 32 * s + lane);
+    int4 d0 = __ldg(reinterpret_cast<const int4*>(diag + 8 * s));
+    int4 d1 = __ldg(reinterpret_cast<const int4*>(diag + 8 * s) + 1);
+    for (;;) {
+        const int64_t sn = s + W;
+        const bool more = sn < ns;  // warp-uniform
+        int64_t p0n = 0;
+        unsigned mn = 0, lnn = 0;
+        int4 d0n = make_int4(0, 0, 0, 0), d1n = d0n;
+        if (more) {  // round 1 of the next slice, in flight during round 2 of this one
+            p0n = __ldg(ptr + sn);
+            mn = __ldg(mask8 + 32 * sn + lane);
+            lnn = __ldg(len8 + 32 * sn + lane);
+            d0n = __ldg(reinterpret_cast<const int4*>(diag + 8 * sn));
+            d1n = __ldg(reinterpret_cast<const int4*>(diag + 8 * sn) + 1);
+        }
+        const int64_t r = 32 * s + lane;
+        const char* xb = reinterpret_cast<const char*>(x + r);
+        const double* vp = val + p0 + lane;
+        const int dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        double vv[8], xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            vv[j] = 0.0;
+            xv[j] = 0.0;
+            if ((m >> j) & 1u) {
+                vv[j] = __ldg(vp + 32 * j);
+                xv[j] = __ldg(reinterpret_cast<const double*>(xb + 8 * (int64_t)dd[j]));
+            }
+        }
+        const bool st = r < nrows && ln != SELL_BOUNDARY;  // boundary rows (G > 1): launch_spmv_rows
+        double bv = 0.0;
+        if (RESID && st) bv = __ldg(b + r);
+        double sum = 0.0;  // absent positions add 0.0 * 0.0 = +0.0: no bit of the sum changes (sell_row)
+#pragma unroll
+        for (int j = 0; j < 8; j++) sum = __dadd_rn(sum, __dmul_rn(vv[j], xv[j]));
+        if (st) y[r] = RESID ? bv - sum : sum;
+        if (!more) break;
+        s = sn; p0 = p0n; m = mn; ln = lnn; d0 = d0n; d1 = d1n;
+    }
+}
+
+static void spmv_sell_diag(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                           const int* istate, cudaStream_t s) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t blocks = (a.nrows + SELL_THREADS - 1) / SELL_THREADS;
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks, (int64_t)SD_CTAS_PER_SM * sms);
+    if (resid) spmv_sell_diag_kernel<true><<<grid, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_diag, a.sell_len, a.sell_mask, a.sell_val, x, y, b, istate);
+    else spmv_sell_diag_kernel<false><<<grid, SELL_THREADS, 0, s>>>(a.nrows, a.sell_ptr, a.sell_diag, a.sell_len, a.sell_mask, a.sell_val, x, y, b, istate);
+}
+
+// K1 for matrices whose slices are all diagonal (the stencil configs c1, c3, c4, c5): the same
+// SELL-32 row sums with the matrix streamed by the bulk-copy engine.  Persistent CTAs, CPS
+// per SM, of CW consumer warps + 1 producer warp; tile = CW slices (32 CW rows).  Per tile
+// the producer issues four bulk copies into a shared-memory ring stage -- the tile's values
+// (contiguous in the SELL copy, at most 8 per row), its row lengths, masks and slice offset
+// lists -- completion counted on the stage's mbarrier, and leaves each slice's offset inside
+// the stage next to them.  Consumer warp w owns slice w of every tile (thread = row): it
+// picks its column offsets from the list in shared memory (no shuffles), issues the x
+// gathers (L1 / L2: a stencil's neighbours), takes its values from the stage, releases the
+// stage, and sums in the row's CSR order with separate multiply and add (bitwise the
+// oracle's row loop).  The DRAM stream (8 B per nonzero + 2 B per row) no longer waits on a
+// chain of dependent loads per warp (lengths -> values -> gathers): SP_STAGES tiles per CTA
+// are always in flight.
+template <int CW>
+struct SellPipe {
+    static constexpr int THREADS = (CW + 1) * 32;
+    static constexpr int ROWS = CW * 32;
+    static constexpr int VAL_BYTES = ROWS * 8 * (int)sizeof(double);  // <= 8 entries per row
+    static constexpr int STAGE_BYTES = VAL_BYTES + 3 * ROWS + CW * (int)sizeof(int);  // + len, mask, diag, slice offsets
+};
+
+template <int CW, int STAGES, int CPS, bool RESID>
+__global__ void __launch_bounds__(SellPipe<CW>::THREADS, CPS)
+    spmv_sell_pipe_kernel(int64_t nrows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ diag,
+                          const uint8_t* __restrict__ len8, const uint8_t* __restrict__ mask8,
+                          const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                          const double* __restrict__ b, const int* istate) {
+    using P = SellPipe<CW>;
+    if (!running(istate)) return;  // uniform: before any barrier is initialised
+    extern __shared__ __align__(128) unsigned char smem_sp[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_sp + (size_t)STAGES * P::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, CW); }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t ns = (nrows + 31) / 32;
+    const int64_t ntiles = (ns + CW - 1) / CW;
+    const int64_t nk = ntiles > (int64_t)blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (warp == CW) {
+        // ---------------- producer warp: lanes 0..CW read the slice offsets of the tile, one
+        // tile ahead; lane 0 issues the copies ----------------
+        auto load_ptr = [&](int64_t k) -> int64_t {
+            if (k >= nk || lane > CW) return 0;
+            const int64_t s = min((blockIdx.x + k * (int64_t)gridDim.x) * CW + lane, ns);
+            return __ldg(ptr + s);
+        };
+        int64_t pn = load_ptr(0);
+        for (int64_t k = 0; k < nk; k++) {
+            const int64_t pc = pn;
+            pn = load_ptr(k + 1);
+            const int st = (int)(k % STAGES);
+            unsigned char* stage = smem_sp + (size_t)st * P::STAGE_BYTES;
+            const int64_t s0 = (blockIdx.x + k * (int64_t)gridDim.x) * CW;
+            const int nsl = (int)min((int64_t)CW, ns - s0);
+            const int64_t e0 = __shfl_sync(FULL_MASK, pc, 0), e1 = __shfl_sync(FULL_MASK, pc, nsl);
+            if (lane == 0) mbar_wait(empty + st, (uint32_t)(((k / STAGES) & 1) ^ 1));
+            __syncwarp();
+            if (lane < CW) reinterpret_cast<int*>(stage + P::VAL_BYTES + 3 * P::ROWS)[lane] = (int)(pc - e0);
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t vb = (uint32_t)((e1 - e0) * (int64_t)sizeof(double)), mb = (uint32_t)nsl * 32u;
+                mbar_arrive_expect_tx(full + st, vb + 3u * mb);  // release: the offsets above are visible
+                if (vb) bulk_g2s(stage, val + e0, vb, full + st);
+                bulk_g2s(stage + P::VAL_BYTES, len8 + 32 * s0, mb, full + st);
+                bulk_g2s(stage + P::VAL_BYTES + P::ROWS, mask8 + 32 * s0, mb, full + st);
+                bulk_g2s(stage + P::VAL_BYTES + 2 * P::ROWS, diag + 8 * s0, mb, full + st);
+            }
+        }
+    } else {
+        // ---------------- consumer warp w: slice w of every tile ----------------
+        for (int64_t k = 0; k < nk; k++) {
+            const int st = (int)(k % STAGES);
+            const unsigned char* stage = smem_sp + (size_t)st * P::STAGE_BYTES;
+            const int64_t s0 = (blockIdx.x + k * (int64_t)gridDim.x) * CW;
+            const int64_t r = (s0 + warp) * 32 + lane;
+            const bool have = s0 + warp < ns;  // warp-uniform (slices past the end were not copied)
+            mbar_wait(full + st, (uint32_t)((k / STAGES) & 1));
+            int len = have ? (int)stage[P::VAL_BYTES + 32 * warp + lane] : 0;  // rows >= nrows: padded with 0
+            const bool bnd = (len == SELL_BOUNDARY);  // G > 1 boundary row: launch_spmv_rows, after the halo
+            if (bnd) len = 0;
+            const unsigned m = (have && !bnd) ? (unsigned)stage[P::VAL_BYTES + P::ROWS + 32 * warp + lane] : 0u;
+            const int4* dg = reinterpret_cast<const int4*>(stage + P::VAL_BYTES + 2 * P::ROWS + 32 * warp);
+            const int4 d0 = dg[0], d1 = dg[1];
+            const int dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+            const double* vs = reinterpret_cast<const double*>(stage) +
+                               reinterpret_cast<const int*>(stage + P::VAL_BYTES + 3 * P::ROWS)[warp] + lane;
+            const char* xb = reinterpret_cast<const char*>(x + r);
+            double xv[8], vv[8];
+            // list position j in order = the row's CSR order (see sell_row)
+#pragma unroll
+            for (int j = 0; j < 8; j++) xv[j] = ((m >> j) & 1u) ? __ldg(reinterpret_cast<const double*>(xb + 8 * (int64_t)dd[j])) : 0.0;
+            double bv = 0.0;
+            if (RESID && m) bv = __ldg(b + r);
+#pragma unroll
+            for (int j = 0; j < 8; j++) vv[j] = ((m >> j) & 1u) ? vs[32 * j] : 0.0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + st);  // the stage refills while the gathers are in flight
+            double sum = 0.0;  // absent positions add 0.0 * 0.0 = +0.0: no bit of the sum changes (sell_row)
+#pragma unroll
+            for (int j = 0; j < 8; j++) sum = __dadd_rn(sum, __dmul_rn(vv[j], xv[j]));
+            if (have && r < nrows && !bnd) {
+                if (RESID && !m) bv = __ldg(b + r);
+                y[r] = RESID ? bv - sum : sum;
+            }
+        }
+    }
+}
+
+template <int CW, int STAGES, int CPS>
+static bool spmv_sell_pipe(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
+                           const int* istate, cudaStream_t s) {
+    using P = SellPipe<CW>;
+    static int sms = 0;
+    static bool ok = false;
+    const size_t smem = (size_t)STAGES * P::STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        ok = cudaFuncSetAttribute(spmv_sell_pipe_kernel<CW, STAGES, CPS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+             cudaFuncSetAttribute(spmv_sell_pipe_kernel<CW, STAGES, CPS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+    }
+    if (!ok) return false;
+    const int64_t ntiles = ((a.nrows + 31) / 32 + CW - 1) / CW;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, CPS * (int64_t)sms);
+    if (resid) spmv_sell_pipe_kernel<CW, STAGES, CPS, true><<<grid, P::THREADS, smem, s>>>(a.nrows, a.sell_ptr, a.sell_diag, a.sell_len, a.sell_mask, a.sell_val, x, y, b, istate);
+    else spmv_sell_pipe_kernel<CW, STAGES, CPS, false><<<grid, P::THREADS, smem, s>>>(a.nrows, a.sell_ptr, a.sell_diag, a.sell_len, a.sell_mask, a.sell_val, x, y, b, istate);
+    return true;
+}
+
 template <typename IT>
 static void spmv_sell(const SpmvArgs& a, const double* x, double* y, const double* b, bool resid,
                       const int* istate, cudaStream_t s) {
     const unsigned blocks = (unsigned)((a.nrows + SELL_THREADS - 1) / SELL_THREADS);
     if (blocks == 0) return;
+    if (a.sell_kind == SELL_ALL_DIAG && a.sell_pipe_min_n >= 0 && a.nrows >= a.sell_pipe_min_n) {
+        static int cfg = -1;  // A/B hook: 0 resident warps walking slices, 1 bulk-copy pipeline
+        if (cfg < 0) { const char* e = std::getenv("IGS_SELL_PIPE_CFG"); cfg = e ? std::atoi(e) : 0; }
+        if (cfg == 0) { spmv_sell_diag(a, x, y, b, resid, istate, s); return; }
+        if (spmv_sell_pipe<16, 3, 2>(a, x, y, b, resid, istate, s)) return;
+    }
     // L2 prefetch distance in CTAs: about one resident wave (4 CTAs per SM of 256 threads).
     // c4: 5.5 -> 6.4 TB/s (the latency of the dependent value/column -> gather phases now
     // hits L2 instead of DRAM)
