@@ -209,8 +209,8 @@ typedef enum {
     IGS_INFO_CSR_COMPACT = 9,      /* 1: the CSR arrays hold only the boundary rows         */
     IGS_INFO_SELL_DIAG_SLICES = 10,/* SELL slices stored as diagonal offsets (no column
                                       indices)                                */
-    IGS_INFO_SELL_PIPE = 11,       /* 1: every slice is diagonal and the SpMV is the bulk-copy
-                                      pipeline kernel                        */
+    IGS_INFO_SELL_WALK = 11,       /* 1: every slice is diagonal and the SpMV is the kernel of
+                                      resident warps walking slices          */
     IGS_INFO_SPMV_BYTES = 12       /* bytes one SpMV launch streams in the stored format (SELL
                                       copy or CSR) incl. x and y; the byte model of the
                                       roofline keeps the CSR definition       */

@@ -656,9 +656,9 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     ctx->A.sell_mask = ctx->d_sell_mask;
     ctx->sell_diag_slices = ndiag;
     ctx->A.sell_kind = ndiag == ns ? 1 : (ndiag == 0 ? 2 : 0);
-    // test / A-B hook: row count from which an all-diagonal matrix takes the bulk-copy
-    // pipeline SpMV (0: always, so the tests reach it at small n; -1: never)
-    if (const char* e = std::getenv("IGS_SELL_PIPE_MIN_N")) ctx->A.sell_pipe_min_n = std::atoll(e);
+    // test / A-B hook: row count from which an all-diagonal matrix takes the
+    // slice-walking SpMV (0: always, so the tests reach it at small n; -1: never)
+    if (const char* e = std::getenv("IGS_SELL_WALK_MIN_N")) ctx->A.sell_walk_min_n = std::atoll(e);
     ctx->sell_entries = tot;
     // bytes one SpMV launch streams from the SELL copy (IGS_INFO_SPMV_BYTES): stored values,
     // column indices of the explicit slices, row lengths, masks / offset lists when any slice
@@ -2054,9 +2054,9 @@ extern "C" igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value) {
         case IGS_INFO_SPMV_BYTES:
             *value = ctx->A.sell_ptr ? ctx->sell_stream_bytes + 8 * ctx->n_ghost : (int64_t)spmv_bytes(ctx);
             break;
-        case IGS_INFO_SELL_PIPE:
-            *value = ctx->A.sell_ptr && ctx->A.sell_kind == 1 && ctx->A.sell_pipe_min_n >= 0 &&
-                     ctx->A.nrows >= ctx->A.sell_pipe_min_n;
+        case IGS_INFO_SELL_WALK:
+            *value = ctx->A.sell_ptr && ctx->A.sell_kind == 1 && ctx->A.sell_walk_min_n >= 0 &&
+                     ctx->A.nrows >= ctx->A.sell_walk_min_n;
             break;
         default: ARG_CHECK(false, "igs_info: unknown key");
     }

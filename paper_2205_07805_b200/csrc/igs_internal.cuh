@@ -80,8 +80,8 @@ struct SpmvArgs {
     const int32_t* sell_diag = nullptr;  // [nslices * 8]
     const uint8_t* sell_mask = nullptr;  // [nrows]
     int sell_kind = 0;                   // 0 mixed, 1 every slice diagonal, 2 none diagonal
-    // every slice diagonal and nrows >= this: the bulk-copy pipeline kernel (< 0: never)
-    int64_t sell_pipe_min_n = 262144;
+    // every slice diagonal and nrows >= this: resident warps walking slices (spmv_sell_diag_kernel) (< 0: never)
+    int64_t sell_walk_min_n = 262144;
     // G > 1: rows with a ghost column (sell_len == SELL_BOUNDARY, not in the SELL arrays),
     // multiplied by launch_spmv_rows once the halo has arrived.  With a SELL copy the CSR
     // arrays above hold only these rows (row t of the compact CSR is row bnd_rows[t])

@@ -269,7 +269,7 @@ def igs_plan_remap(row_begin, n_local, rowptr, colind, ghosts):
 
 # ------------------------------------------------------------------------- convenience
 INFO_KEYS = ["xchg", "nranks", "n_ghost", "n_send", "n_peers", "n_bnd", "graph_launches", "pcycle_launches",
-             "sell", "csr_compact", "sell_diag_slices", "sell_pipe", "spmv_bytes"]
+             "sell", "csr_compact", "sell_diag_slices", "sell_walk", "spmv_bytes"]
 
 
 def igs_info(ctx: int) -> dict:

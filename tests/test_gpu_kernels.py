@@ -184,27 +184,27 @@ def _sell_case(name):
     return A, "most"
 
 
-@pytest.mark.parametrize("diag", ["1", "0", "pipe"])
+@pytest.mark.parametrize("diag", ["1", "0", "walk"])
 @pytest.mark.parametrize("name", ["band7_masked", "band9", "band8_mixed", "band5_int64", "c1", "c4_24", "c4_33", "c5_12",
                                   "c3_600"])
 def test_sell_diag_slices_bitwise(torch_cuda, name, diag, monkeypatch):
     """The SELL-32 copy with diagonal slices (column = row + the slice's offset picked by the
     row's mask) and with every slice explicit (IGS_SELL_DIAG=0) both equal the oracle's row
     loop (P:1059 Step 4) bit for bit; the slice classification is the one the matrix implies.
-    "pipe": all-diagonal matrices through the bulk-copy pipeline kernel at any size
-    (IGS_SELL_PIPE_MIN_N=0; by default from 262144 rows on -- c3_600 takes it either way)."""
+    "walk": all-diagonal matrices through the kernel of resident warps walking slices at any size
+    (IGS_SELL_WALK_MIN_N=0; by default from 262144 rows on -- c3_600 takes it either way)."""
     torch = torch_cuda
     import paper_2205_07805_b200 as P
     monkeypatch.setenv("IGS_SELL_DIAG", "0" if diag == "0" else "1")
-    if diag == "pipe":
-        monkeypatch.setenv("IGS_SELL_PIPE_MIN_N", "0")
+    if diag == "walk":
+        monkeypatch.setenv("IGS_SELL_WALK_MIN_N", "0")
     A, expect = _sell_case(name)
     s = P.Solver(A)
     info = s.info()
     assert info["sell"] == 1
     ns = (A.n_rows + 31) // 32
     nd = info["sell_diag_slices"]
-    assert info["sell_pipe"] == int(nd == ns and (diag == "pipe" or A.n_rows >= 262144))
+    assert info["sell_walk"] == int(nd == ns and (diag == "walk" or A.n_rows >= 262144))
     if diag == "0":
         assert nd == 0
     elif expect == "ends":          # rows within 90 of either end miss an offset: <= 8 left
@@ -225,26 +225,26 @@ def test_sell_diag_slices_bitwise(torch_cuda, name, diag, monkeypatch):
 @pytest.mark.parametrize("N", [24, 66])
 def test_sell_diag_slices_solve_bitwise(torch_cuda, N, monkeypatch):
     """A GMRES(30) Alg. 3 cycle (persistent kernel at 24^3, graph-replayed kernels at 66^3,
-    where the SpMV and the cycle-end residual take the bulk-copy pipeline kernel) gives the
+    where the SpMV and the cycle-end residual take the slice-walking kernel) gives the
     same H, residual history and x bit for bit with diagonal slices, without them, and with
-    diagonal slices but the one-thread-per-row kernel (IGS_SELL_PIPE_MIN_N=-1)."""
+    diagonal slices but the one-thread-per-row kernel (IGS_SELL_WALK_MIN_N=-1)."""
     torch = torch_cuda
     import paper_2205_07805_b200 as P
     prob = W.config("c4", N=N)
     out = {}
-    for diag, pipe in (("1", None), ("0", None), ("1", "-1")):
+    for diag, walk in (("1", None), ("0", None), ("1", "-1")):
         monkeypatch.setenv("IGS_SELL_DIAG", diag)
-        if pipe is None:
-            monkeypatch.delenv("IGS_SELL_PIPE_MIN_N", raising=False)
+        if walk is None:
+            monkeypatch.delenv("IGS_SELL_WALK_MIN_N", raising=False)
         else:
-            monkeypatch.setenv("IGS_SELL_PIPE_MIN_N", pipe)
+            monkeypatch.setenv("IGS_SELL_WALK_MIN_N", walk)
         s = P.Solver(prob.A)
         assert (s.info()["sell_diag_slices"] > 0) == (diag == "1")
-        assert s.info()["sell_pipe"] == int(diag == "1" and pipe is None and N == 66)
+        assert s.info()["sell_walk"] == int(diag == "1" and walk is None and N == 66)
         b = _dev(torch, prob.b)
         x = torch.zeros_like(b)
         r = s.solve(b, k=30, restart=30, tol=0.0, gs_iters=2, x_out=x)
-        out[(diag, pipe)] = (np.asarray(r["H"]).tobytes(), np.asarray(r["res_hist"]).tobytes(), x.cpu().numpy().tobytes())
+        out[(diag, walk)] = (np.asarray(r["H"]).tobytes(), np.asarray(r["res_hist"]).tobytes(), x.cpu().numpy().tobytes())
         s.close()
     assert out[("1", None)] == out[("0", None)] == out[("1", "-1")]
 
