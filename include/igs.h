@@ -345,6 +345,26 @@ igs_status igs_plan_remap(int64_t row_begin, int64_t n_local, const int64_t* row
                           const void* colind, int colind_bits, int64_t n_ghost,
                           const int64_t* ghosts, int64_t* local_colind);
 
+/* Host-only layout of the SELL-32 copy igs_create keeps of a short-row block (
+ * the SpMV of P:1059 Step 4 reads it): slices of 32 rows; a slice whose rows use at most 8
+ * distinct offsets c - r (every column local, increasing along each row) is "diagonal": its
+ * ascending offset list is diag[8s..8s+7], the entry of row 32s+l with offset list[j] is
+ * val[ptr[s] + 32j + l], present iff bit j of mask[32s+l]; any other slice is "explicit":
+ * entry k of row 32s+l (CSR order) is val[ptr[s] + 32k + l] with column col[cptr[s] + 32k + l]
+ * (cptr[s+1] == cptr[s] marks a diagonal slice).  len[r] = nonzeros of row r, 255 for the rows
+ * listed in bnd_rows (ascending; G > 1 boundary rows: nothing stored).
+ *   local_col: columns in the block's local space, int64; want_diag = 0 keeps every slice
+ *   explicit.  Outputs (each may be NULL): ptr, cptr [ceil(n/32) + 1]; diag [8 ceil(n/32)];
+ *   len, mask [32 ceil(n/32)]; val [cap_val]; col [cap_col].  *n_val, *n_col = entries the
+ *   val / col arrays need (call once with val = col = NULL to size them), -1 when a row has
+ *   >= 255 entries (no SELL copy is built); *n_diag = diagonal slices.  IGS_ERR_ARG on bad
+ *   arguments or a capacity below the need.  No device is touched. */
+igs_status igs_plan_sell(int64_t n, const int64_t* rowptr, const int64_t* local_col,
+                         const double* values, int want_diag, int64_t n_bnd, const int64_t* bnd_rows,
+                         int64_t* ptr, int64_t* cptr, int32_t* diag, uint8_t* len, uint8_t* mask,
+                         int64_t cap_val, double* val, int64_t cap_col, int64_t* col,
+                         int64_t* n_val, int64_t* n_col, int64_t* n_diag);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libigs.so")
 SOURCES = ["kernels.cu", "diag.cu", "api.cu", "plan.cpp"]
-HEADERS = ["igs_internal.cuh", "ptx_util.cuh", "xchg.cuh"]
+HEADERS = ["igs_internal.cuh", "ptx_util.cuh", "xchg.cuh", "sell_plan.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

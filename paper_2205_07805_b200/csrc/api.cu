@@ -25,6 +25,7 @@
 
 #include "../../include/igs.h"
 #include "igs_internal.cuh"
+#include "sell_plan.h"
 #include "xchg.cuh"
 
 namespace igs {
@@ -533,8 +534,6 @@ static void free_ctx(igs_ctx* c) {
 static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vector<int64_t>& local_col,
                              const double* values, bool idx64, std::vector<int64_t>& bnd) {
     const int64_t n = ctx->n_local, ns = (n + 31) / 32;
-    std::vector<int64_t> sp((size_t)ns + 1, 0);
-    std::vector<uint8_t> len((size_t)n);
     // G > 1: rows that touch a ghost column are left to the boundary pass (row-list kernel,
     // after the halo); the SELL pass runs while the halo is in flight and skips them
     // (row length SELL_BOUNDARY, no entries stored)
@@ -547,92 +546,22 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     if (const char* e = std::getenv("IGS_TEST_BND_EVERY"))
         if (ctx->nranks == 1 && std::atoi(e) > 0)
             for (int64_t r = 0; r < n; r += std::atoi(e)) bnd.push_back(r);
-    // diagonal slices: every column local, each row's offsets c - r strictly
-    // increasing in CSR order (so the row's order is the slice list's order), at most 8
-    // distinct offsets in the slice.  A diagonal slice is stored by list position: the entry
-    // of row 32s+l with offset list[j] sits at sell_ptr[s] + 32j + l (rows without that
-    // offset: a zero that is never read), so the value loads need no per-row index at all;
-    // an explicit slice by entry index k as before.  Test hook IGS_SELL_DIAG=0 keeps every
-    // slice explicit.
+    // the slice layout is host-only work (plan.cpp, also behind igs_plan_sell for the CPU
+    // tests).  Test hook IGS_SELL_DIAG=0 keeps every slice explicit.
     const char* edg = std::getenv("IGS_SELL_DIAG");
-    const bool want_diag = !(edg && std::atoi(edg) == 0);
-    std::vector<int64_t> cp((size_t)ns + 1, 0);
-    std::vector<int32_t> dg((size_t)ns * 8, 0);
-    std::vector<uint8_t> mk((size_t)n, 0);
-    int64_t ctot = 0, ndiag = 0;
-    size_t bi = 0;
-    for (int64_t s = 0; s < ns; s++) {
-        const int64_t r0 = 32 * s, r1 = std::min<int64_t>(n, r0 + 32);
-        int64_t mx = 0;
-        for (int64_t r = r0; r < r1; r++) {
-            if (bi < bnd.size() && bnd[bi] == r) { len[(size_t)r] = SELL_BOUNDARY; bi++; continue; }
-            const int64_t l = rowptr[r + 1] - rowptr[r];
-            if (l >= SELL_BOUNDARY) { bnd.clear(); return IGS_OK; }  // long rows: keep the CSR kernels
-            len[(size_t)r] = (uint8_t)l;
-            mx = std::max(mx, l);
-        }
-        bool ok = want_diag;
-        int64_t D[8];
-        int nd = 0;
-        for (int64_t r = r0; r < r1 && ok; r++) {
-            if (len[(size_t)r] == SELL_BOUNDARY) continue;
-            int64_t prev = INT64_MIN;
-            for (int64_t q = rowptr[r]; q < rowptr[r + 1] && ok; q++) {
-                const int64_t c = local_col[(size_t)q], o = c - r;
-                if (c < 0 || c >= n || o <= prev || o > INT32_MAX || o < INT32_MIN) { ok = false; break; }
-                prev = o;
-                bool seen = false;
-                for (int i = 0; i < nd; i++) seen = seen || D[i] == o;
-                if (!seen) {
-                    if (nd == 8) { ok = false; break; }
-                    D[nd++] = o;
-                }
-            }
-        }
-        if (ok) {
-            std::sort(D, D + nd);
-            for (int i = 0; i < nd; i++) dg[(size_t)s * 8 + i] = (int32_t)D[i];
-            for (int64_t r = r0; r < r1; r++) {
-                if (len[(size_t)r] == SELL_BOUNDARY) continue;
-                unsigned m = 0;
-                for (int64_t q = rowptr[r]; q < rowptr[r + 1]; q++) {
-                    const int64_t o = local_col[(size_t)q] - r;
-                    m |= 1u << (int)(std::lower_bound(D, D + nd, o) - D);
-                }
-                mk[(size_t)r] = (uint8_t)m;
-            }
-            ndiag++;
-            sp[(size_t)s + 1] = sp[(size_t)s] + 32 * nd;
-        } else {
-            sp[(size_t)s + 1] = sp[(size_t)s] + 32 * mx;
-            ctot += 32 * mx;
-        }
-        cp[(size_t)s + 1] = ctot;
-    }
-    const int64_t tot = std::max<int64_t>(sp[(size_t)ns], 1);
-    std::vector<double> sv((size_t)tot, 0.0);
+    SellHost h;
+    sell_plan(n, rowptr, local_col.data(), values, bnd, !(edg && std::atoi(edg) == 0), h);
+    if (!h.built) { bnd.clear(); return IGS_OK; }  // long rows: keep the CSR kernels
+    const std::vector<int64_t>&sp = h.ptr, &cp = h.cptr;
+    const std::vector<int32_t>& dg = h.diag;
+    const std::vector<uint8_t>&len = h.len, &mk = h.mask;
+    const std::vector<double>& sv = h.val;
+    const int64_t tot = (int64_t)sv.size(), ctot = cp[(size_t)ns], ndiag = h.ndiag;
     std::vector<char> sc((size_t)std::max<int64_t>(ctot, 1) * (idx64 ? 8 : 4), 0);
-    for (int64_t r = 0; r < n; r++) {
-        if (len[(size_t)r] == SELL_BOUNDARY) continue;
-        const int64_t s = r >> 5, base = sp[(size_t)s] + (r & 31), cb = cp[(size_t)s] + (r & 31);
-        const bool diag = cp[(size_t)s + 1] == cp[(size_t)s];
-        const int32_t* D = dg.data() + 8 * s;
-        const int nd = (int)((sp[(size_t)s + 1] - sp[(size_t)s]) / 32);
-        for (int64_t q = rowptr[r], k = 0; q < rowptr[r + 1]; q++, k++) {
-            if (diag) {
-                const int jpos = (int)(std::lower_bound(D, D + nd, (int32_t)(local_col[(size_t)q] - r)) - D);
-                sv[(size_t)(base + 32 * jpos)] = values[q];
-                continue;
-            }
-            sv[(size_t)(base + 32 * k)] = values[q];
-            const int64_t at = cb + 32 * k;
-            if (idx64) reinterpret_cast<int64_t*>(sc.data())[at] = local_col[(size_t)q];
-            else reinterpret_cast<int32_t*>(sc.data())[at] = (int32_t)local_col[(size_t)q];
-        }
+    for (int64_t q = 0; q < ctot; q++) {
+        if (idx64) reinterpret_cast<int64_t*>(sc.data())[q] = h.col[(size_t)q];
+        else reinterpret_cast<int32_t*>(sc.data())[q] = (int32_t)h.col[(size_t)q];
     }
-    // row lengths and masks padded to whole slices: the SpMV's L2 prefetch reads whole slices
-    len.resize((size_t)ns * 32, 0);
-    mk.resize((size_t)ns * 32, 0);
     CUDA_TRY(cudaMalloc(&ctx->d_sell_ptr, sizeof(int64_t) * sp.size()));
     CUDA_TRY(cudaMalloc(&ctx->d_sell_len, len.size()));
     CUDA_TRY(cudaMalloc(&ctx->d_sell_val, sizeof(double) * sv.size()));

@@ -29,7 +29,7 @@ EXPORTS = ["igs_create", "igs_nccl_unique_id", "igs_workspace_bytes", "igs_bind_
            "igs_last_error", "igs_op_block_dot", "igs_op_spmv", "igs_op_update",
            "igs_op_trisolve", "igs_plan_ghosts", "igs_plan_remap", "igs_qr",
            "igs_op_basis_diag", "igs_bench_block_dot", "igs_set_timeout", "igs_create_virtual",
-           "igs_virtual_spmv", "igs_virtual_solve", "igs_info", "igs_bench_update"]
+           "igs_virtual_spmv", "igs_virtual_solve", "igs_info", "igs_bench_update", "igs_plan_sell"]
 
 
 class IgsError(RuntimeError):
@@ -86,6 +86,7 @@ def lib() -> ctypes.CDLL:
             "igs_op_basis_diag": [I64, I, P, I64, P, P],
             "igs_plan_ghosts": [I64, I64, P, P, I, I, P, P, P, P],
             "igs_plan_remap": [I64, I64, P, P, I, I64, P, P],
+            "igs_plan_sell": [I64, P, P, P, I, I64, P, P, P, P, P, P, I64, P, I64, P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -265,6 +266,40 @@ def igs_plan_remap(row_begin, n_local, rowptr, colind, ghosts):
                                 int(ghosts.size), _ptr(ghosts) if ghosts.size else None, _ptr(out)),
            "igs_plan_remap")
     return out[:int(rowptr[-1])]
+
+
+def igs_plan_sell(n, rowptr, local_col, values, want_diag=True, bnd_rows=()):
+    """The SELL-32 arrays igs_create builds (host only): dict with ptr, cptr, diag, len, mask,
+    val, col, n_diag -- or None when a row has >= 255 entries (no SELL copy)."""
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    local_col = np.ascontiguousarray(local_col, dtype=np.int64)
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    bnd = np.ascontiguousarray(bnd_rows, dtype=np.int64)
+    ns = (int(n) + 31) // 32
+    nv, nc, nd = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    out = {"ptr": np.zeros(ns + 1, np.int64), "cptr": np.zeros(ns + 1, np.int64),
+           "diag": np.zeros(8 * ns, np.int32), "len": np.zeros(32 * ns, np.uint8),
+           "mask": np.zeros(32 * ns, np.uint8)}
+
+    def call(val, col):
+        _check(lib().igs_plan_sell(int(n), _ptr(rowptr), _ptr(local_col) if local_col.size else None,
+                                   _ptr(values) if values.size else None, int(bool(want_diag)),
+                                   int(bnd.size), _ptr(bnd) if bnd.size else None,
+                                   _ptr(out["ptr"]), _ptr(out["cptr"]), _ptr(out["diag"]) if ns else None,
+                                   _ptr(out["len"]) if ns else None, _ptr(out["mask"]) if ns else None,
+                                   0 if val is None else int(val.size), None if val is None else _ptr(val),
+                                   0 if col is None else int(col.size), None if col is None else _ptr(col),
+                                   ctypes.byref(nv), ctypes.byref(nc), ctypes.byref(nd)), "igs_plan_sell")
+
+    call(None, None)
+    if nv.value < 0:
+        return None
+    out["val"] = np.zeros(max(nv.value, 1), np.float64)
+    out["col"] = np.zeros(max(nc.value, 1), np.int64)
+    call(out["val"], out["col"])
+    out["val"], out["col"] = out["val"][:nv.value], out["col"][:nc.value]
+    out["n_diag"] = nd.value
+    return out
 
 
 # ------------------------------------------------------------------------- convenience
