@@ -546,6 +546,14 @@ static igs_status build_sell(igs_ctx* ctx, const int64_t* rowptr, const std::vec
     if (const char* e = std::getenv("IGS_TEST_BND_EVERY"))
         if (ctx->nranks == 1 && std::atoi(e) > 0)
             for (int64_t r = 0; r < n; r += std::atoi(e)) bnd.push_back(r);
+    // IGS_TEST_BND_ENDS=m: the first and the last m rows instead (the shape of a z-slab's
+    // boundary: its two outer planes; tools/slab_proxy.py)
+    if (const char* e = std::getenv("IGS_TEST_BND_ENDS"))
+        if (ctx->nranks == 1 && bnd.empty() && std::atoll(e) > 0) {
+            const int64_t m = std::min<int64_t>(std::atoll(e), n / 2);
+            for (int64_t r = 0; r < m; r++) bnd.push_back(r);
+            for (int64_t r = n - m; r < n; r++) bnd.push_back(r);
+        }
     // the slice layout is host-only work (plan.cpp, also behind igs_plan_sell for the CPU
     // tests).  Test hook IGS_SELL_DIAG=0 keeps every slice explicit.
     const char* edg = std::getenv("IGS_SELL_DIAG");

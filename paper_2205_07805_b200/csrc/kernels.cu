@@ -1112,14 +1112,19 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
         const int tg = (int)(ntiles < sms ? ntiles : sms);
         // the column sweep from p = 96 on (c3 p = 300: 6.39 -> 6.75 TB/s; at p = 10-75 the
         // tile kernel is ahead: c4 p = 25 6.92 vs 5.79; profiles/r2/bdot_sweep_ab.md);
-        // IGS_BDOT_SW_MIN_P moves the switch (A/B and test hook)
+        // and below p = 8 (one column group: the tile kernel's two u, z slots allow a single
+        // tile of lookahead there -- c4 p = 1 / 5: 203 / 231 -> 148 / 177 us isolated, 0.3 ms of the
+        // 242 ms bench step in an alternating A/B, profiles/r2/c26);
+        // IGS_BDOT_SW_MIN_P moves the upper switch (A/B and test hook; it also disables the
+        // small-p use when above 1000)
         static int sw_min_p = -1;
         if (sw_min_p < 0) {
             const char* e = std::getenv("IGS_BDOT_SW_MIN_P");
             sw_min_p = e ? std::atoi(e) : 96;
         }
         const size_t wsmem = bdot_sw_smem(p, nv);
-        if (tg <= grid && p >= sw_min_p && wsmem <= 227 * 1024) {
+        const bool sweep = p >= sw_min_p || (p < 8 && sw_min_p <= 1000);
+        if (tg <= grid && sweep && wsmem <= 227 * 1024) {
             if (nv == 2) {
                 cudaFuncSetAttribute(bdot_sw_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem);
                 bdot_sw_kernel<2><<<tg, BT_THREADS, wsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);

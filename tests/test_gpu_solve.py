@@ -660,10 +660,13 @@ def test_split_interior_boundary_spmv_one_gpu(P, monkeypatch):
     prob = W.config("c3", N=64)
     b = torch.from_numpy(prob.b).cuda()
     outs = {}
-    for every in ("7", "0"):
-        monkeypatch.setenv("IGS_TEST_BND_EVERY", every)
+    for every in ("7", "0", "ends"):
+        monkeypatch.setenv("IGS_TEST_BND_EVERY", "0" if every == "ends" else every)
+        if every == "ends":   # the first and last 100 rows instead (a slab's outer planes)
+            monkeypatch.setenv("IGS_TEST_BND_ENDS", "100")
         monkeypatch.setenv("IGS_PERSIST", "0")
         s = P.Solver(prob.A)
+        assert s.info()["n_bnd"] == {"7": (prob.A.n_rows + 6) // 7, "0": 0, "ends": 200}[every]
         outs[every] = s.solve(b, k=60, restart=20, tol=1e-10, gs_iters=2)
         y = torch.empty(prob.A.n_rows, dtype=torch.float64, device="cuda")
         x = torch.from_numpy(np.random.default_rng(1).standard_normal(prob.A.n_rows)).cuda()
@@ -673,6 +676,9 @@ def test_split_interior_boundary_spmv_one_gpu(P, monkeypatch):
     g, u = outs["7"], outs["0"]
     assert g["H"].tobytes() == u["H"].tobytes() and g["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
     assert g["y"].tobytes() == u["y"].tobytes()
+    e = outs["ends"]
+    assert e["H"].tobytes() == u["H"].tobytes() and e["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+    assert e["y"].tobytes() == u["y"].tobytes()
 
 
 @pytest.mark.parametrize("persist", ["1", "0"])

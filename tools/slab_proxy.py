@@ -2,7 +2,10 @@
 """One-GPU proxy of a c4 rank at G = 8: the 128^3 stencil (n = 2,097,152 = one 32-plane
 z-slab of 256^3) through one GMRES(100) cycle, on the plain single-GPU path and on the two
 G > 1 reduction paths with a 1-rank communicator (IGS_XCHG=1: the fused exchange in the
-block dot; IGS_FORCE_NCCL=1: ncclAllReduce after every block dot).  Reports it/s, the byte
+block dot; IGS_FORCE_NCCL=1: ncclAllReduce after every block dot), and with the two outer
+planes routed through the boundary pass of the split SpMV (IGS_TEST_BND_ENDS: the interior
+rows on the main stream, the 2 n / 32 boundary rows by the row-list kernel on the halo stream,
+fork / join inside the captured cycle -- everything a rank does at G > 1 but the transports).  Reports it/s, the byte
 model's GB/s and the per-iteration time next to the HBM ideal -- the per-iteration overhead
 budget of SURVEY §8(e) (80% strong scaling at 8 GPUs needs <= 60-72 us of it).
 
@@ -48,7 +51,10 @@ def main():
     nnz = 7 * n - 6 * a.N * a.N
     model = sum(nnz * 12 + (n + 1) * 4 + 16 * n + 16 * n * p for p in range(1, 101))
     out = {"N": a.N, "n": n}
-    for name, env in (("plain", {}), ("xchg_1rank", {"IGS_XCHG": "1"}), ("ncclallreduce_1rank", {"IGS_FORCE_NCCL": "1"})):
+    plane = str(n // 32)  # a c4 z-slab at G = 8 is 32 planes thick: each outer plane holds n / 32 rows
+    for name, env in (("plain", {}), ("xchg_1rank", {"IGS_XCHG": "1"}), ("ncclallreduce_1rank", {"IGS_FORCE_NCCL": "1"}),
+                      ("split_spmv", {"IGS_TEST_BND_ENDS": plane}),
+                      ("split_spmv_xchg_1rank", {"IGS_TEST_BND_ENDS": plane, "IGS_XCHG": "1"})):
         r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, a.N, a.reps, a.gs)], env=dict(os.environ, **env),
                            capture_output=True, text=True, timeout=900)
         if r.returncode != 0:
