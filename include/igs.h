@@ -211,9 +211,11 @@ typedef enum {
                                       indices)                                */
     IGS_INFO_SELL_WALK = 11,       /* 1: every slice is diagonal and the SpMV is the kernel of
                                       resident warps walking slices          */
-    IGS_INFO_SPMV_BYTES = 12       /* bytes one SpMV launch streams in the stored format (SELL
+    IGS_INFO_SPMV_BYTES = 12,      /* bytes one SpMV launch streams in the stored format (SELL
                                       copy or CSR) incl. x and y; the byte model of the
                                       roofline keeps the CSR definition       */
+    IGS_INFO_PCYCLE_ARES = 13      /* > 0: the last persistent-kernel cycle kept A in shared
+                                      memory (value = CSR entries of the largest CTA share) */
 } igs_info_key;
 igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value);
 

@@ -141,6 +141,9 @@ struct igs_ctx {
     bool pc_enabled = true;   // IGS_PERSIST=0 disables
     bool mgs_fused = true;    // IGS_MGS_FUSED=0: MGS with separate dot and axpy kernels
     bool xs_enabled = true;   // IGS_PC_XSTAGE=0: persistent kernel gathers u from L2 (long rows)
+    int last_ares = 0;        // resident-A entries per CTA of the last persistent launch (0: not resident)
+    bool ares_enabled = true; // IGS_PC_ARES=0: persistent kernel re-reads A from L2 every iteration
+    std::vector<int32_t> h_rowlen;  // row lengths (n <= pcycle_xs_max(), no SELL copy): sizes the resident A
     bool two_fused = true;    // IGS_TWO_FUSED=0: Alg. 2 two-reduce with a separate second block dot
     double two_fused_l2 = 80e6;  // IGS_TWO_FUSED_L2_MB: L2 budget of the fused update + dot
     int pc_ntri = 0;          // IGS_PC_NTRI: forward-substitution CTAs of the persistent kernel (0 = auto)
@@ -743,6 +746,10 @@ static igs_status create_ctx(igs_ctx** out, int64_t n_global, int64_t row_begin,
     // SELL-32 copy for short rows (coalesced per-thread rows).  When it exists
     // it is the only full copy of A on the device: the CSR arrays keep just the boundary rows
     // (G > 1: rows with a ghost column, multiplied after the halo by launch_spmv_rows).
+    if (n_local <= pcycle_xs_max() && ctx->A.lpr == 32 && nranks == 1) {
+        ctx->h_rowlen.resize((size_t)n_local);
+        for (int64_t r = 0; r < n_local; r++) ctx->h_rowlen[(size_t)r] = (int32_t)(rowptr[r + 1] - rowptr[r]);
+    }
     std::vector<int64_t> bnd;
     {
         const char* es = std::getenv("IGS_SELL");  // test hook: IGS_SELL=0 keeps the CSR kernels
@@ -806,6 +813,7 @@ static igs_status create_ctx(igs_ctx** out, int64_t n_global, int64_t row_begin,
         if (const char* e = std::getenv("IGS_PERSIST")) ctx->pc_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_MGS_FUSED")) ctx->mgs_fused = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_PC_XSTAGE")) ctx->xs_enabled = std::atoi(e) != 0;
+        if (const char* e = std::getenv("IGS_PC_ARES")) ctx->ares_enabled = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_TWO_FUSED")) ctx->two_fused = std::atoi(e) != 0;
         if (const char* e = std::getenv("IGS_TWO_FUSED_L2_MB")) ctx->two_fused_l2 = std::atof(e) * 1e6;
         if (const char* e = std::getenv("IGS_PC_NTRI")) ctx->pc_ntri = std::atoi(e);
@@ -1278,9 +1286,20 @@ static igs_status run_cycle(igs_ctx* ctx, int m, int alg, int t0) {
             // two forward-substitution CTAs on alternate iterations once the order-p solve
             // outlasts an iteration (long cycles)
             const int ntri = ctx->pc_ntri > 0 ? ctx->pc_ntri : (m >= 128 && grid >= 8 ? 2 : 1);
+            // long rows with u staged: keep A itself in shared memory for the cycle when every
+            // worker CTA's rows fit (c2: 24 MB of CSR over 145 CTAs); the launcher drops it
+            // when they do not
+            int ares = 0;
+            if (xs && ctx->ares_enabled && !ctx->h_rowlen.empty()) {
+                const int W = pcycle_worker_ctas(grid, gs, ntri);
+                std::vector<int64_t> per((size_t)W, 0);
+                for (int64_t r = 0; r < n; r++) per[(size_t)(r % W)] += ctx->h_rowlen[(size_t)r];
+                ares = (int)std::min<int64_t>(*std::max_element(per.begin(), per.end()), INT32_MAX);
+            }
             cudaError_t el_ = launch_pcycle(d, ctx->A, ctx->d_V, ctx->ldv, ctx->d_z, n, m, gs,
                                            ctx->d_counter + 4, ctx->d_counter, grid, st, ctx->d_pcprof, part, xs,
-                                           ntri);
+                                           ntri, &ares);
+            ctx->last_ares = ares;
             CUDA_TRY(el_);
         });
         if (ctx->d_pcprof) {  // IGS_PC_PROF=1: mean phase durations of this cycle to stderr
@@ -1988,6 +2007,7 @@ extern "C" igs_status igs_info(const igs_ctx* ctx, int key, int64_t* value) {
         case IGS_INFO_SELL: *value = ctx->A.sell_ptr != nullptr; break;
         case IGS_INFO_CSR_COMPACT: *value = ctx->csr_compact; break;
         case IGS_INFO_SELL_DIAG_SLICES: *value = ctx->sell_diag_slices; break;
+        case IGS_INFO_PCYCLE_ARES: *value = ctx->last_ares; break;
         case IGS_INFO_SPMV_BYTES:
             *value = ctx->A.sell_ptr ? ctx->sell_stream_bytes + 8 * ctx->n_ghost : (int64_t)spmv_bytes(ctx);
             break;

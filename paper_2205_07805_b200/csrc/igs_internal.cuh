@@ -102,7 +102,12 @@ void launch_spmv(const SpmvArgs& a, const double* x, double* y, const double* b,
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
                           unsigned long long* prof = nullptr, double* part = nullptr, int xs = 0,
-                          int ntri = 1);
+                          int ntri = 1, int* ares = nullptr);
+// (*ares in: with xs, the most CSR entries any worker CTA owns -- pcycle_worker_ctas(grid, gs,
+//  ntri) workers, warp w of CTA b taking rows w W + b, + 16 W, ... -- when A is to stay in
+//  shared memory for the cycle; out: the value the launch used, 0 when it does not fit)
+int pcycle_worker_ctas(int grid, int gs, int ntri);
+constexpr int PCYCLE_WARPS = 16;
 // (part != nullptr: row-block dots with grid x 2(m+1) partials, for larger n;
 //  xs != 0: u staged in shared memory for the CSR phase A -- n <= pcycle_xs_max())
 int64_t pcycle_xs_max();

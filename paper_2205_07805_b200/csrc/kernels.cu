@@ -2568,7 +2568,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     pcycle_kernel(Dev d, int64_t n, int m, int gs, const PT* __restrict__ rowptr,
                   const IT* __restrict__ col, const double* __restrict__ val, int lpr, double* V,
                   int64_t ld, double* z, unsigned* flags, unsigned* counter, unsigned long long* prof,
-                  double* part, SellDev<IT> sell, int xs, int ntri) {
+                  double* part, SellDev<IT> sell, int xs, int ntri, int ares) {
     extern __shared__ double sm[];
     __shared__ double red[40];
     __shared__ int s_go;
@@ -2692,6 +2692,45 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
         if (b == 0 && tid == 0) { __threadfence(); st_release_u32(flags + 2, 1u); }
         return;
     }
+    // ares > 0 (with xs, 32 lanes per row): the CTA's rows of A stay in shared memory for the
+    // whole cycle -- the row assignment of phase A is static (warp w of CTA b: rows w W + b,
+    // + 16 W, ...), so warp w copies its rows' values and (16-bit) columns once, in CSR order,
+    // behind the staged u; per iteration phase A then reads A from shared memory instead of
+    // 4 dependent L2 round trips per long row (c2: 24 MB of CSR = 162 KB per SM).  Same
+    // entries in the same order per lane: bitwise the plain phase.
+    //   layout after s_xs[n]: values [ares] | columns uint16 [ares] | row lengths int [PC_WARPS K]
+    double* s_av = s_red + 2 * PC_WARPS * 32 + n;
+    unsigned short* s_ac = reinterpret_cast<unsigned short*>(s_av + ares);
+    int* s_rl = reinterpret_cast<int*>(s_ac + ((ares + 3) & ~3));
+    __shared__ int s_woff[PC_WARPS + 1];
+    const int rstep = W * PC_WARPS;  // rows between two rows of the same warp
+    if (ares > 0) {
+        if (tid < PC_WARPS) {
+            int tot = 0, k = 0;
+            for (int64_t r = (int64_t)tid * W + b; r < n; r += rstep, k++) {
+                const int len = (int)(__ldg(rowptr + r + 1) - __ldg(rowptr + r));
+                s_rl[k * PC_WARPS + tid] = len;
+                tot += len;
+            }
+            s_woff[tid + 1] = tot;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            s_woff[0] = 0;
+            for (int w = 0; w < PC_WARPS; w++) s_woff[w + 1] += s_woff[w];
+        }
+        __syncthreads();
+        int o = s_woff[warp];
+        for (int64_t r = (int64_t)warp * W + b; r < n; r += rstep) {
+            const int64_t q0 = (int64_t)__ldg(rowptr + r), q1 = (int64_t)__ldg(rowptr + r + 1);
+            for (int64_t q = q0 + lane; q < q1; q += 32) {
+                s_av[o + (int)(q - q0)] = __ldg(val + q);
+                s_ac[o + (int)(q - q0)] = (unsigned short)__ldg(col + q);
+            }
+            o += (int)(q1 - q0);
+        }
+        __syncthreads();
+    }
     for (int p = 1; p <= m; p++) {
         const bool drain = (p == m);
         const double* u = V + (int64_t)p * ld;
@@ -2715,6 +2754,27 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
                 for (int64_t i = tid; i < n; i += PC_THREADS) s_xs[i] = __ldcg(u + i);
                 __syncthreads();
             }
+            if (ares > 0) {  // A resident in shared memory (lpr = 32: one row per warp at a time)
+                int o = s_woff[warp], k = 0;
+                for (int64_t r = (int64_t)warp * W + b; r < n; r += rstep, k++) {
+                    const int len = s_rl[k * PC_WARPS + warp];
+                    double sum = 0.0;
+                    int j = lane;
+                    for (; j + (PC_XS_UNROLL - 1) * 32 < len; j += PC_XS_UNROLL * 32) {
+                        int cu[PC_XS_UNROLL];
+                        double vu[PC_XS_UNROLL];
+#pragma unroll
+                        for (int t = 0; t < PC_XS_UNROLL; t++) { cu[t] = s_ac[o + j + t * 32]; vu[t] = s_av[o + j + t * 32]; }
+#pragma unroll
+                        for (int t = 0; t < PC_XS_UNROLL; t++) sum = fma(vu[t], s_xs[cu[t]], sum);
+                    }
+                    for (; j < len; j += 32) sum = fma(s_av[o + j], s_xs[s_ac[o + j]], sum);
+#pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(FULL_MASK, sum, off);
+                    if (lane == 0) z[r] = sum;
+                    o += len;
+                }
+            } else
             // row groups dealt round-robin over the CTAs first (warp w of CTA b takes group
             // w W + b): consecutive rows -- similar lengths -- land on different SMs
 #if PC_ROW_INTERLEAVE
@@ -2995,9 +3055,19 @@ int64_t pcycle_xs_max() { return 8192; }  // staged u: <= 64 KB of shared memory
 template <typename IT, typename PT>
 static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                              int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                             unsigned long long* prof, double* part, int xs, int ntri) {
+                             unsigned long long* prof, double* part, int xs, int ntri, int* ares_io) {
     auto fn = pcycle_kernel<IT, PT>;
-    const size_t smem = pcycle_smem(d.m) + (xs ? (size_t)n * sizeof(double) : 0);
+    int ares = ares_io ? *ares_io : 0;
+    // resident A (xs only): values + 16-bit columns of the CTA's rows + its warps' row lengths
+    const int W = pcycle_worker_ctas(grid, gs, ntri);
+    const size_t base = pcycle_smem(d.m) + (xs ? (size_t)n * sizeof(double) : 0);
+    auto ares_bytes = [&](int a) {
+        const int64_t K = (n + (int64_t)W * PC_WARPS - 1) / ((int64_t)W * PC_WARPS);
+        return (size_t)a * 8 + (size_t)((a + 3) & ~3) * 2 + (size_t)(PC_WARPS * K) * sizeof(int);
+    };
+    if (!xs || a.lpr != 32 || n > 65535 || ares <= 0 || base + ares_bytes(ares) > 227 * 1024) ares = 0;
+    const size_t smem = base + (ares ? ares_bytes(ares) : 0);
+    if (ares_io) *ares_io = ares;  // what the launch uses
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -3011,21 +3081,27 @@ static cudaError_t pcycle_go(const Dev& d, const SpmvArgs& a, double* V, int64_t
     int lpr = a.lpr > 0 ? a.lpr : 4;
     SellDev<IT> sell = sell_dev<IT>(a);
     void* args[] = {&dd, &n, &m, &gs, (void*)&rp, (void*)&ci, (void*)&va, &lpr, &V, &ld, &z, &flags, &counter, &prof,
-                    &part, (void*)&sell, &xs, &ntri};
+                    &part, (void*)&sell, &xs, &ntri, &ares};
     return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(PC_THREADS), args, smem, s);
 }
 
 int pcycle_max_grid(int num_sms) { return num_sms; }
 
+int pcycle_worker_ctas(int grid, int gs, int ntri) {
+    const int nt = (gs == 2 && grid >= 3) ? std::max(1, std::min(ntri, grid - 2)) : 0;
+    return grid > 1 ? grid - 1 - nt : 1;
+}
+static_assert(PCYCLE_WARPS == PC_WARPS, "igs_internal.cuh: PCYCLE_WARPS");
+
 cudaError_t launch_pcycle(const Dev& d, const SpmvArgs& a, double* V, int64_t ld, double* z, int64_t n,
                           int m, int gs, unsigned* flags, unsigned* counter, int grid, cudaStream_t s,
-                          unsigned long long* prof, double* part, int xs, int ntri) {
+                          unsigned long long* prof, double* part, int xs, int ntri, int* ares) {
     if (a.idx64) {
-        if (a.ptr64) return pcycle_go<int64_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
-        return pcycle_go<int64_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
+        if (a.ptr64) return pcycle_go<int64_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri, ares);
+        return pcycle_go<int64_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri, ares);
     }
-    if (a.ptr64) return pcycle_go<int32_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
-    return pcycle_go<int32_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri);
+    if (a.ptr64) return pcycle_go<int32_t, int64_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri, ares);
+    return pcycle_go<int32_t, int32_t>(d, a, V, ld, z, n, m, gs, flags, counter, grid, s, prof, part, xs, ntri, ares);
 }
 
 }  // namespace igs

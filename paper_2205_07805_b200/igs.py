@@ -304,7 +304,7 @@ def igs_plan_sell(n, rowptr, local_col, values, want_diag=True, bnd_rows=()):
 
 # ------------------------------------------------------------------------- convenience
 INFO_KEYS = ["xchg", "nranks", "n_ghost", "n_send", "n_peers", "n_bnd", "graph_launches", "pcycle_launches",
-             "sell", "csr_compact", "sell_diag_slices", "sell_walk", "spmv_bytes"]
+             "sell", "csr_compact", "sell_diag_slices", "sell_walk", "spmv_bytes", "pcycle_ares"]
 
 
 def igs_info(ctx: int) -> dict:

@@ -810,8 +810,9 @@ def test_persistent_long_rows(P, case, gs, monkeypatch):
         A, bvec = _ragged_long_rows(); k = 150
     b = torch.from_numpy(bvec).cuda()
     outs = {}
-    for tag, env in (("xs", {"IGS_PC_XSTAGE": "1"}), ("l2", {"IGS_PC_XSTAGE": "0"}), ("pk", {"IGS_PERSIST": "0"})):
-        for key in ("IGS_PC_XSTAGE", "IGS_PERSIST"):
+    for tag, env in (("xs", {"IGS_PC_XSTAGE": "1"}), ("l2", {"IGS_PC_XSTAGE": "0"}), ("pk", {"IGS_PERSIST": "0"}),
+                     ("xs_l2a", {"IGS_PC_XSTAGE": "1", "IGS_PC_ARES": "0"})):
+        for key in ("IGS_PC_XSTAGE", "IGS_PERSIST", "IGS_PC_ARES"):
             monkeypatch.delenv(key, raising=False)
         for key, val in env.items():
             monkeypatch.setenv(key, val)
@@ -819,11 +820,18 @@ def test_persistent_long_rows(P, case, gs, monkeypatch):
         s.set_timing(1)
         outs[tag] = s.solve(b, k=k, gs_iters=gs, want_loo=True)
         assert (s.kernel_stats()["persist"]["launches"] > 0) == (tag != "pk")
+        # with u staged, the CTAs' rows of A stay in shared memory for the cycle when they fit
+        # (c2: yes; IGS_PC_ARES=0: A re-read from L2 every iteration)
+        ares = s.info()["pcycle_ares"]
+        assert (ares > 0) == (tag == "xs") or (case == "ragged" and tag == "xs"), (tag, ares)
         s.set_timing(0)
         s.close()
     r, u, pk = outs["xs"], outs["l2"], outs["pk"]
     assert r["H"].tobytes() == u["H"].tobytes()
     assert r["x"].cpu().numpy().tobytes() == u["x"].cpu().numpy().tobytes()
+    assert r["H"].tobytes() == outs["xs_l2a"]["H"].tobytes()
+    assert r["x"].cpu().numpy().tobytes() == outs["xs_l2a"]["x"].cpu().numpy().tobytes()
+    assert np.asarray(r["res_hist"]).tobytes() == np.asarray(outs["xs_l2a"]["res_hist"]).tobytes()
     assert r["iters"] == pk["iters"] and r["term"] == pk["term"] and r["reductions"] == pk["reductions"]
     o = oracle.gmres(A, bvec, k, variant=VARIANT[gs], dot_block=4096, want_V=True)
     d, c = _compare_cols(r["H"], o["H"], o["res_hist"])
