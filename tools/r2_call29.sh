@@ -28,7 +28,7 @@ run() {  # cfg k kernel p skip
   ncu --metrics $M --clock-control none -k regex:$3 -s $5 -c 1 --csv \
       --log-file gpurun_out/c29_tr_${3}_${1}_p${4}.csv python tools/traffic_run.py --config $1 --k $2 > /dev/null 2>&1
 }
-for p in 10 50; do run c4 100 bdot_tma_kernel $p $((p-1)); run c4 100 update_kernel $p $((p+1)); done
+for p in 10 50; do run c4 100 bdot_tma_kernel $p $((p-8)); run c4 100 update_kernel $p $((p+1)); done  # (the block dot below p = 8 is bdot_sw_kernel: the tile kernel's first launch is p = 8)
 run c4 100 bdot_sw_kernel 100 4; run c4 100 update_kernel 100 101
 for p in 10 50 99; do run c4 100 spmv_sell_diag_kernel $p $((p+1)); done
 echo "traffic rc=$?"
