@@ -1377,16 +1377,19 @@ __global__ void __launch_bounds__(UD_THREADS)
 // p + 2 dots from the same shared tile (8 columns per butterfly, R / 32 rows per lane).  One HBM
 // read of V_p and no L2 re-read; p <= update_dot_tma_max_p() (two tiles in 227 KB).
 constexpr int UT_CONS = 8, UT_THREADS = (UT_CONS + 1) * 32;
+#ifndef UT_RSTEP
+#define UT_RSTEP 32   // 128: only 256- or 128-row tiles (A/B build)
+#endif
 
-// tile rows R (128 or 256) x (p V columns + u + z), two tiles in flight
+// tile rows R (128 .. 256 in steps of UT_RSTEP) x (p V columns + u + z), two tiles in flight
 size_t update_dot_tma_smem(int p, int R) {
     return (size_t)2 * (p + 2) * R * sizeof(double) +
            (size_t)(2 * p + 1 + 2 * R + UT_CONS * (p + 2)) * sizeof(double) + 4 * sizeof(uint64_t);
 }
 
-int update_dot_tma_rows(int p) {  // 0: does not fit
-    if (update_dot_tma_smem(p, 256) <= 227 * 1024) return 256;
-    if (update_dot_tma_smem(p, 128) <= 227 * 1024) return 128;
+int update_dot_tma_rows(int p) {  // the tallest tile (multiple of 32 rows) of which two fit; 0: none
+    for (int R = 256; R >= 128; R -= UT_RSTEP)
+        if (update_dot_tma_smem(p, R) <= 227 * 1024) return R;
     return 0;
 }
 

@@ -950,7 +950,7 @@ def test_two_reduce_fused_update_dot(P, cfg, N, monkeypatch):
 def test_two_reduce_fused_variants(P, l2mb, monkeypatch):
     """Both fused update + dot kernels of Alg. 2 two-reduce on every iteration of a
     100-column cycle: IGS_TWO_FUSED_L2_MB=0 forces the shared-memory tile variant (tile rows
-    256 while p <= 52, then 128; ragged last tile), 1000 the L2 re-read variant; both within
+    256 while p <= 52, then 224, 192, 160, 128 as p grows; ragged last tile), 1000 the L2 re-read variant; both within
     the parity bar of the unfused path (IGS_TWO_FUSED=0) and of each other."""
     import torch
     prob = W.config("c4", N=47)  # n = 103823: ragged, above the fusion threshold
