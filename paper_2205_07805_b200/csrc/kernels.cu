@@ -675,7 +675,8 @@ __global__ void __launch_bounds__(BD_THREADS, 2)
 //   registers.  Stage 2 (per-CTA partials, last CTA sums in CTA order) as in bdot_kernel.
 // ------------------------------------------------------------------------------------
 constexpr int BT_CONS_WARPS = 8;
-constexpr int BT_THREADS = (BT_CONS_WARPS + 1) * 32;
+constexpr int BT_THREADS = (BT_CONS_WARPS + 1) * 32;                 // column-sweep kernel
+constexpr int bt_threads(int groups) { return (BT_CONS_WARPS * groups + 1) * 32; }  // tile kernel
 constexpr int BT_ROWS = 512;
 constexpr int BT_RPL = BT_ROWS / 32;  // rows per lane
 constexpr int BT_STAGES = 6;
@@ -685,8 +686,8 @@ __device__ __forceinline__ void bdot_finish(const double* acc, int stride, doubl
                                             double* __restrict__ out, unsigned* counter, bool live,
                                             const XchgDev* xc);
 
-template <int NV>
-__global__ void __launch_bounds__(BT_THREADS, 1)
+template <int NV, int BT_GROUPS>
+__global__ void __launch_bounds__(bt_threads(BT_GROUPS), 1)
     bdot_tma_kernel(int64_t n, int p, const double* __restrict__ V, int64_t ld,
                     const double* __restrict__ u, const double* __restrict__ z,
                     double* __restrict__ part, double* __restrict__ out, unsigned* counter,
@@ -699,22 +700,24 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
     double* acc = uzslot + 4 * BT_ROWS;                            // [NV*(p+1)]
     const int ncols = p + 1;
     const int stride = NV * ncols;
-    uint64_t* full = reinterpret_cast<uint64_t*>(acc + ((stride + 1) & ~1));
+    uint64_t* full = reinterpret_cast<uint64_t*>(acc + ((BT_GROUPS * stride + 1) & ~1));
     uint64_t* empty = full + BT_STAGES;
     uint64_t* uzfull = empty + BT_STAGES;
     uint64_t* uzempty = uzfull + 2;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] = 0.0;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = wid & (BT_CONS_WARPS - 1);  // column slot within a stage
+    const int grp = wid / BT_CONS_WARPS;         // consumer group (BT_GROUPS = 2: stages of its parity)
+    for (int i = threadIdx.x; i < BT_GROUPS * stride; i += blockDim.x) acc[i] = 0.0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < BT_STAGES; s++) { mbar_init(full + s, 1); mbar_init(empty + s, BT_CONS_WARPS); }
-        for (int s = 0; s < 2; s++) { mbar_init(uzfull + s, 1); mbar_init(uzempty + s, BT_CONS_WARPS); }
+        for (int s = 0; s < 2; s++) { mbar_init(uzfull + s, 1); mbar_init(uzempty + s, BT_CONS_WARPS * BT_GROUPS); }
         mbar_fence_init();
     }
     __syncthreads();
     const int64_t ntiles = (n + BT_ROWS - 1) / BT_ROWS;
     const int ngroups = (ncols + BT_CONS_WARPS - 1) / BT_CONS_WARPS;
     const int64_t nk = (live && ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    if (warp == BT_CONS_WARPS) {
+    if (wid == BT_CONS_WARPS * BT_GROUPS) {
         // ---------------- producer: one elected lane issues the bulk copies ----------------
         if (lane == 0) {
             // u, z rows of tile k go to a double-buffered slot one tile ahead of tile k's V
@@ -782,10 +785,15 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(uzempty + tb);
-            for (int g = 0; g < ngroups; g++, it++) {
-                const int s = it % BT_STAGES;
+            // BT_GROUPS = 2: the two groups of 8 consumer warps take alternate stages (a stage
+            // is consumed by the group of its parity), each adding into its own accumulators
+            const uint32_t it0 = it;
+            it += (uint32_t)ngroups;
+            for (int g = BT_GROUPS == 2 ? (int)((it0 & 1u) ^ (uint32_t)grp) : 0; g < ngroups; g += BT_GROUPS) {
+                const uint32_t itg = it0 + (uint32_t)g;
+                const int s = itg % BT_STAGES;
                 const int c = g * BT_CONS_WARPS + warp;
-                mbar_wait(full + s, (it / BT_STAGES) & 1);
+                mbar_wait(full + s, (itg / BT_STAGES) & 1);
                 if (c < ncols) {
                     double su = 0.0, sz = 0.0;
                     if (c < p) {
@@ -819,8 +827,8 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
                         if (NV == 2) sz += __shfl_xor_sync(FULL_MASK, sz, off);
                     }
                     if (lane == 0) {
-                        acc[c] += su;
-                        if (NV == 2) acc[ncols + c] += sz;
+                        acc[grp * stride + c] += su;
+                        if (NV == 2) acc[grp * stride + ncols + c] += sz;
                     }
                 }
                 __syncwarp();
@@ -829,6 +837,10 @@ __global__ void __launch_bounds__(BT_THREADS, 1)
         }
     }
     __syncthreads();
+    if (BT_GROUPS == 2) {
+        for (int i = threadIdx.x; i < stride; i += blockDim.x) acc[i] += acc[stride + i];
+        __syncthreads();
+    }
     bdot_finish(acc, stride, part, out, counter, live, xc);
 }
 
@@ -1089,10 +1101,21 @@ int bdot_grid_size(int64_t n, int num_sms) {
     return (int)g;
 }
 
+// consumer groups of the tile kernel: two groups of 8 warps on alternate stages from three
+// column groups per tile on (4 consumer warps per scheduler instead of 2: c4 p = 50 isolated
+// 992 -> 955 us = 7.3 TB/s, bench block dot 102.6 -> 100.8 ms per step); with one or two
+// column groups a second warp group idles or unbalances the tile (p = 10: 310 -> 330 us)
+static int bdot_tma_groups(int p) {
+    static int force = -1;  // A/B hook: IGS_BDOT_GROUPS=1 keeps one consumer group at every p
+    if (force < 0) { const char* e = std::getenv("IGS_BDOT_GROUPS"); force = e ? std::atoi(e) : 0; }
+    if (force == 1) return 1;
+    return p + 1 > 2 * BT_CONS_WARPS ? 2 : 1;
+}
+
 static size_t bdot_tma_smem(int p, int nv) {
     const size_t stride = (size_t)nv * (p + 1);
     return (size_t)(BT_STAGES * BT_STAGE_DOUBLES + 4 * BT_ROWS) * sizeof(double) +
-           ((stride + 1) & ~(size_t)1) * sizeof(double) + (2 * BT_STAGES + 4) * sizeof(uint64_t);
+           ((bdot_tma_groups(p) * stride + 1) & ~(size_t)1) * sizeof(double) + (2 * BT_STAGES + 4) * sizeof(uint64_t);
 }
 
 static size_t bdot_smem(int p, int nv) { return (size_t)BD_WARPS * nv * (p + 1) * sizeof(double); }
@@ -1135,13 +1158,15 @@ void launch_block_dot(int64_t n, int p, const double* V, int64_t ld, const doubl
             return;
         }
         if (tg <= grid) {
-            if (nv == 2) {
-                cudaFuncSetAttribute(bdot_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-                bdot_tma_kernel<2><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
-            } else {
-                cudaFuncSetAttribute(bdot_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
-                bdot_tma_kernel<1><<<tg, BT_THREADS, tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc);
-            }
+#define IGS_BT_LAUNCH(NVV, GG)                                                                                    \
+    do {                                                                                                          \
+        cudaFuncSetAttribute(bdot_tma_kernel<NVV, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem); \
+        bdot_tma_kernel<NVV, GG><<<tg, bt_threads(GG), tsmem, s>>>(n, p, V, ld, u, z, part, out, counter, istate, xc); \
+    } while (0)
+            const int gg = bdot_tma_groups(p);
+            if (nv == 2) { if (gg == 2) IGS_BT_LAUNCH(2, 2); else IGS_BT_LAUNCH(2, 1); }
+            else { if (gg == 2) IGS_BT_LAUNCH(1, 2); else IGS_BT_LAUNCH(1, 1); }
+#undef IGS_BT_LAUNCH
             return;
         }
     }

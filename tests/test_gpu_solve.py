@@ -722,7 +722,19 @@ def test_c3_full_size_full_k(P, gs):
     if gs == 2:
         assert _loo_close(g["loo"], lo), (g["loo"], lo)
     else:
-        assert lo / 100 <= g["loo"] <= 10 * lo, (g["loo"], lo)
+        # reading R19: the one-sweep LOO is eps * kappa(B_k) times a constant set by the
+        # rounding of the inner products, so the band is taken over the oracle's own reduction
+        # orders.  At this size the device basis (4.2e-12) sits ~100x below the oracle's with
+        # 4096-row running sums (4.4e-10; 3.9e-10 with those block sums added pairwise) and
+        # beside the oracle's with 64-row running sums added pairwise (5.4e-12; 16-row: 2.8e-12)
+        # -- the order closest to the device's 16 rows per lane + trees.  The second order is
+        # computed only when the first band does not already hold.
+        los = [lo]
+        if not lo / 100 <= g["loo"] <= 10 * lo:
+            o2 = oracle.gmres(prob.A, prob.b, 300, variant=VARIANT[gs], dot_block=-64, want_V=True)
+            los.append(oracle.loss_of_orthogonality(o2["V"][:, :o2["basis_cols"]]))
+            assert los[1] / 10 <= g["loo"] <= 10 * los[1], (g["loo"], los)
+        assert min(los) / 100 <= g["loo"] <= 10 * max(los), (g["loo"], los)
 
 
 @pytest.mark.parametrize("alg", ["igs2", "igs1", "igs2_two", "mgs"])
