@@ -3,7 +3,7 @@ out=gpurun_out/sweep.jsonl
 : > $out
 for c in c1 c2 c3 c4; do
   for a in igs1 igs2 igs2_two mgs; do
-    reps=3; [ $c = c4 ] && reps=2
+    reps=3; [ $c = c4 ] && reps=4   # (2 solves after one warm-up still sit on the process's first, slower solves)
     timeout 600 python tools/bench_configs.py --config $c --alg $a --reps $reps 2>/dev/null | tail -1 >> $out
   done
 done
