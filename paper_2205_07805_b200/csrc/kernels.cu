@@ -1101,15 +1101,17 @@ int bdot_grid_size(int64_t n, int num_sms) {
     return (int)g;
 }
 
-// consumer groups of the tile kernel: two groups of 8 warps on alternate stages from three
-// column groups per tile on (4 consumer warps per scheduler instead of 2: c4 p = 50 isolated
-// 992 -> 955 us = 7.3 TB/s, bench block dot 102.6 -> 100.8 ms per step); with one or two
-// column groups a second warp group idles or unbalances the tile (p = 10: 310 -> 330 us)
+// consumer groups of the tile kernel: two groups of 8 warps on alternate stages from four
+// column groups per tile on (p >= 24; 4 consumer warps per scheduler instead of 2: c4 p = 50
+// isolated 992 -> 955 us = 7.3 TB/s, bench block dot 102.6 -> 100.8 ms per step).  With fewer
+// column groups the second warp group idles or unbalances the tile (p = 10: 310 -> 330 us;
+// p = 16 / 20: 393 / 434 vs 397 / 441 us; p = 24 / 32: 530 / 665 -> 509 / 631 us,
+// profiles/r2/c42)
 static int bdot_tma_groups(int p) {
     static int force = -1;  // A/B hook: IGS_BDOT_GROUPS=1 keeps one consumer group at every p
     if (force < 0) { const char* e = std::getenv("IGS_BDOT_GROUPS"); force = e ? std::atoi(e) : 0; }
     if (force == 1) return 1;
-    return p + 1 > 2 * BT_CONS_WARPS ? 2 : 1;
+    return p + 1 > 3 * BT_CONS_WARPS ? 2 : 1;
 }
 
 static size_t bdot_tma_smem(int p, int nv) {
